@@ -1,0 +1,369 @@
+"""Benchmark of the unified HDR LPA operator (BASELINE.json metric).
+
+Metric: HDR frames/s (and output Mpixel/s) reconstructing synthetic 3-sensor
+4-Mpixel (2400x1700) raw frames.  Workloads (BASELINE.json configs):
+  cfg2 (default, configs[1]): aligned rig, order-1 LPA, fixed window
+  cfg3 (configs[2]): sub-pixel misaligned rig, order-2 LPA, ICI (J=4)
+  cfg4 (configs[3]): cfg3 reconstructed to the 2x upsampled 4800x3400 grid
+A step = one reconstruction of one frame (all three sensors -> RGB).
+
+Our arm:  python bench.py [--gpus N --steps K --warmup W --workload cfg2]
+Reference arm:  python bench.py --impl reference ...  (the CPU restatement of
+the reference path, oracle/lpa_oracle.c, on all host cores; rank 0 only).
+
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Inputs: 8 distinct pre-simulated frames per rank cycled
+(8 x 24.5 MB = 196 MB > 126 MB L2, so every step reads its raw frame from HBM).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+W_IN, H_IN = 2400, 1700
+N_DISTINCT = 8
+
+WORKLOADS = {
+    "cfg1": dict(rig="aligned", order=0, J=1, out=(256, 256), size=(256, 256),
+                 desc="3-sensor 256x256 RGGB, order-0 LPA, fixed scale, identity alignment"),
+    "cfg2": dict(rig="aligned", order=1, J=1, out=(W_IN, H_IN), size=(W_IN, H_IN),
+                 desc="3-sensor 4-Mpixel 2400x1700 raw, order-1 LPA, full noise model, fixed window"),
+    "cfg3": dict(rig="misaligned", order=2, J=4, out=(W_IN, H_IN), size=(W_IN, H_IN),
+                 desc="3-sensor 4-Mpixel, sub-pixel affine misalignment, order-2 LPA, ICI J=4"),
+    "cfg4": dict(rig="misaligned", order=2, J=4, out=(2 * W_IN, 2 * H_IN), size=(W_IN, H_IN),
+                 desc="3-sensor 4-Mpixel to 2x upsampled 4800x3400 grid, order-2 LPA, ICI J=4"),
+}
+
+# algorithmic FLOP per inside-window sample per scale:
+# FP32 8 (offsets, window, weight) + FP64 3+(p-1)+p(p+1)+2p (basis + moments)
+FLOP64_PER_SAMPLE = {0: 0, 1: 20, 2: 62}
+FLOP32_PER_SAMPLE = {0: 12, 1: 8, 2: 8}
+
+
+def _params(wl):
+    import paper_1308_4908_b200 as hl
+
+    return hl.ReconstructionParams(order=wl["order"], scale=0.7, ici_scales=wl["J"])
+
+
+def _dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/hdrlpa_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines()]
+        except OSError:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+                for n, v in zip(names, r[3:7]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+REF_BAND_ROWS = {"cfg1": None, "cfg2": 400, "cfg3": 32, "cfg4": 32}
+_SIM_CACHE = {}
+
+
+def cpu_reference_frame_seconds(wl, threads, band_rows=None, seed=123):
+    """Time the CPU restatement of the reference path (oracle: frames_to_samples
+    + SampleIndex + per-pixel fits) on one frame, or on a band of output rows
+    with the sensor frames cropped to the rows that band can reach (so the
+    index build shrinks with it).  Returns (seconds, fraction of a frame,
+    sample description)."""
+    from oracle import oracle
+    from paper_1308_4908_b200 import simulate as sim
+
+    W, H = wl["size"]
+    key = (wl["rig"], W, H, seed)
+    if key not in _SIM_CACHE:
+        gt = sim.hdr_chart(W, H)
+        rig = sim.baseline_rig(wl["rig"], W, H, seed=seed)
+        _SIM_CACHE[key] = (rig, sim.simulate_rig(gt, rig))
+    rig, frames = _SIM_CACHE[key]
+    cals = rig.calibrations()
+    params = _params(wl)
+    out_w, out_h = wl["out"]
+    rows, frac = None, 1.0
+    if band_rows is not None and band_rows < out_h:
+        rows = (0, band_rows)
+        frac = band_rows / out_h
+        reach = band_rows * H / out_h + params.resolved_max_radius() + 24  # + rotation drift
+        keep = min(H, int(math.ceil(reach)))
+        frames = [type(f)(f.data[:keep], f.bit_depth, f.pattern) for f in frames]
+        cals = [type(c)(type(c.bias)(c.bias.data[:keep]),
+                        type(c.bias)(c.readout_variance.data[:keep]),
+                        type(c.bias)(c.nonuniformity.data[:keep])) for c in cals]
+    t0 = time.perf_counter()
+    oracle.reconstruct(frames, rig.sensors, cals, (out_w, out_h), params, ref_size=(W, H),
+                       threads=threads, rows=rows)
+    dt = time.perf_counter() - t0
+    what = "full frame" if rows is None else f"output rows 0-{rows[1]} of {out_h} (sensors cropped)"
+    desc = (f"{what} of {wl['desc']}: frames_to_samples + SampleIndex + per-pixel fits, "
+            f"{threads} threads")
+    return dt, frac, desc
+
+
+def run_reference(args, wl, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    threads = oracle.max_threads()
+    band = REF_BAND_ROWS[args.workload]
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, frac, desc = cpu_reference_frame_seconds(wl, threads, band_rows=band, seed=100 + i % 2)
+        if i >= args.warmup:
+            times.append(dt / frac)
+    sec = float(np.mean(times))
+    fps = 1.0 / sec
+    mpx = fps * wl["out"][0] * wl["out"][1] / 1e6
+    line = {
+        "impl": "reference", "metric": "HDR frames/s", "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "out": list(wl["out"])},
+        "mpix_per_s": mpx,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, wl, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1308_4908_b200 as hl
+    from paper_1308_4908_b200 import _native as N
+    from paper_1308_4908_b200 import simulate as sim
+    from paper_1308_4908_b200.engine import DeviceRig
+    from paper_1308_4908_b200.pipeline import FramePipeline
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W, H = wl["size"]
+    out_w, out_h = wl["out"]
+    params = _params(wl)
+    gt = sim.hdr_chart(W, H)
+    rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0)
+    cals = rigspec.calibrations()
+    frame_sets = [sim.simulate_rig_torch(gt, rigspec, dev, seed=1000 * rank + i)
+                  for i in range(N_DISTINCT)]
+    torch.cuda.synchronize()
+    rig = DeviceRig.from_device(frame_sets[0], rigspec.sensors, cals)
+    out = rig.allocate_outputs((out_w, out_h))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, flags=0):
+        rig.set_frames(frame_sets[i % N_DISTINCT])
+        rig.reconstruct((out_w, out_h), params, ref_size=(W, H), out=out, stream=stream,
+                        flags=flags)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, k):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(k):
+            fn(i)
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for i in range(args.warmup):
+        step(i)
+    with ClockSampler(local) as clocks:
+        ms = timed(step, args.steps)
+    clk = clocks.summary()
+    ms_step = ms / args.steps
+    fps = world * args.steps / (ms / 1e3)
+    mpx = fps * out_w * out_h / 1e6
+
+    # fast kernel alone (the dominant kernel), same stream, same inputs
+    for i in range(2):
+        step(i, flags=N.HDR_FLAG_FAST_ONLY)
+    ms_fast = timed(lambda i: step(i, flags=N.HDR_FLAG_FAST_ONLY), args.steps) / args.steps
+    slow_items = rig.slow_items((out_w, out_h))
+
+    # algorithmic work of one launch: inside-window samples of the accepted fits
+    cnt = rig.reconstruct((out_w, out_h), params, ref_size=(W, H), want_count=True,
+                          want_scale_idx=True)
+    n_inside = float(cnt["count"].to(torch.int64).sum().item())
+    p = wl["order"]
+    flop64 = n_inside * FLOP64_PER_SAMPLE[p]
+    flop32 = n_inside * FLOP32_PER_SAMPLE[p]
+    peak64 = ctypes_probe(N, stream)
+    if p == 0:
+        achieved = flop32 / (ms_fast * 1e-3)
+        bound, peak, peak_src = "fp32", 148 * 128 * 2 * (clk["sm_max_mhz"] or 1965.0) * 1e6, \
+            "nominal 148 SM x 128 FMA lanes x 2 x max SM clock (no measured FP32 peak)"
+    else:
+        achieved = flop64 / (ms_fast * 1e-3)
+        bound, peak, peak_src = "fp64", peak64, "measured in-run DFMA probe (hdr_fp64_peak_probe)"
+    in_bytes = sum(t.numel() * 2 for t in frame_sets[0])
+    out_bytes = out_w * out_h * 12
+    hbm_achieved = (in_bytes + out_bytes) / (ms_fast * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
+
+    # end to end through the public pipeline API: pinned host frames in, pinned RGB out
+    host_sets = [[t.cpu().pin_memory() for t in fs] for fs in frame_sets]
+    host_out = [torch.empty((out_h, out_w, 3), dtype=torch.float32).pin_memory()
+                for _ in range(2)]
+    pipe = FramePipeline(rigspec.sensors, cals, [tuple(t.shape) for t in frame_sets[0]],
+                         (out_w, out_h), params, ref_size=(W, H), device=dev)
+    for i in range(args.warmup):
+        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % 2])
+    pipe.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(pipe.s_in)
+    for i in range(args.steps):
+        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % 2])
+    pipe.s_in.wait_stream(pipe.s_out)
+    e1.record(pipe.s_in)
+    pipe.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    fps_e2e = world * args.steps / (ms_e2e / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle
+
+        thr = oracle.max_threads()
+        dt, frac, desc = cpu_reference_frame_seconds(wl, thr, band_rows=REF_BAND_ROWS[args.workload])
+        cpu = {"value": frac / dt, "unit": "frames/s", "cores": thr, "kind": "port",
+               "sample": desc + f" (scaled x{1 / frac:.1f} to a frame)"}
+
+    if rank == 0:
+        line = {
+            "metric": "HDR frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "in": [W, H],
+                       "out": [out_w, out_h], "sensors": 3, "order": wl["order"],
+                       "ici_scales": wl["J"], "scale": 0.7,
+                       "l2": "inputs larger than L2: 8 distinct frames x 24.5 MB cycled",
+                       "parallelism": f"frame-parallel x{world}"},
+            "mpix_per_s": mpx,
+            "roofline": {"bound": bound, "achieved": achieved / 1e12, "peak": peak / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src, "kernel": "lpa_fast_kernel",
+                         "kernel_ms": ms_fast, "inside_samples_per_launch": n_inside,
+                         "flop64_per_launch": flop64, "flop32_per_launch": flop32,
+                         "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": peaks["hbm_gbs"],
+                                 "frac": hbm_achieved / peaks["hbm_gbs"],
+                                 "algorithmic_bytes": in_bytes + out_bytes}},
+            "slow_path_items": slow_items,
+            "cpu_baseline": cpu,
+            "e2e": {"value": fps_e2e, "unit": "frames/s", "h2d_bytes_per_step": pipe.h2d_bytes,
+                    "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": ms_e2e / args.steps},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_probe(N, stream):
+    import ctypes
+
+    v = ctypes.c_double()
+    N.check(N.lib().hdr_fp64_peak_probe(ctypes.byref(v), stream.cuda_stream), "fp64 probe")
+    return v.value
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    world, rank, local = _dist_init()
+    if args.impl == "reference":
+        run_reference(args, wl, world, rank)
+    else:
+        run_ours(args, wl, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

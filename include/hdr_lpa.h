@@ -1,0 +1,171 @@
+/*
+ * hdr_lpa.h -- C ABI of the B200-native unified HDR LPA operator.
+ *
+ * Plain C: device pointers, sizes and scalars only (no torch or CUDA types in
+ * the signatures; the CUDA stream is passed as `void *` = cudaStream_t).
+ *
+ * Each entry point replaces one reference interface of hdrfuse (paths are
+ * relative to the reference package root pkg/src/hdrfuse/):
+ *
+ *   hdr_lpa_reconstruct   <- lpa.py:411-433 reconstruct_frame (through
+ *                            lpa.py:379-408 reconstruct_channel,
+ *                            lpa.py:322-376 _evaluate_index and the numba
+ *                            kernel _kernels.py:203-300 lpa_evaluate), fused
+ *                            with radiometry.py:303-349 frames_to_samples and
+ *                            radiometry.py:208-242 SampleIndex: the raw
+ *                            frames are consumed directly, no sample list or
+ *                            index is ever materialised.
+ *   hdr_saturation_mask   <- radiometry.py:298-300 saturation_mask (+ the
+ *                            defective-pixel exclusion of radiometry.py:316-317)
+ *   hdr_lpa_workspace_bytes  workspace sizing (the reference allocates its
+ *                            scratch per query chunk, _kernels.py:251-256)
+ *   hdr_lpa_status_string    error text; the Python layer maps codes to the
+ *                            reference's exception types (ValueError,
+ *                            ConfigurationError, ShapeMismatchError)
+ *
+ * Ownership: the caller owns every buffer (inputs read-only, outputs written
+ * in place, like lpa.py:343-345).  Calls are stream-ordered and reentrant per
+ * stream; there are no hidden allocations on the hot path.
+ *
+ * Per-pixel numeric failure never returns an error: the pixel becomes NaN
+ * (_kernels.py:297-300), exactly as in the reference.
+ */
+#ifndef HDR_LPA_H
+#define HDR_LPA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDR_LPA_MAX_SENSORS 8
+#define HDR_LPA_MAX_SCALES 8
+#define HDR_LPA_ABI_VERSION 1
+
+/* status codes */
+#define HDR_OK 0
+#define HDR_ERR_ARG 1        /* invalid argument / parameter  -> ValueError          */
+#define HDR_ERR_CONFIG 2     /* non-positive g*t*a*n etc.     -> ConfigurationError  */
+#define HDR_ERR_SHAPE 3      /* inconsistent sizes            -> ShapeMismatchError  */
+#define HDR_ERR_WORKSPACE 4  /* workspace too small                                  */
+#define HDR_ERR_CUDA 5       /* CUDA launch / runtime error                          */
+
+/* Weight modes (ReconstructionParams.weight_mode, lpa.py:54-61) */
+#define HDR_WEIGHT_VARIANCE 0
+#define HDR_WEIGHT_SIGMA 1
+
+/* HdrParams.flags: diagnostics only.  FAST_ONLY skips the exact slow path
+ * (its work items stay unprocessed, their outputs unwritten); used by the
+ * bench to time the fast kernel on its own. */
+#define HDR_FLAG_FAST_ONLY 1
+
+/* Outcome plane codes (optional diagnostics): order*16 + radius-step of the
+ * accepted fit (radius step 0 = base radius), or HDR_OUTCOME_NAN. */
+#define HDR_OUTCOME_NAN 0xFF
+
+/*
+ * One sensor: its raw frame on the device plus the SensorConfig
+ * (radiometry.py:35-92) and NoiseCalibration (radiometry.py:95-136) fields.
+ * Calibration entries are scalars unless the matching plane pointer is
+ * non-NULL (device, float64, width*height row-major), mirroring the rig
+ * schema's "scalar or PFM" noise entries (rig.py:67-95).
+ */
+typedef struct HdrSensor {
+    const uint16_t *raw;        /* device, height rows of `pitch` elements */
+    int width, height, pitch;
+    int saturation_level;       /* keep <=> raw < saturation_level */
+    int tile[4];                /* ColorChannel (R=0,G=1,B=2) at [(y%2)*2 + x%2] */
+    double exposure_time;       /* t  (s)            */
+    double gain;                /* g  (DV/e)         */
+    double exposure_scaling;    /* n  in (0, 1]      */
+    double transform[6];        /* 2x3 row-major: sensor (x, y) -> reference */
+    double bias;                /* b     (DV)   */
+    double readout_variance;    /* Var[r] (DV^2) */
+    double nonuniformity;       /* a            */
+    const double *bias_plane;       /* nullable */
+    const double *readvar_plane;    /* nullable */
+    const double *nonuni_plane;     /* nullable */
+    const uint8_t *defective;       /* nullable, width*height, 1 = discard */
+} HdrSensor;
+
+/*
+ * ReconstructionParams (lpa.py:40-74) resolved per channel, plus the ICI
+ * extension (no reference counterpart).
+ *   scale[c][k]  : window scale h (px^2) of channel c at ICI scale k
+ *                  (k = 0 is ReconstructionParams.channel_scale(c)).
+ *   n_scales == 1: fixed-scale LPA (the reference's behaviour).
+ */
+typedef struct HdrParams {
+    int order;                  /* 0, 1, 2 */
+    int weight_mode;            /* HDR_WEIGHT_* */
+    int n_scales;               /* 1..HDR_LPA_MAX_SCALES */
+    int flags;                  /* HDR_FLAG_* (0 for normal operation) */
+    double scale[3][HDR_LPA_MAX_SCALES];
+    double max_radius;          /* resolved_max_radius() (lpa.py:71-74) */
+    double cond_threshold;      /* 1e8 default */
+    double ici_gamma;           /* confidence-interval width factor */
+} HdrParams;
+
+/* Outputs: device pointers; only rgb is required. */
+typedef struct HdrOutputs {
+    float *rgb;                 /* out_h*out_w*3, HWC, max(val,0) as float32, NaN = no data */
+    float *grad;                /* nullable: [3 channels][2 (gx, gy)][out_h][out_w], unclamped */
+    uint8_t *scale_idx;         /* nullable: [3][out_h][out_w] selected ICI scale index */
+    uint8_t *outcome;           /* nullable: [3][out_h][out_w] HDR_OUTCOME codes */
+    float *value;               /* nullable: [3][out_h][out_w] unclamped fitted constant term */
+    uint16_t *count;            /* nullable: [3][out_h][out_w] samples inside the accepted window
+                                   (selected ICI scale; 0 where NaN) */
+} HdrOutputs;
+
+/* Bytes of device workspace hdr_lpa_reconstruct needs for this output size. */
+int hdr_lpa_workspace_bytes(int out_w, int out_h, size_t *bytes);
+
+/*
+ * Reconstruct one HDR frame on the output grid (out_w x out_h) whose pixel
+ * centres are x_j = (j + 0.5) * ref_w / out_w - 0.5 in reference coordinates
+ * (lpa.py:213-224).  Row band: only output rows [row_begin, row_end) are
+ * computed (row_end <= 0 means out_h); outputs are still indexed over the
+ * full frame.  `workspace` is device memory of hdr_lpa_workspace_bytes().
+ */
+int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
+                        int out_w, int out_h, double ref_w, double ref_h,
+                        int row_begin, int row_end, const HdrOutputs *out,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Saturation (+ defective) mask of one sensor as bit-planes: bit (x % 32) of
+ * out_bits[y * words_per_row + x / 32] is set where the pixel is discarded.
+ * words_per_row >= ceil(width / 32).
+ */
+int hdr_saturation_mask(const HdrSensor *sensor, uint32_t *out_bits, int words_per_row,
+                        void *stream);
+
+/*
+ * Per-pixel radiance samples of one sensor (the columns frames_to_samples
+ * would produce, radiometry.py:303-336) as fp32 planes, exactly as the
+ * reconstruction kernel sees them: value[i] = f_hat, inv_den[i] = 1/sigma^2
+ * (weight_mode variance) or 1/sigma (sigma); inv_den == 0 marks a pixel that
+ * yields no sample (saturated or defective).
+ */
+int hdr_radiance_planes(const HdrSensor *sensor, int weight_mode, float *value, float *inv_den,
+                        void *stream);
+
+/* Number of (pixel, channel) items the last call on this workspace routed
+ * through the exact slow path (device value; reads it synchronously). */
+int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream);
+
+/*
+ * Measured float64 FMA throughput of the device (DFMA chains on every SM),
+ * the roofline denominator of the moment accumulation.  Writes FLOP/s.
+ */
+int hdr_fp64_peak_probe(double *flops_per_s, void *stream);
+
+const char *hdr_lpa_status_string(int status);
+int hdr_lpa_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDR_LPA_H */

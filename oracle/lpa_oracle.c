@@ -464,7 +464,7 @@ static double fit_variance(double qx, double qy, double h11, double h12, double 
 static void ladder_eval(double qx, double qy, double hinv, double r0, int order0,
                         double max_radius, double cond_threshold, const OIndex *ix,
                         int use_sigma, FitScratch *S, double *val, double *gx, double *gy,
-                        uint8_t *outcome) {
+                        uint8_t *outcome, uint16_t *count) {
     for (int order = order0; order >= 0; --order) {
         double r = r0;
         if (r > max_radius) r = max_radius;
@@ -481,6 +481,7 @@ static void ladder_eval(double qx, double qy, double hinv, double r0, int order0
                     *gy = NAN;
                 }
                 *outcome = (uint8_t)(order * 16 + (step < 15 ? step : 15));
+                *count = (uint16_t)(S->count < 65535 ? S->count : 65535);
                 return;
             }
             if (r >= max_radius * (1.0 - 1e-12)) break;
@@ -493,6 +494,7 @@ static void ladder_eval(double qx, double qy, double hinv, double r0, int order0
     *gx = NAN;
     *gy = NAN;
     *outcome = OUT_NAN;
+    *count = 0;
 }
 
 /*
@@ -508,7 +510,8 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
                                int order, int n_scales, const double *hinv, const double *rk,
                                double max_radius, double cond_threshold, int use_sigma,
                                double gamma, int n_threads, double *val, double *gx,
-                               double *gy, uint8_t *outcome, uint8_t *scale_idx) {
+                               double *gy, uint8_t *outcome, uint8_t *scale_idx,
+                               uint16_t *count) {
     OIndex ix;
     build_index(sensors, n_sensors, channel, &ix);
     int64_t m = (int64_t)out_w * out_h;
@@ -517,6 +520,7 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
             val[i] = gx[i] = gy[i] = NAN;
             outcome[i] = OUT_NAN;
             scale_idx[i] = 0;
+            count[i] = 0;
         }
         free_index(&ix);
         return 0;
@@ -533,7 +537,7 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
             scale_idx[i] = 0;
             if (n_scales <= 1) {
                 ladder_eval(qx, qy, hinv[0], rk[0], order, max_radius, cond_threshold, &ix,
-                            use_sigma, &S, &val[i], &gx[i], &gy[i], &outcome[i]);
+                            use_sigma, &S, &val[i], &gx[i], &gy[i], &outcome[i], &count[i]);
                 continue;
             }
             /* ICI: k = 0 must succeed at the requested order, else reference ladder */
@@ -542,7 +546,7 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
                             use_sigma, &S);
             if (st != OK) {
                 ladder_eval(qx, qy, hinv[0], rk[0], order, max_radius, cond_threshold, &ix,
-                            use_sigma, &S, &val[i], &gx[i], &gy[i], &outcome[i]);
+                            use_sigma, &S, &val[i], &gx[i], &gy[i], &outcome[i], &count[i]);
                 continue;
             }
             double v = fit_variance(qx, qy, hinv[0], 0.0, hinv[0], r0, order, &ix, use_sigma, &S);
@@ -573,6 +577,7 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
             }
             outcome[i] = (uint8_t)(order * 16);
             scale_idx[i] = (uint8_t)kbest;
+            count[i] = (uint16_t)(best.count < 65535 ? best.count : 65535);
         }
     }
     free_index(&ix);

@@ -104,6 +104,7 @@ def _load():
             ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_int,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p,
         ]
         fn = _scipy_dsyevd()
         if fn:
@@ -249,12 +250,14 @@ def scale_ladder(h: float, n_scales: int, ratio: float):
 
 
 def reconstruct(frames, configs, cals, out_size, params, ref_size=None, threads=None,
-                channels=(0, 1, 2)):
+                channels=(0, 1, 2), rows=None):
     """Reference-semantics reconstruction on the CPU.
 
     Returns a dict: ``rgb`` (H, W, 3) float32 clamped like lpa.py:428 (NaN kept),
     ``val``/``gx``/``gy`` (3, H, W) float64 unclamped, ``outcome`` (3, H, W) u8
-    (order*16 + radius step, 0xFF = NaN), ``scale_idx`` (3, H, W) u8.
+    (order*16 + radius step, 0xFF = NaN), ``scale_idx`` (3, H, W) u8, ``count``
+    (3, H, W) u16 samples in the accepted window.  ``rows=(r0, r1)`` restricts
+    the evaluation to that band of output rows (the outputs cover the band).
     """
     lib = _load()
     arr, keep = make_sensors(frames, configs, cals)
@@ -262,6 +265,9 @@ def reconstruct(frames, configs, cals, out_size, params, ref_size=None, threads=
     if ref_size is None:
         ref_size = out_size
     xs, ys = grid_coordinates(out_size, ref_size)
+    if rows is not None:
+        ys = np.ascontiguousarray(ys[rows[0]:rows[1]])
+        out_h = len(ys)
     n_scales = int(getattr(params, "ici_scales", 1) or 1)
     ratio = float(getattr(params, "ici_ratio", math.sqrt(2.0)))
     gamma = float(getattr(params, "ici_gamma", 1.5))
@@ -273,26 +279,30 @@ def reconstruct(frames, configs, cals, out_size, params, ref_size=None, threads=
     gy = np.full((3, out_h, out_w), np.nan)
     outcome = np.full((3, out_h, out_w), 0xFF, np.uint8)
     sidx = np.zeros((3, out_h, out_w), np.uint8)
+    count = np.zeros((3, out_h, out_w), np.uint16)
     nthreads = int(threads) if threads else 0
     for c in channels:
         hs = scale_ladder(channel_scale(params, c), n_scales, ratio)
         hinv = np.array([1.0 / h for h in hs])
         rk = np.array([SUPPORT_SIGMAS * math.sqrt(h) for h in hs])
-        bufs = [np.empty(m) for _ in range(3)] + [np.empty(m, np.uint8) for _ in range(2)]
+        bufs = [np.empty(m) for _ in range(3)] + [np.empty(m, np.uint8) for _ in range(2)] + [
+            np.empty(m, np.uint16)]
         lib.oracle_reconstruct_channel(
             arr, len(frames), c, xs.ctypes.data, out_w, ys.ctypes.data, out_h,
             int(params.order), n_scales, hinv.ctypes.data, rk.ctypes.data,
             max_r, float(params.cond_threshold), use_sigma, gamma, nthreads,
             bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data,
-            bufs[3].ctypes.data, bufs[4].ctypes.data,
+            bufs[3].ctypes.data, bufs[4].ctypes.data, bufs[5].ctypes.data,
         )
         val[c] = bufs[0].reshape(out_h, out_w)
         gx[c] = bufs[1].reshape(out_h, out_w)
         gy[c] = bufs[2].reshape(out_h, out_w)
         outcome[c] = bufs[3].reshape(out_h, out_w)
         sidx[c] = bufs[4].reshape(out_h, out_w)
+        count[c] = bufs[5].reshape(out_h, out_w)
     del keep
     rgb = np.empty((out_h, out_w, 3), np.float32)
     for c in range(3):
         rgb[:, :, c] = np.maximum(val[c], 0.0).astype(np.float32)
-    return {"rgb": rgb, "val": val, "gx": gx, "gy": gy, "outcome": outcome, "scale_idx": sidx}
+    return {"rgb": rgb, "val": val, "gx": gx, "gy": gy, "outcome": outcome, "scale_idx": sidx,
+            "count": count}

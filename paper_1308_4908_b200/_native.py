@@ -1,0 +1,158 @@
+"""ctypes binding of the C ABI in include/hdr_lpa.h (libhdrlpa.so).
+
+The shared library is built in-tree for sm_100a by :func:`build` (called by
+``__graft_entry__.build()``) and loaded from ``paper_1308_4908_b200/``.  There
+is no fallback: if the library cannot be built or loaded, every entry point
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from pathlib import Path
+
+from .radiometry import ConfigurationError
+from .validation import ShapeMismatchError
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB_PATH = PKG / "libhdrlpa.so"
+SOURCES = [PKG / "csrc" / "hdr_lpa.cu", PKG / "csrc" / "lpa_device.cuh", ROOT / "include" / "hdr_lpa.h"]
+
+MAX_SENSORS = 8
+MAX_SCALES = 8
+
+HDR_OK, HDR_ERR_ARG, HDR_ERR_CONFIG, HDR_ERR_SHAPE, HDR_ERR_WORKSPACE, HDR_ERR_CUDA = range(6)
+HDR_WEIGHT_VARIANCE, HDR_WEIGHT_SIGMA = 0, 1
+HDR_OUTCOME_NAN = 0xFF
+HDR_FLAG_FAST_ONLY = 1
+
+EXPORTED = (
+    "hdr_lpa_workspace_bytes",
+    "hdr_lpa_reconstruct",
+    "hdr_saturation_mask",
+    "hdr_radiance_planes",
+    "hdr_lpa_slow_items",
+    "hdr_fp64_peak_probe",
+    "hdr_lpa_status_string",
+    "hdr_lpa_abi_version",
+)
+
+
+class HdrSensor(ctypes.Structure):
+    _fields_ = [
+        ("raw", ctypes.c_void_p),
+        ("width", ctypes.c_int),
+        ("height", ctypes.c_int),
+        ("pitch", ctypes.c_int),
+        ("saturation_level", ctypes.c_int),
+        ("tile", ctypes.c_int * 4),
+        ("exposure_time", ctypes.c_double),
+        ("gain", ctypes.c_double),
+        ("exposure_scaling", ctypes.c_double),
+        ("transform", ctypes.c_double * 6),
+        ("bias", ctypes.c_double),
+        ("readout_variance", ctypes.c_double),
+        ("nonuniformity", ctypes.c_double),
+        ("bias_plane", ctypes.c_void_p),
+        ("readvar_plane", ctypes.c_void_p),
+        ("nonuni_plane", ctypes.c_void_p),
+        ("defective", ctypes.c_void_p),
+    ]
+
+
+class HdrParams(ctypes.Structure):
+    _fields_ = [
+        ("order", ctypes.c_int),
+        ("weight_mode", ctypes.c_int),
+        ("n_scales", ctypes.c_int),
+        ("flags", ctypes.c_int),
+        ("scale", (ctypes.c_double * MAX_SCALES) * 3),
+        ("max_radius", ctypes.c_double),
+        ("cond_threshold", ctypes.c_double),
+        ("ici_gamma", ctypes.c_double),
+    ]
+
+
+class HdrOutputs(ctypes.Structure):
+    _fields_ = [
+        ("rgb", ctypes.c_void_p),
+        ("grad", ctypes.c_void_p),
+        ("scale_idx", ctypes.c_void_p),
+        ("outcome", ctypes.c_void_p),
+        ("value", ctypes.c_void_p),
+        ("count", ctypes.c_void_p),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def nvcc_command(out: Path):
+    return [
+        "nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+        "-Xcompiler", "-fPIC", "-shared", "-I", str(ROOT / "include"), "-o", str(out),
+        str(PKG / "csrc" / "hdr_lpa.cu"),
+    ]
+
+
+def build(force: bool = False) -> Path:
+    """Compile libhdrlpa.so for sm_100a in-tree (skipped when up to date)."""
+    if LIB_PATH.exists() and not force:
+        mtime = LIB_PATH.stat().st_mtime
+        if all(s.stat().st_mtime <= mtime for s in SOURCES):
+            return LIB_PATH
+    tmp = LIB_PATH.with_name(f"libhdrlpa.{os.getpid()}.tmp.so")
+    subprocess.run(nvcc_command(tmp), check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+def lib():
+    """The loaded library (built first if missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(str(build()))
+            L.hdr_lpa_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int,
+                                                  ctypes.POINTER(ctypes.c_size_t)]
+            L.hdr_lpa_reconstruct.argtypes = [
+                ctypes.POINTER(HdrSensor), ctypes.c_int, ctypes.POINTER(HdrParams),
+                ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                ctypes.c_int, ctypes.c_int, ctypes.POINTER(HdrOutputs),
+                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+            ]
+            L.hdr_saturation_mask.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_void_p,
+                                              ctypes.c_int, ctypes.c_void_p]
+            L.hdr_radiance_planes.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            L.hdr_lpa_slow_items.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
+                                             ctypes.c_void_p]
+            L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
+            L.hdr_lpa_status_string.restype = ctypes.c_char_p
+            L.hdr_lpa_status_string.argtypes = [ctypes.c_int]
+            for name in EXPORTED:
+                if name != "hdr_lpa_status_string":
+                    getattr(L, name).restype = ctypes.c_int
+            if L.hdr_lpa_abi_version() != 1:
+                raise RuntimeError("libhdrlpa.so ABI version mismatch")
+            _lib = L
+        return _lib
+
+
+def check(status: int, what: str) -> None:
+    """Map C status codes onto the reference's exception types."""
+    if status == HDR_OK:
+        return
+    msg = f"{what}: {lib().hdr_lpa_status_string(status).decode()}"
+    if status == HDR_ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if status == HDR_ERR_SHAPE:
+        raise ShapeMismatchError(msg)
+    if status in (HDR_ERR_ARG, HDR_ERR_WORKSPACE):
+        raise ValueError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,414 @@
+// lpa_device.cuh -- device-side building blocks of the unified HDR LPA operator
+// (sm_100a).  Reference semantics cited as pkg/src/hdrfuse/<file>:<line>.
+//
+// Precision design:
+//   * sample positions, offsets d = X - q and the support test |d|^2 > r^2 are
+//     float64 in the reference's exact operation order (no FMA contraction:
+//     __dmul_rn/__dadd_rn), so the sample SET of every window is the
+//     reference's, bit for bit;
+//   * radiance f_hat and the inverse weight denominator are rounded to fp32
+//     once per staged pixel; the Gaussian window is fp32 (MUFU ex2);
+//   * the normal equations are accumulated in float64 (DFMA) for order >= 1
+//     -- SURVEY.md s6.3 measured that fp32 sums break the 1e-4 parity bar --
+//     and solved by an in-register fp64 Cholesky.  Order 0 accumulates fp32.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hdr_lpa.h"
+
+namespace hdrlpa {
+
+constexpr int MAXS = HDR_LPA_MAX_SENSORS;
+constexpr int MAXJ = HDR_LPA_MAX_SCALES;
+
+// fit status codes (_kernels.py:15-18) + the fast path's "needs exact decision"
+constexpr int FIT_OK = 0;
+constexpr int FIT_FAIL = 1;   // TOO_FEW / ILL_CONDITIONED (decided)
+constexpr int FIT_AMBIG = 2;  // condition number too close to the threshold to decide from bounds
+
+struct DevSensor {
+    const uint16_t *raw;
+    int width, height, pitch, sat;
+    int phmask[3];            // bit ph set <=> tile[ph] == channel
+    int separable;            // T01 == 0 && T10 == 0 -> X(x), Y(y) separable
+    double T[6];              // sensor -> reference
+    double N[4];              // inverse of the linear part
+    double nrow0, nrow1;      // |N row 0|, |N row 1| (window bbox half-widths per unit radius)
+    // radiometry (radiometry.py:264-336)
+    double bias, readvar, nonuni;
+    const double *bias_p, *readvar_p, *nonuni_p;
+    const uint8_t *defective;
+    double g, t, n;
+    double inv_denom, inv_denom2, c_shot, qv;  // scalar-calibration constants
+    int planes;               // any calibration plane present
+    // fast-path staging geometry
+    int rw, rh;               // staged region (even), phase planes are (rh/2) x (rw/2)
+    int smem_off;             // float2 offset of this sensor's 4 phase planes
+    int pad_;
+};
+
+struct DevParams {
+    DevSensor s[MAXS];
+    int n_sensors, order, n_scales, use_sigma;
+    int out_w, out_h, row_begin, row_end;
+    int tiles_x, pad0;
+    double sx, sy;            // ref_w / out_w, ref_h / out_h  (lpa.py:222-223)
+    double r[3][MAXJ];        // min(3 sqrt(h), max_radius)     (lpa.py:353, _kernels.py:276-277)
+    double r2[3][MAXJ];       // r * r
+    float hl[3][MAXJ];        // log2(e) / h  (window exponent in exp2 form, fast path)
+    double hinv[3][MAXJ];     // 1 / h (float64 window exponent, exact path)
+    double max_radius, cond, gamma;
+    double fast_R;            // radius the staged tiles cover
+    float *rgb;
+    float *grad;
+    uint8_t *sidx;
+    uint8_t *outcome;
+    float *value;
+    uint16_t *count;
+    int flags, pad1;
+    uint32_t *work_count;
+    uint32_t *work_items;
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Output pixel centre in reference coordinates (lpa.py:222-223):
+// (j + 0.5) * (ref / out) - 0.5, no contraction.
+__device__ __forceinline__ double qcoord(int j, double s) {
+    return __dadd_rn(__dmul_rn(__dadd_rn((double)j, 0.5), s), -0.5);
+}
+
+// Radiance sample of one sensor pixel (radiometry.py:271-336), rounded to fp32:
+// .x = f_hat (electrons/s), .y = 1/den with den = sigma^2 (variance mode) or
+// sigma (sigma mode, _kernels.py:166-167); .y == 0 marks "no sample"
+// (saturated, defective or outside the frame).
+__device__ __forceinline__ float2 radiance_sample(const DevSensor &S, int x, int y, int use_sigma) {
+    if (x < 0 || y < 0 || x >= S.width || y >= S.height) return make_float2(0.f, 0.f);
+    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+    if (raw >= S.sat) return make_float2(0.f, 0.f);                       // :298-300
+    const size_t i = (size_t)y * S.width + x;
+    if (S.defective && __ldg(S.defective + i)) return make_float2(0.f, 0.f);  // :316-317
+    double f, var;
+    if (!S.planes) {
+        f = ((double)raw - S.bias) * S.inv_denom;                          // :279
+        const double shot = S.c_shot * fmax(f, 0.0);                       // :294
+        var = (shot + S.readvar) * S.inv_denom2;                           // :295
+        var = fmax(var, S.qv);                                             // :327-328
+    } else {
+        const double b = S.bias_p ? __ldg(S.bias_p + i) : S.bias;
+        const double a = S.nonuni_p ? __ldg(S.nonuni_p + i) : S.nonuni;
+        const double vr = S.readvar_p ? __ldg(S.readvar_p + i) : S.readvar;
+        const double denom = S.g * S.t * S.n * a;                          // :265
+        f = ((double)raw - b) / denom;
+        const double d2 = denom * denom;
+        const double shot = S.g * S.g * S.t * a * S.n * fmax(f, 0.0);
+        var = fmax((shot + vr) / d2, (1.0 / 12.0) / d2);
+    }
+    const float iv = use_sigma ? (float)rsqrt(var) : (float)(1.0 / var);
+    return make_float2((float)f, iv);
+}
+
+// Sensor-space bounding box of the support disk |X - q| <= r (padded by one
+// pixel; membership is decided exactly afterwards).
+__device__ __forceinline__ void window_bbox(const DevSensor &S, double qx, double qy, double r,
+                                            int &xlo, int &xhi, int &ylo, int &yhi) {
+    const double u = qx - S.T[2], v = qy - S.T[5];
+    const double cx = S.N[0] * u + S.N[1] * v;
+    const double cy = S.N[2] * u + S.N[3] * v;
+    const double hx = r * S.nrow0, hy = r * S.nrow1;
+    xlo = (int)floor(cx - hx) - 1;
+    xhi = (int)ceil(cx + hx) + 1;
+    ylo = (int)floor(cy - hy) - 1;
+    yhi = (int)ceil(cy + hy) + 1;
+}
+
+// ---------------------------------------------------------------------------
+// Moment accumulators (_kernels.py:155-182).  P = number of coefficients.
+// ---------------------------------------------------------------------------
+template <int P, bool F32 = (P == 1)>
+struct Acc {
+    static constexpr int NA = P * (P + 1) / 2;
+    double A[NA];   // upper triangle, row-major packed
+    double b[P];
+    int count;
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) A[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < P; ++i) b[i] = 0.0;
+        count = 0;
+    }
+    __device__ __forceinline__ void add(double wd, float val, double dx, double dy, double dxx,
+                                        double dyy) {
+        double phi[6];
+        phi[0] = 1.0;
+        if (P >= 3) {
+            phi[1] = dx;
+            phi[2] = dy;
+        }
+        if (P >= 6) {
+            phi[3] = dxx;
+            phi[4] = __dmul_rn(dx, dy);
+            phi[5] = dyy;
+        }
+        const double yd = (double)val;
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            const double wa = (a == 0) ? wd : wd * phi[a];
+            b[a] = fma(wa, yd, b[a]);
+#pragma unroll
+            for (int c = a; c < P; ++c) {
+                A[k] = (c == 0) ? A[k] + wa : fma(wa, phi[c], A[k]);
+                ++k;
+            }
+        }
+        ++count;
+    }
+};
+
+// order 0 on the fast path: fp32 weighted mean (max rel. error 6.4e-7)
+template <>
+struct Acc<1, true> {
+    float A[1];
+    float b[1];
+    int count;
+    __device__ __forceinline__ void zero() {
+        A[0] = 0.f;
+        b[0] = 0.f;
+        count = 0;
+    }
+    __device__ __forceinline__ void add(float w, float val, double, double, double, double) {
+        A[0] += w;
+        b[0] = fmaf(w, val, b[0]);
+        ++count;
+    }
+};
+
+template <int P>
+__device__ __forceinline__ constexpr int uidx(int a, int c) {  // packed upper index, a <= c
+    return a * P - a * (a - 1) / 2 + (c - a);
+}
+
+// Result of a solved window: coefficients and g = A^{-1} e1 (for the ICI variance)
+struct Fit {
+    double c0, c1, c2;
+    double g[6];
+};
+
+// In-register Cholesky of the packed SPD matrix (_kernels.py:76-101).
+// Returns false on a non-positive pivot.  L is packed lower, row-major.
+template <int P>
+__device__ __forceinline__ bool cholesky(const double *A, double *L, double *inv) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double s = A[uidx<P>(j, i)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) s -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
+            if (i == j) {
+                if (!(s > 0.0)) return false;
+                const double d = sqrt(s);
+                L[i * (i + 1) / 2 + i] = d;
+                inv[i] = 1.0 / d;
+            } else {
+                L[i * (i + 1) / 2 + j] = s * inv[j];
+            }
+        }
+    }
+    return true;
+}
+
+// Solve from the Cholesky factor; also L^{-1} to get the condition bounds and
+// g = A^{-1} e1.  cu/cl: upper/lower bounds on lambda_max/lambda_min:
+//   lambda_max <= tr(A), lambda_min >= 1/tr(A^{-1})        -> cu = tr(A) tr(A^{-1})
+//   lambda_max >= max_i A_ii, lambda_max(A^{-1}) >= max_i (A^{-1})_ii -> cl
+template <int P>
+__device__ __forceinline__ void chol_finish(const double *A, const double *b, const double *L,
+                                            const double *inv, Fit &fit, double &cu, double &cl) {
+    double z[P], c[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        double s = b[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) s -= L[i * (i + 1) / 2 + k] * z[k];
+        z[i] = s * inv[i];
+    }
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+        double s = z[i];
+#pragma unroll
+        for (int k = i + 1; k < P; ++k) s -= L[k * (k + 1) / 2 + i] * c[k];
+        c[i] = s * inv[i];
+    }
+    fit.c0 = c[0];
+    fit.c1 = (P >= 3) ? c[1] : 0.0;
+    fit.c2 = (P >= 3) ? c[2] : 0.0;
+    // Linv, lower triangular, packed
+    double Li[P * (P + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        Li[i * (i + 1) / 2 + i] = inv[i];
+#pragma unroll
+        for (int j = 0; j < i; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = j; k < i; ++k) s += L[i * (i + 1) / 2 + k] * Li[k * (k + 1) / 2 + j];
+            Li[i * (i + 1) / 2 + j] = -s * inv[i];
+        }
+    }
+    double trA = 0.0, mA = 0.0, trI = 0.0, mI = 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        const double ajj = A[uidx<P>(j, j)];
+        trA += ajj;
+        mA = fmax(mA, ajj);
+        double dj = 0.0, gj = 0.0;
+#pragma unroll
+        for (int i = j; i < P; ++i) {
+            const double lij = Li[i * (i + 1) / 2 + j];
+            dj += lij * lij;
+            gj += lij * Li[i * (i + 1) / 2 + 0];
+        }
+        trI += dj;
+        mI = fmax(mI, dj);
+        fit.g[j] = gj;
+    }
+    cu = trA * trI;
+    cl = mA * mI;
+}
+
+// Fast decision: OK / FAIL / AMBIG, with the reference's tests
+// (_kernels.py:184-199): count < p, A00 <= 0 (p == 1), cond > threshold, pivot <= 0.
+template <int P, bool F32>
+__device__ __forceinline__ int solve_fast(const Acc<P, F32> &acc, double cond, Fit &fit) {
+    if (acc.count < P) return FIT_FAIL;
+    if constexpr (P == 1) {
+        if (!(acc.A[0] > 0)) return FIT_FAIL;
+        fit.c0 = (double)(acc.b[0] / acc.A[0]);
+        fit.c1 = fit.c2 = 0.0;
+        fit.g[0] = 1.0 / (double)acc.A[0];
+        return FIT_OK;
+    } else {
+        double L[P * (P + 1) / 2], inv[P];
+        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;  // pivot <= 0: far beyond 1e8
+        double cu, cl;
+        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
+        const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
+        if (cu <= cond * (1.0 - margin)) return FIT_OK;
+        if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
+        return FIT_AMBIG;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Exact eigenvalue range for the slow path (_kernels.py:26-73)
+// ---------------------------------------------------------------------------
+// p == 3: the reference's trigonometric closed form, same operation order
+__device__ __forceinline__ void eig_range3(const double *A, double &lmin, double &lmax) {
+    const double a11 = A[uidx<3>(0, 0)], a22 = A[uidx<3>(1, 1)], a33 = A[uidx<3>(2, 2)];
+    const double a12 = A[uidx<3>(0, 1)], a13 = A[uidx<3>(0, 2)], a23 = A[uidx<3>(1, 2)];
+    const double q = __ddiv_rn(__dadd_rn(__dadd_rn(a11, a22), a33), 3.0);
+    const double p1 = __dadd_rn(__dadd_rn(__dmul_rn(a12, a12), __dmul_rn(a13, a13)), __dmul_rn(a23, a23));
+    const double e1 = __dsub_rn(a11, q), e2 = __dsub_rn(a22, q), e3 = __dsub_rn(a33, q);
+    const double p2 = __dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(e1, e1), __dmul_rn(e2, e2)), __dmul_rn(e3, e3)),
+        __dmul_rn(2.0, p1));
+    const double scale = fabs(a11) + fabs(a22) + fabs(a33) + 1e-300;
+    if (p2 <= 1e-30 * scale * scale) {
+        lmin = lmax = q;
+        return;
+    }
+    const double pp = sqrt(__ddiv_rn(p2, 6.0));
+    const double b11 = __ddiv_rn(e1, pp), b22 = __ddiv_rn(e2, pp), b33 = __ddiv_rn(e3, pp);
+    const double b12 = __ddiv_rn(a12, pp), b13 = __ddiv_rn(a13, pp), b23 = __ddiv_rn(a23, pp);
+    const double t1 = __dmul_rn(b11, __dsub_rn(__dmul_rn(b22, b33), __dmul_rn(b23, b23)));
+    const double t2 = __dmul_rn(b12, __dsub_rn(__dmul_rn(b12, b33), __dmul_rn(b23, b13)));
+    const double t3 = __dmul_rn(b13, __dsub_rn(__dmul_rn(b12, b23), __dmul_rn(b22, b13)));
+    double r = __ddiv_rn(__dadd_rn(__dsub_rn(t1, t2), t3), 2.0);
+    r = fmin(fmax(r, -1.0), 1.0);
+    const double phi = __ddiv_rn(acos(r), 3.0);
+    const double tp = __dmul_rn(2.0, pp);
+    lmax = __dadd_rn(q, __dmul_rn(tp, cos(phi)));
+    lmin = __dadd_rn(q, __dmul_rn(tp, cos(__dadd_rn(phi, 2.0943951023931953))));  // 2.0 * math.pi / 3.0
+}
+
+// p == 6: cyclic Jacobi (the reference calls LAPACK dsyevd, _kernels.py:72)
+__device__ __noinline__ void eig_range6(const double *A, double &lmin, double &lmax) {
+    double M[6][6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = i; j < 6; ++j) M[i][j] = M[j][i] = A[uidx<6>(i, j)];
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, diag = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            diag += M[i][i] * M[i][i];
+#pragma unroll
+            for (int j = i + 1; j < 6; ++j) off += M[i][j] * M[i][j];
+        }
+        if (off <= 1e-40 * diag) break;
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+            for (int q = p + 1; q < 6; ++q) {
+                const double apq = M[p][q];
+                if (apq == 0.0) continue;
+                const double theta = (M[q][q] - M[p][p]) / (2.0 * apq);
+                const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = rsqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const double mkp = M[k][p], mkq = M[k][q];
+                    M[k][p] = c * mkp - s * mkq;
+                    M[k][q] = s * mkp + c * mkq;
+                }
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const double mpk = M[p][k], mqk = M[q][k];
+                    M[p][k] = c * mpk - s * mqk;
+                    M[q][k] = s * mpk + c * mqk;
+                }
+            }
+    }
+    lmin = lmax = M[0][0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) {
+        lmin = fmin(lmin, M[i][i]);
+        lmax = fmax(lmax, M[i][i]);
+    }
+}
+
+// Exact decision (slow path), mirroring _fit_at's tail (_kernels.py:184-200).
+template <int P, bool F32>
+__device__ __forceinline__ int solve_exact(const Acc<P, F32> &acc, double cond, Fit &fit) {
+    if (acc.count < P) return FIT_FAIL;
+    if constexpr (P == 1) {
+        if (!(acc.A[0] > 0)) return FIT_FAIL;
+        fit.c0 = (double)(acc.b[0] / acc.A[0]);
+        fit.c1 = fit.c2 = 0.0;
+        fit.g[0] = 1.0 / (double)acc.A[0];
+        return FIT_OK;
+    } else {
+        double lmin, lmax;
+        if constexpr (P == 3)
+            eig_range3(acc.A, lmin, lmax);
+        else
+            eig_range6(acc.A, lmin, lmax);
+        if (lmin <= 0.0 || lmax > cond * lmin) return FIT_FAIL;
+        double L[P * (P + 1) / 2], inv[P];
+        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;
+        double cu, cl;
+        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
+        return FIT_OK;
+    }
+}
+
+}  // namespace hdrlpa

@@ -1,0 +1,294 @@
+"""Device-resident rig: raw frames + sensor descriptors on one GPU.
+
+PyTorch is used only as the device-memory and stream provider: raw frames,
+calibration planes, outputs and the workspace are torch tensors whose device
+pointers go through the C ABI (``hdr_lpa_reconstruct``,
+``hdr_saturation_mask``, ``hdr_radiance_planes``) on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .lpa import ReconstructionParams
+from .validation import ShapeMismatchError
+
+
+def _uniform_value(plane: np.ndarray):
+    """Scalar if the calibration plane is uniform (exactly), else None."""
+    flat = plane.ravel()
+    if flat.size and (flat == flat[0]).all():
+        return float(flat[0])
+    return None
+
+
+def hdr_params(params: ReconstructionParams, flags: int = 0) -> N.HdrParams:
+    """Resolve ReconstructionParams into the C struct (per-channel scales)."""
+    P = N.HdrParams()
+    P.flags = int(flags)
+    P.order = int(params.order)
+    P.weight_mode = N.HDR_WEIGHT_SIGMA if params.weight_mode == "sigma" else N.HDR_WEIGHT_VARIANCE
+    P.n_scales = int(params.ici_scales)
+    for c in range(3):
+        for k, h in enumerate(params.channel_scales(c)):
+            P.scale[c][k] = float(h)
+    P.max_radius = float(params.resolved_max_radius())
+    P.cond_threshold = float(params.cond_threshold)
+    P.ici_gamma = float(params.ici_gamma)
+    return P
+
+
+class DeviceRig:
+    """Sensors of one rig resident on a CUDA device.
+
+    ``raws`` are (h, w) int16 tensors holding the uint16 bits of each frame
+    (torch has no general uint16 arithmetic; the kernels read the bits as
+    uint16).  Configs/calibrations are the host objects of
+    :mod:`.radiometry` (or any object with the same attributes).
+    """
+
+    def __init__(self, raws, configs, cal_entries, defective, device):
+        if len(raws) > N.MAX_SENSORS:
+            raise ValueError(f"at most {N.MAX_SENSORS} sensors are supported")
+        self.device = torch.device(device)
+        self.configs = list(configs)
+        self._cal = cal_entries      # per sensor: dict name -> (scalar or device f64 tensor)
+        self._defective = defective  # per sensor: device u8 tensor or None
+        self._workspaces = {}
+        self.raws = []
+        self.set_frames(raws)
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def from_host(cls, frames, configs, cals, device=None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        device = torch.device(device)
+        raws, cal_entries, defective = [], [], []
+        for f, cfg, cal in zip(frames, configs, cals):
+            data = np.ascontiguousarray(getattr(f, "data", f), dtype=np.uint16)
+            h, w = data.shape
+            raws.append(torch.from_numpy(data.view(np.int16)).to(device))
+            entry = {}
+            for name in ("bias", "readout_variance", "nonuniformity"):
+                plane = np.asarray(getattr(getattr(cal, name), "data", getattr(cal, name)),
+                                   dtype=np.float64)
+                if plane.ndim == 0:
+                    entry[name] = float(plane)
+                    continue
+                if plane.shape != (h, w):
+                    raise ShapeMismatchError(
+                        f"dimension mismatch: {name} {plane.shape} vs frame {(h, w)}")
+                u = _uniform_value(plane)
+                entry[name] = u if u is not None else torch.from_numpy(
+                    np.ascontiguousarray(plane)).to(device)
+            cal_entries.append(entry)
+            d = getattr(cfg, "defective", None)
+            if d is not None and len(d):
+                m = np.zeros(h * w, np.uint8)
+                m[np.asarray(d, dtype=np.int64)] = 1
+                defective.append(torch.from_numpy(m).to(device))
+            else:
+                defective.append(None)
+        return cls(raws, configs, cal_entries, defective, device)
+
+    @classmethod
+    def from_device(cls, raws, configs, cals):
+        """Rig over raw frames already on a device (int16/uint16 tensors);
+        calibrations must be uniform (scalars) or host planes."""
+        device = raws[0].device
+        entries = []
+        for cal, r in zip(cals, raws):
+            entry = {}
+            for name in ("bias", "readout_variance", "nonuniformity"):
+                plane = np.asarray(getattr(getattr(cal, name), "data", getattr(cal, name)),
+                                   dtype=np.float64)
+                u = float(plane) if plane.ndim == 0 else _uniform_value(plane)
+                entry[name] = u if u is not None else torch.from_numpy(
+                    np.ascontiguousarray(plane)).to(device)
+            entries.append(entry)
+        defective = []
+        for cfg, r in zip(configs, raws):
+            d = getattr(cfg, "defective", None)
+            if d is not None and len(d):
+                m = torch.zeros(r.numel(), dtype=torch.uint8, device=device)
+                m[torch.as_tensor(np.asarray(d, dtype=np.int64), device=device)] = 1
+                defective.append(m)
+            else:
+                defective.append(None)
+        return cls(list(raws), configs, entries, defective, device)
+
+    def set_frames(self, raws):
+        """Point the rig at new raw frames (same shapes), e.g. the next video frame."""
+        raws = list(raws)
+        if len(raws) != len(self.configs):
+            raise ShapeMismatchError(f"{len(raws)} frames for {len(self.configs)} sensors")
+        for k, r in enumerate(raws):
+            if r.dtype not in (torch.int16, torch.uint16) or r.dim() != 2 or r.device != self.device:
+                raise ValueError("raw frames must be 2-D int16/uint16 tensors on the rig's device")
+            if r.stride(1) != 1:
+                raise ValueError("raw frames must be row-contiguous")
+            if self.raws and tuple(r.shape) != tuple(self.raws[k].shape):
+                raise ShapeMismatchError("frame shape changed")
+        self.raws = raws
+        self._sensors = self._build_sensors()
+
+    def _build_sensors(self):
+        arr = (N.HdrSensor * len(self.raws))()
+        for k, (raw, cfg) in enumerate(zip(self.raws, self.configs)):
+            s = arr[k]
+            s.raw = raw.data_ptr()
+            s.height, s.width = int(raw.shape[0]), int(raw.shape[1])
+            s.pitch = int(raw.stride(0))
+            s.saturation_level = int(cfg.saturation_level)
+            pat = cfg.pattern
+            tile = pat.flat_tile() if hasattr(pat, "flat_tile") else tuple(
+                int(pat.tile[i][j]) for i in (0, 1) for j in (0, 1))
+            for i in range(4):
+                s.tile[i] = int(tile[i])
+            s.exposure_time = float(cfg.exposure_time)
+            s.gain = float(cfg.gain)
+            s.exposure_scaling = float(cfg.exposure_scaling)
+            T = np.asarray(cfg.transform, dtype=np.float64).reshape(6)
+            for i in range(6):
+                s.transform[i] = float(T[i])
+            cal = self._cal[k]
+            for name, sfield, pfield in (("bias", "bias", "bias_plane"),
+                                         ("readout_variance", "readout_variance", "readvar_plane"),
+                                         ("nonuniformity", "nonuniformity", "nonuni_plane")):
+                v = cal[name]
+                if isinstance(v, torch.Tensor):
+                    setattr(s, sfield, 0.0)
+                    setattr(s, pfield, v.data_ptr())
+                else:
+                    setattr(s, sfield, float(v))
+                    setattr(s, pfield, None)
+            d = self._defective[k]
+            s.defective = d.data_ptr() if d is not None else None
+        return arr
+
+    # -- hot path ----------------------------------------------------------
+    def workspace(self, out_w: int, out_h: int) -> torch.Tensor:
+        key = (out_w, out_h)
+        if key not in self._workspaces:
+            nbytes = ctypes.c_size_t()
+            N.check(N.lib().hdr_lpa_workspace_bytes(out_w, out_h, ctypes.byref(nbytes)),
+                    "hdr_lpa_workspace_bytes")
+            self._workspaces[key] = torch.empty(int(nbytes.value), dtype=torch.uint8,
+                                                device=self.device)
+        return self._workspaces[key]
+
+    def allocate_outputs(self, out_size, want_grad=False, want_scale_idx=False,
+                         want_outcome=False, raw_value=False, want_count=False):
+        out_w, out_h = out_size
+        dev = self.device
+        out = {"rgb": torch.empty((out_h, out_w, 3), dtype=torch.float32, device=dev)}
+        if want_grad:
+            out["grad"] = torch.empty((3, 2, out_h, out_w), dtype=torch.float32, device=dev)
+        if want_scale_idx:
+            out["scale_idx"] = torch.empty((3, out_h, out_w), dtype=torch.uint8, device=dev)
+        if want_outcome:
+            out["outcome"] = torch.empty((3, out_h, out_w), dtype=torch.uint8, device=dev)
+        if raw_value:
+            out["value"] = torch.empty((3, out_h, out_w), dtype=torch.float32, device=dev)
+        if want_count:
+            out["count"] = torch.empty((3, out_h, out_w), dtype=torch.int16, device=dev)
+        return out
+
+    def reconstruct(self, out_size, params: ReconstructionParams, ref_size=None, rows=None,
+                    want_grad=False, want_scale_idx=False, want_outcome=False, raw_value=False,
+                    want_count=False, out=None, stream=None, flags=0):
+        """Launch the reconstruction on the current (or given) stream.
+
+        Returns the dict of output tensors (``rgb`` (H, W, 3) float32 and the
+        optional ``grad``/``scale_idx``/``outcome``/``value`` planes).  With
+        ``rows=(r0, r1)`` only that output row band is computed.
+        """
+        out_w, out_h = int(out_size[0]), int(out_size[1])
+        if ref_size is None:
+            ref_size = (out_w, out_h)  # lpa.py:393 (ref_size or out_size)
+        if out is None:
+            out = self.allocate_outputs((out_w, out_h), want_grad, want_scale_idx,
+                                        want_outcome, raw_value, want_count)
+        o = N.HdrOutputs()
+        o.rgb = out["rgb"].data_ptr()
+        o.grad = out["grad"].data_ptr() if "grad" in out else None
+        o.scale_idx = out["scale_idx"].data_ptr() if "scale_idx" in out else None
+        o.outcome = out["outcome"].data_ptr() if "outcome" in out else None
+        o.value = out["value"].data_ptr() if "value" in out else None
+        o.count = out["count"].data_ptr() if "count" in out else None
+        ws = self.workspace(out_w, out_h)
+        r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            rc = N.lib().hdr_lpa_reconstruct(
+                self._sensors, len(self.raws), ctypes.byref(hdr_params(params, flags)),
+                out_w, out_h, float(ref_size[0]), float(ref_size[1]), r0, r1,
+                ctypes.byref(o), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        N.check(rc, "hdr_lpa_reconstruct")
+        return out
+
+    def slow_items(self, out_size) -> int:
+        """Work items the last reconstruct on this output size sent to the slow path."""
+        ws = self.workspace(int(out_size[0]), int(out_size[1]))
+        n = ctypes.c_uint32()
+        st = torch.cuda.current_stream(self.device)
+        N.check(N.lib().hdr_lpa_slow_items(ws.data_ptr(), ctypes.byref(n), st.cuda_stream),
+                "hdr_lpa_slow_items")
+        return int(n.value)
+
+    # -- auxiliary outputs ---------------------------------------------------
+    def saturation_masks(self):
+        """Boolean (h, w) discard masks per sensor, computed on the GPU."""
+        masks = []
+        st = torch.cuda.current_stream(self.device)
+        for k, raw in enumerate(self.raws):
+            h, w = int(raw.shape[0]), int(raw.shape[1])
+            wpr = (w + 31) // 32
+            bits = torch.empty((h, wpr), dtype=torch.int32, device=self.device)
+            N.check(N.lib().hdr_saturation_mask(ctypes.byref(self._sensors[k]), bits.data_ptr(),
+                                                wpr, st.cuda_stream), "hdr_saturation_mask")
+            b = bits.cpu().numpy().view(np.uint32)
+            unpacked = np.unpackbits(b.view(np.uint8).reshape(h, wpr, 4)[..., ::1],
+                                     axis=-1, bitorder="little").reshape(h, wpr * 32)
+            masks.append(unpacked[:, :w].astype(bool))
+        return masks
+
+    def radiance_planes(self, weight_mode: str = "variance"):
+        """Per sensor (value, inv_den) float32 (h, w) device tensors."""
+        st = torch.cuda.current_stream(self.device)
+        mode = N.HDR_WEIGHT_SIGMA if weight_mode == "sigma" else N.HDR_WEIGHT_VARIANCE
+        res = []
+        for k, raw in enumerate(self.raws):
+            v = torch.empty(tuple(raw.shape), dtype=torch.float32, device=self.device)
+            iv = torch.empty_like(v)
+            N.check(N.lib().hdr_radiance_planes(ctypes.byref(self._sensors[k]), mode,
+                                                v.data_ptr(), iv.data_ptr(), st.cuda_stream),
+                    "hdr_radiance_planes")
+            res.append((v, iv))
+        return res
+
+    def materialize_samples(self):
+        """Sample columns in the reference's order (sensor-major, raster):
+        positions (n, 2) f64, channels u8, values f64, sigmas f64, sensor ids."""
+        cols = []
+        for k, (v, iv) in enumerate(self.radiance_planes("variance")):
+            cfg = self.configs[k]
+            v = v.cpu().numpy().ravel()
+            iv = iv.cpu().numpy().ravel()
+            h, w = int(self.raws[k].shape[0]), int(self.raws[k].shape[1])
+            idx = np.flatnonzero(iv > 0)
+            ys, xs = np.divmod(idx, w)
+            T = np.asarray(cfg.transform, dtype=np.float64)
+            X = T[0, 0] * xs + T[0, 1] * ys + T[0, 2]
+            Y = T[1, 0] * xs + T[1, 1] * ys + T[1, 2]
+            tile = np.asarray(cfg.pattern.flat_tile(), np.uint8)
+            ch = tile[(ys % 2) * 2 + xs % 2]
+            cols.append((np.column_stack([X, Y]), ch, v[idx].astype(np.float64),
+                         1.0 / np.sqrt(iv[idx].astype(np.float64)),
+                         np.full(len(idx), k, np.int32)))
+        return tuple(np.concatenate([c[i] for c in cols]) for i in range(5))

@@ -1,0 +1,80 @@
+"""Streaming frame pipeline: pinned host raw frames in, pinned host HDR out.
+
+The paper's implementation overlaps transfers with computation on two
+streams.  Here three CUDA streams carry, per frame,
+H2D of the raw sensor frames -> reconstruction -> D2H of the RGB result,
+with double-buffered device slots so frame i+1's upload and frame i-1's
+download overlap frame i's kernels.  Ordering is expressed with CUDA events
+only; the host never blocks inside :meth:`FramePipeline.submit`.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .engine import DeviceRig
+from .lpa import ReconstructionParams
+
+
+class FramePipeline:
+    def __init__(self, configs, cals, sensor_shapes, out_size, params: ReconstructionParams,
+                 ref_size=None, device=None, slots: int = 2):
+        self.device = torch.device(device if device is not None else
+                                   torch.device("cuda", torch.cuda.current_device()))
+        self.out_size = (int(out_size[0]), int(out_size[1]))
+        self.ref_size = ref_size
+        self.params = params
+        self.slots = slots
+        self.raw_slots = [[torch.empty(tuple(s), dtype=torch.int16, device=self.device)
+                           for s in sensor_shapes] for _ in range(slots)]
+        self.rigs = [DeviceRig.from_device(r, configs, cals) for r in self.raw_slots]
+        # share one workspace (kernels of consecutive frames are stream-ordered)
+        ws = self.rigs[0].workspace(*self.out_size)
+        for r in self.rigs[1:]:
+            r._workspaces[self.out_size] = ws
+        self.outs = [self.rigs[0].allocate_outputs(self.out_size) for _ in range(slots)]
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_comp = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self.ev_in = [torch.cuda.Event() for _ in range(slots)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(slots)]
+        self.ev_out = [torch.cuda.Event() for _ in range(slots)]
+        self.ev_free = [None] * slots   # compute of the previous frame in this slot
+        self.n = 0
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.raw_slots[0])
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.outs[0]["rgb"].numel() * 4
+
+    def submit(self, host_raws, host_rgb):
+        """Queue one frame: ``host_raws`` pinned int16 (h, w) tensors, result
+        into the pinned float32 (H, W, 3) tensor ``host_rgb``."""
+        k = self.n % self.slots
+        with torch.cuda.stream(self.s_in):
+            if self.ev_free[k] is not None:
+                self.s_in.wait_event(self.ev_free[k])
+            for dst, src in zip(self.raw_slots[k], host_raws):
+                dst.copy_(src, non_blocking=True)
+            self.ev_in[k].record(self.s_in)
+        with torch.cuda.stream(self.s_comp):
+            self.s_comp.wait_event(self.ev_in[k])
+            if self.n >= self.slots:
+                self.s_comp.wait_event(self.ev_out[k])  # output slot downloaded
+            self.rigs[k].reconstruct(self.out_size, self.params, ref_size=self.ref_size,
+                                     out=self.outs[k], stream=self.s_comp)
+            self.ev_comp[k].record(self.s_comp)
+            self.ev_free[k] = self.ev_comp[k]
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_comp[k])
+            host_rgb.copy_(self.outs[k]["rgb"], non_blocking=True)
+            self.ev_out[k].record(self.s_out)
+        self.n += 1
+        return self.ev_out[k]
+
+    def synchronize(self):
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.synchronize()
