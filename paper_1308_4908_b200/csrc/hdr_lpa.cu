@@ -17,6 +17,8 @@
 //      those items from global memory with the reference's complete semantics
 //      (radius ladder x1.5 up to max_radius, order fallback, exact eigenvalue
 //      range) -- _kernels.py:257-300.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <climits>
 #include <math.h>
@@ -36,91 +38,208 @@ struct NC {
 };
 
 // ---------------------------------------------------------------------------
-// Window sweeps.  The iteration order (sensor, Bayer phase, row, column over
-// the window's sensor bbox) depends only on (q, r, sensor), never on the tile,
-// so a pixel's result is identical whichever path or band computes it.
+// Window sweeps.  A sweep enumerates the samples of one channel inside the
+// support disk |X - q| <= r, in the order (sensor, Bayer phase, row, column),
+// and calls body(value, 1/den, dx, dy, dx^2, dy^2, |d|^2 as fp32) for each.
+// Offsets and the membership test are float64 in the reference's exact
+// operation order (radiometry.py:84, _kernels.py:160-163), so both sweeps
+// below select exactly the reference's sample set in the same order.
 // ---------------------------------------------------------------------------
-template <class Fetch, class Body>
-__device__ __forceinline__ void sweep(const DevParams &P, int c, double qx, double qy, double r,
-                                      double r2, Fetch fetch, Body body) {
-    for (int s = 0; s < P.n_sensors; ++s) {
-        const DevSensor &S = P.s[s];
-        const int pm = S.phmask[c];
-        if (!pm) continue;
-        int xlo, xhi, ylo, yhi;
-        window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
-        const double T0 = S.T[0], T1 = S.T[1], T2 = S.T[2];
-        const double T3 = S.T[3], T4 = S.T[4], T5 = S.T[5];
-        for (int ph = 0; ph < 4; ++ph) {
-            if (!((pm >> ph) & 1)) continue;
-            const int py = ph >> 1, px = ph & 1;
-            const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
-            for (int y = ys; y <= yhi; y += 2) {
-                const double yd = (double)y;
-                const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
-                for (int x = xs; x <= xhi; x += 2) {
-                    const float2 e = fetch(s, x, y);
-                    if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
-                    const double xd = (double)x;
-                    // apply_transform (radiometry.py:84): T00*x + T01*y + T02
-                    const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
-                    const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
-                    const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
-                    const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
-                    if (__dadd_rn(dxx, dyy) > r2) continue;  // _kernels.py:162
-                    body(e, dx, dy, dxx, dyy);
+
+// Slow path: straight from global memory, everything recomputed per candidate.
+struct GlobalSweep {
+    const DevParams &P;
+    double qx, qy;
+    template <class Body>
+    __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int pm = S.phmask[c];
+            if (!pm) continue;
+            int xlo, xhi, ylo, yhi;
+            window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
+            const double T0 = S.T[0], T1 = S.T[1], T2 = S.T[2];
+            const double T3 = S.T[3], T4 = S.T[4], T5 = S.T[5];
+            for (int ph = 0; ph < 4; ++ph) {
+                if (!((pm >> ph) & 1)) continue;
+                const int py = ph >> 1, px = ph & 1;
+                const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
+                for (int y = ys; y <= yhi; y += 2) {
+                    const double yd = (double)y;
+                    const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
+                    for (int x = xs; x <= xhi; x += 2) {
+                        const float2 e = radiance_sample(S, x, y, P.use_sigma);
+                        if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
+                        const double xd = (double)x;
+                        const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
+                        const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
+                        const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                        const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
+                        const double d2 = __dadd_rn(dxx, dyy);
+                        if (d2 > r2) continue;  // _kernels.py:162
+                        body((double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                    }
                 }
             }
         }
     }
-}
+};
 
-// Window weight W = exp(-dX^T Hinv dX) (_kernels.py:164-168) with isotropic
-// Hinv = I/h.  Fast path: fp32 MUFU ex2 (q <= 9 at the base/ICI radii).  Exact
-// path: float64 exp in the reference's operation order, because the radius
-// ladder reaches q ~ 1e2 where fp32 would underflow.
+// Fast path: the tile's staged shared-memory planes and coordinate tables.
+// Sensors whose transform has no rotation/shear (T01 = T10 = 0) are
+// separable: X depends on x only, so the exact column offsets dx, dx^2 are
+// computed once per (sensor, phase) and kept in registers; the membership
+// test is then one float64 add per candidate.  Rotated sensors pre-test
+// |d|^2 in fp32 (error < 1e-5 px^2, margin 1e-3) and run the exact float64
+// test only for candidates near or inside the disk.
+template <int MAXC>
+struct TileSweep {
+    const DevParams &P;
+    const unsigned char *sm;
+    const int (*org)[2];
+    double qx, qy;
+    template <class Body>
+    __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int pm = S.phmask[c];
+            if (!pm) continue;
+            const int ox = org[s][0], oy = org[s][1];
+            const double *vals = (const double *)(sm + S.off_val);
+            const float *ivs = (const float *)(sm + S.off_iv);
+            const double *tx0 = (const double *)(sm + S.off_tx0);
+            const double *ty4 = (const double *)(sm + S.off_ty4);
+            const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
+            int xlo, xhi, ylo, yhi;
+            window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
+            if (S.separable) {
+                for (int ph = 0; ph < 4; ++ph) {
+                    if (!((pm >> ph) & 1)) continue;
+                    const int py = ph >> 1, px = ph & 1;
+                    const int ys = ylo + ((py - ylo) & 1);
+                    const int xs0 = xlo + ((px - xlo) & 1);
+                    const int nc = xhi >= xs0 ? ((xhi - xs0) >> 1) + 1 : 0;
+                    for (int c0 = 0; c0 < nc; c0 += MAXC) {
+                        const int xs = xs0 + 2 * c0;
+                        double cdx[MAXC], cdxx[MAXC];
+#pragma unroll
+                        for (int i = 0; i < MAXC; ++i) {
+                            if (c0 + i < nc) {
+                                cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx);  // X(x) - qx
+                                cdxx[i] = __dmul_rn(cdx[i], cdx[i]);
+                            } else {
+                                cdx[i] = 0.0;
+                                cdxx[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+                            }
+                        }
+                        const int colbase = ph * plane + ((xs - ox) >> 1);
+                        for (int y = ys; y <= yhi; y += 2) {
+                            const int ly = y - oy;
+                            const double dy = __dsub_rn(ty4[ly], qy);  // Y(y) - qy
+                            const double dyy = __dmul_rn(dy, dy);
+                            if (dyy > r2) continue;
+                            const int rb = colbase + (ly >> 1) * pw;
+#pragma unroll
+                            for (int i = 0; i < MAXC; ++i) {
+                                const double d2 = __dadd_rn(cdxx[i], dyy);
+                                if (d2 <= r2) {
+                                    const float iv = ivs[rb + i];
+                                    if (iv > 0.f)
+                                        body(vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                }
+                            }
+                        }
+                    }
+                }
+            } else {
+                const double *tx3 = (const double *)(sm + S.off_tx3);
+                const double *ty1 = (const double *)(sm + S.off_ty1);
+                const double T2 = S.T[2], T5 = S.T[5];
+                // sensor-space position of q relative to the bbox corner (fp32 pre-test)
+                const double u = qx - T2, v = qy - T5;
+                const float fcx = (float)(S.N[0] * u + S.N[1] * v - (double)xlo);
+                const float fcy = (float)(S.N[2] * u + S.N[3] * v - (double)ylo);
+                const float r2hi = (float)r2 + 1e-3f;
+                const float a0 = S.Tf[0], a1 = S.Tf[1], a3 = S.Tf[2], a4 = S.Tf[3];
+                for (int ph = 0; ph < 4; ++ph) {
+                    if (!((pm >> ph) & 1)) continue;
+                    const int py = ph >> 1, px = ph & 1;
+                    const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
+                    float ey = (float)(ys - ylo) - fcy;
+                    for (int y = ys; y <= yhi; y += 2, ey += 2.f) {
+                        const int ly = y - oy;
+                        const double t1y = ty1[ly], t4y = ty4[ly];
+                        const int rb = ph * plane + (ly >> 1) * pw - (ox >> 1);
+                        float ex = (float)(xs - xlo) - fcx;
+                        for (int x = xs; x <= xhi; x += 2, ex += 2.f) {
+                            const float fx = fmaf(a0, ex, a1 * ey), fy = fmaf(a3, ex, a4 * ey);
+                            if (fmaf(fx, fx, fy * fy) > r2hi) continue;
+                            const int k = rb + (x >> 1);
+                            const float iv = ivs[k];
+                            if (!(iv > 0.f)) continue;
+                            const int lx = x - ox;
+                            const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
+                            const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
+                            const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                            const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
+                            const double d2 = __dadd_rn(dxx, dyy);
+                            if (d2 > r2) continue;
+                            body(vals[k], iv, dx, dy, dxx, dyy, (float)d2);
+                        }
+                    }
+                }
+            }
+        }
+    }
+};
+
+// Window weight (_kernels.py:164-168) W = exp(-dX^T Hinv dX), Hinv = I/h.
+// Fast path: fp32 MUFU ex2 (q <= 9 at the base/ICI radii).  Exact path:
+// float64 exp in the reference's operation order, because the radius ladder
+// reaches q ~ 1e2 where fp32 would underflow.
 template <bool EXACT>
 __device__ __forceinline__ double window_w(const DevParams &P, int c, int k, double dx, double dy,
-                                           double dxx, double dyy) {
+                                           float d2f) {
     if constexpr (EXACT) {
         const double hi = P.hinv[c][k];
         const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
         return exp(-q);
     } else {
-        return (double)ex2_approx(-P.hl[c][k] * (float)(dxx + dyy));
+        return (double)ex2_approx(-P.hl[c][k] * d2f);
     }
 }
 
-template <int ORDER, bool EXACT>
-using AccFor = Acc<NC<ORDER>::P, (!EXACT && ORDER == 0)>;
-
-template <int ORDER, bool EXACT, class Fetch>
-__device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, double qx, double qy,
-                                           double r, double r2, Fetch fetch,
-                                           AccFor<ORDER, EXACT> &acc) {
+template <int ORDER, bool EXACT, class Sweep>
+__device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, double r, double r2,
+                                           const Sweep &sweep, Acc<NC<ORDER>::P> &acc) {
     acc.zero();
-    sweep(P, c, qx, qy, r, r2, fetch, [&](float2 e, double dx, double dy, double dxx, double dyy) {
-        if constexpr (!EXACT && ORDER == 0) {
-            const float W = ex2_approx(-P.hl[c][k] * (float)(dxx + dyy));
-            acc.add(W * e.y, e.x, dx, dy, dxx, dyy);
+    sweep(c, r, r2, [&](double v, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
+        if constexpr (EXACT) {
+            acc.add(window_w<true>(P, c, k, dx, dy, d2f) * (double)iv, v, dx, dy, dxx, dyy);
         } else {
-            const double W = window_w<EXACT>(P, c, k, dx, dy, dxx, dyy);
-            acc.add(W * (double)e.y, e.x, dx, dy, dxx, dyy);
+            const float w = ex2_approx(-P.hl[c][k] * d2f) * iv;  // w = W / den
+            acc.add((double)w, v, dx, dy, dxx, dyy);
         }
     });
 }
 
 // Variance of the constant term (ICI spec): v = sum w^2 var (phi . g)^2,
 // with w^2 var = W^2/den for variance weights and W^2 for sigma weights.
-template <int ORDER, bool EXACT, class Fetch>
-__device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, double qx,
-                                               double qy, Fetch fetch, const double *g) {
+template <int ORDER, bool EXACT, class Sweep>
+__device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, const Sweep &sweep,
+                                               const double *g) {
     const bool sig = P.use_sigma;
     double v = 0.0;
-    sweep(P, c, qx, qy, P.r[c][k], P.r2[c][k], fetch,
-          [&](float2 e, double dx, double dy, double dxx, double dyy) {
-              const double W = window_w<EXACT>(P, c, k, dx, dy, dxx, dyy);
-              const double t = sig ? W * W : W * W * (double)e.y;
+    sweep(c, P.r[c][k], P.r2[c][k],
+          [&](double, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
+              double t;
+              if constexpr (EXACT) {
+                  const double W = window_w<true>(P, c, k, dx, dy, d2f);
+                  t = sig ? W * W : W * W * (double)iv;
+              } else {
+                  const float W = ex2_approx(-P.hl[c][k] * d2f);
+                  t = (double)(sig ? W * W : W * W * iv);
+              }
               double pg = g[0];
               if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
               if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
@@ -135,6 +254,8 @@ struct PixelResult {
     int sidx;
     int count;    // samples in the accepted window
 };
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 __device__ __forceinline__ void write_result(const DevParams &P, int pix, int c,
                                              const PixelResult &R) {
@@ -155,23 +276,22 @@ __device__ __forceinline__ void write_result(const DevParams &P, int pix, int c,
 
 // ---------------------------------------------------------------------------
 // Exact evaluation (slow path): lpa_evaluate's ladder (_kernels.py:257-300)
-// and the ICI rule, from global memory.
+// and the ICI rule.
 // ---------------------------------------------------------------------------
-template <int ORDER, class Fetch>
-__device__ bool ladder_order(const DevParams &P, int c, double qx, double qy, Fetch fetch,
-                             PixelResult &R) {
+template <int ORDER, class Sweep>
+__device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
     constexpr int PN = NC<ORDER>::P;
     double r = P.r[c][0];  // already min(r0, max_radius)
     int step = 0;
-    AccFor<ORDER, true> acc;
+    Acc<PN> acc;
     for (;;) {
-        accumulate<ORDER, true>(P, c, 0, qx, qy, r, __dmul_rn(r, r), fetch, acc);
+        accumulate<ORDER, true>(P, c, 0, r, __dmul_rn(r, r), sweep, acc);
         Fit fit;
         if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
             R.count = acc.count;
             R.val = fit.c0;
-            R.gx = ORDER >= 1 ? fit.c1 : __longlong_as_double(0x7ff8000000000000ll);
-            R.gy = ORDER >= 1 ? fit.c2 : __longlong_as_double(0x7ff8000000000000ll);
+            R.gx = ORDER >= 1 ? fit.c1 : qnan();
+            R.gy = ORDER >= 1 ? fit.c2 : qnan();
             R.outcome = ORDER * 16 + (step < 15 ? step : 15);
             return true;
         }
@@ -181,41 +301,40 @@ __device__ bool ladder_order(const DevParams &P, int c, double qx, double qy, Fe
     }
 }
 
-template <int ORDER, class Fetch>
-__device__ void ladder(const DevParams &P, int c, double qx, double qy, Fetch fetch,
-                       PixelResult &R) {
+template <int ORDER, class Sweep>
+__device__ void ladder(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
     R.sidx = 0;
-    if (ladder_order<ORDER>(P, c, qx, qy, fetch, R)) return;
+    if (ladder_order<ORDER>(P, c, sweep, R)) return;
     if constexpr (ORDER >= 1) {
-        if (ladder_order<ORDER - 1>(P, c, qx, qy, fetch, R)) return;
+        if (ladder_order<ORDER - 1>(P, c, sweep, R)) return;
     }
     if constexpr (ORDER >= 2) {
-        if (ladder_order<0>(P, c, qx, qy, fetch, R)) return;
+        if (ladder_order<0>(P, c, sweep, R)) return;
     }
-    const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    R.val = R.gx = R.gy = nan;
+    R.val = R.gx = R.gy = qnan();
     R.outcome = HDR_OUTCOME_NAN;
     R.count = 0;
 }
 
-// ICI with a pluggable decision (fast: bounds, may return AMBIG; exact).
-// Returns FIT_OK with R filled, FIT_FAIL if scale 0 fails (caller runs the
-// ladder), FIT_AMBIG if a decision needs the exact path.
-template <int ORDER, bool EXACT, class Fetch>
-__device__ int ici(const DevParams &P, int c, double qx, double qy, Fetch fetch, PixelResult &R) {
+// ICI with a pluggable decision: fast (condition
+// bounds; may return AMBIG) or exact.  Returns FIT_OK with R filled, FIT_FAIL
+// if scale 0 fails (the caller runs the ladder), FIT_AMBIG if a decision
+// needs the exact path.
+template <int ORDER, bool EXACT, class Sweep>
+__device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
     constexpr int PN = NC<ORDER>::P;
-    AccFor<ORDER, EXACT> acc;
+    Acc<PN> acc;
     Fit fit;
     double L = 0.0, U = 0.0;
     for (int k = 0; k < P.n_scales; ++k) {
-        accumulate<ORDER, EXACT>(P, c, k, qx, qy, P.r[c][k], P.r2[c][k], fetch, acc);
+        accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
         const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
         if (st == FIT_AMBIG) return FIT_AMBIG;
         if (st != FIT_OK) {
             if (k == 0) return FIT_FAIL;
-            break;  // invalid scale ends the search at k-1
+            break;  // an invalid scale ends the search at k-1
         }
-        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, qx, qy, fetch, fit.g));
+        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g));
         const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
         if (k == 0) {
             L = lo;
@@ -231,7 +350,7 @@ __device__ int ici(const DevParams &P, int c, double qx, double qy, Fetch fetch,
         R.sidx = k;
         R.count = acc.count;
     }
-    if (ORDER == 0) R.gx = R.gy = __longlong_as_double(0x7ff8000000000000ll);
+    if (ORDER == 0) R.gx = R.gy = qnan();
     R.outcome = ORDER * 16;
     return FIT_OK;
 }
@@ -239,25 +358,53 @@ __device__ int ici(const DevParams &P, int c, double qx, double qy, Fetch fetch,
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
     const uint32_t n = *P.work_count;
-    auto fetch = [&](int s, int x, int y) { return radiance_sample(P.s[s], x, y, P.use_sigma); };
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t item = P.work_items[i];
         const int pix = (int)(item >> 2), c = (int)(item & 3);
         const int ox = pix % P.out_w, oy = pix / P.out_w;
-        const double qx = qcoord(ox, P.sx), qy = qcoord(oy, P.sy);
+        const GlobalSweep sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         PixelResult R;
         if (P.n_scales > 1) {
-            if (ici<ORDER, true>(P, c, qx, qy, fetch, R) != FIT_OK) ladder<ORDER>(P, c, qx, qy, fetch, R);
+            if (ici<ORDER, true>(P, c, sweep, R) != FIT_OK) ladder<ORDER>(P, c, sweep, R);
         } else {
-            ladder<ORDER>(P, c, qx, qy, fetch, R);
+            ladder<ORDER>(P, c, sweep, R);
         }
         write_result(P, pix, c, R);
     }
 }
 
 // ---------------------------------------------------------------------------
-// Fast path
+// Fast path: persistent CTAs, double-buffered TMA staging of the raw tiles.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile(
+        "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(
+            smem_addr(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void region_origin(const DevSensor &S, const DevParams &P, int tx0,
                                               int ty0, int tx1, int ty1, int &ox, int &oy) {
     // union of the window bboxes of the tile's corner queries at radius fast_R;
@@ -272,47 +419,109 @@ __device__ __forceinline__ void region_origin(const DevSensor &S, const DevParam
         xmin = min(xmin, xlo);
         ymin = min(ymin, ylo);
     }
-    ox = xmin & ~1;  // even, so phase = coordinate parity
+    // x: multiple of 8 elements -- a TMA tile copy must start on a 16-byte
+    // boundary of the row (measured: unaligned starts raise an illegal-
+    // instruction fault; scripts/probes/tma_probe.cu).  Both even, so the
+    // Bayer phase of a staged pixel equals the parity of its coordinates.
+    ox = xmin & ~7;
     oy = ymin & ~1;
 }
 
-template <int ORDER, bool ICI>
-__global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__ DevParams P) {
-    extern __shared__ float2 smem[];
-    __shared__ int s_org[MAXS][2];
-    constexpr int PN = NC<ORDER>::P;
+__device__ __forceinline__ void tile_bounds(const DevParams &P, int t, int &tx0, int &ty0, int &tx1,
+                                            int &ty1) {
+    tx0 = (t % P.tiles_x) * TW;
+    ty0 = P.row_begin + (t / P.tiles_x) * TH;
+    tx1 = min(tx0 + TW, P.out_w) - 1;
+    ty1 = min(ty0 + TH, P.row_end) - 1;
+}
 
-    const int tile = blockIdx.x;
-    const int tx0 = (tile % P.tiles_x) * TW;
-    const int ty0 = P.row_begin + (tile / P.tiles_x) * TH;
-    const int tx1 = min(tx0 + TW, P.out_w) - 1;
-    const int ty1 = min(ty0 + TH, P.row_end) - 1;
-
-    if (threadIdx.x < P.n_sensors) {
-        int ox, oy;
-        region_origin(P.s[threadIdx.x], P, tx0, ty0, tx1, ty1, ox, oy);
-        s_org[threadIdx.x][0] = ox;
-        s_org[threadIdx.x][1] = oy;
+// Thread 0: origins of tile t's staged regions and, with TMA, one bulk tensor
+// copy per sensor into raw buffer b, completing on mbarrier b.
+__device__ __forceinline__ void stage_issue(const DevParams &P, unsigned char *sm, int t, int b,
+                                            int (*org)[2], uint64_t *bar) {
+    int tx0, ty0, tx1, ty1;
+    tile_bounds(P, t, tx0, ty0, tx1, ty1);
+    uint32_t bytes = 0;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        region_origin(P.s[s], P, tx0, ty0, tx1, ty1, org[s][0], org[s][1]);
+        bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 2);
     }
-    __syncthreads();
+    if (P.use_tma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, bytes);
+        for (int s = 0; s < P.n_sensors; ++s)
+            tma_load_2d(sm + P.s[s].off_raw[b], &P.tmap[s], org[s][0], org[s][1], bar);
+    }
+}
 
-    // Stage raw footprint -> (f_hat, 1/den) in Bayer phase planes.
+// All threads: raw buffer b -> (f_hat, 1/den) Bayer phase planes + exact
+// float64 coordinate tables of the regions.
+__device__ __forceinline__ void stage_convert(const DevParams &P, unsigned char *sm, int b,
+                                              const int (*org)[2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = NT / 32;
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
-        const int ox = s_org[s][0], oy = s_org[s][1];
+        const int ox = org[s][0], oy = org[s][1];
         const int rw = S.rw, rh = S.rh, pw = rw >> 1, plane = pw * (rh >> 1);
-        float2 *base = smem + S.smem_off;
-        for (int idx = threadIdx.x; idx < rw * rh; idx += NT) {
-            const int ly = idx / rw, lx = idx - ly * rw;
-            const float2 e = radiance_sample(S, ox + lx, oy + ly, P.use_sigma);
-            base[((ly & 1) * 2 + (lx & 1)) * plane + (ly >> 1) * pw + (lx >> 1)] = e;
+        const uint16_t *rawb = (const uint16_t *)(sm + S.off_raw[b]);
+        double *vals = (double *)(sm + S.off_val);
+        float *ivs = (float *)(sm + S.off_iv);
+        if (!P.use_tma) {  // unaligned pitch: cooperative copy into the raw buffer first
+            uint16_t *rw_b = (uint16_t *)(sm + S.off_raw[b]);
+            for (int ly = warp; ly < rh; ly += NW) {
+                const int y = oy + ly;
+                for (int lx = lane; lx < rw; lx += 32) {
+                    const int x = ox + lx;
+                    uint16_t v = 0;
+                    if (x >= 0 && y >= 0 && x < S.width && y < S.height)
+                        v = __ldg(S.raw + (size_t)y * S.pitch + x);
+                    rw_b[ly * rw + lx] = v;
+                }
+            }
+            __syncwarp();
+        }
+        for (int ly = warp; ly < rh; ly += NW) {
+            const int y = oy + ly;
+            const bool yin = y >= 0 && y < S.height;
+            for (int lx = lane; lx < rw; lx += 32) {
+                const int x = ox + lx;
+                float2 e = make_float2(0.f, 0.f);
+                if (yin && x >= 0 && x < S.width)
+                    e = radiance_from_raw(S, (int)rawb[ly * rw + lx], x, y, P.use_sigma);
+                const int k = ((ly & 1) * 2 + (lx & 1)) * plane + (ly >> 1) * pw + (lx >> 1);
+                vals[k] = (double)e.x;
+                ivs[k] = e.y;
+            }
+        }
+        // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y) (exact,
+        // since fl(T01*y) = fl(T10*x) = 0); otherwise the four partial products.
+        double *tx0t = (double *)(sm + S.off_tx0), *tx3t = (double *)(sm + S.off_tx3);
+        double *ty1t = (double *)(sm + S.off_ty1), *ty4t = (double *)(sm + S.off_ty4);
+        for (int i = threadIdx.x; i < rw; i += NT) {
+            const double xd = (double)(ox + i);
+            const double a = __dmul_rn(S.T[0], xd);
+            tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
+            tx3t[i] = __dmul_rn(S.T[3], xd);
+        }
+        for (int i = threadIdx.x; i < rh; i += NT) {
+            const double yd = (double)(oy + i);
+            const double bb = __dmul_rn(S.T[4], yd);
+            ty1t[i] = __dmul_rn(S.T[1], yd);
+            ty4t[i] = S.separable ? __dadd_rn(bb, S.T[5]) : bb;
         }
     }
-    __syncthreads();
+}
 
+template <int ORDER, bool ICI, int MAXC>
+__device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm, int t,
+                                             const int (*org)[2]) {
+    constexpr int PN = NC<ORDER>::P;
+    int tx0, ty0, tx1, ty1;
+    tile_bounds(P, t, tx0, ty0, tx1, ty1);
     const int px = tx0 + (int)(threadIdx.x % TW);
     const int py = ty0 + (int)(threadIdx.x / TW);
-    if (px >= P.out_w || py >= P.row_end) return;
+    if (px > tx1 || py > ty1) return;
     const int pix = py * P.out_w + px;
     const double qx = qcoord(px, P.sx), qy = qcoord(py, P.sy);
 
@@ -322,17 +531,10 @@ __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__
         const DevSensor &S = P.s[s];
         int xlo, xhi, ylo, yhi;
         window_bbox(S, qx, qy, P.fast_R, xlo, xhi, ylo, yhi);
-        covered &= xlo >= s_org[s][0] && ylo >= s_org[s][1] && xhi < s_org[s][0] + S.rw &&
-                   yhi < s_org[s][1] + S.rh;
+        covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
+                   yhi < org[s][1] + S.rh;
     }
-
-    auto fetch = [&](int s, int x, int y) {
-        const DevSensor &S = P.s[s];
-        const int lx = x - s_org[s][0], ly = y - s_org[s][1];
-        const int pw = S.rw >> 1;
-        return smem[S.smem_off + ((y & 1) * 2 + (x & 1)) * (pw * (S.rh >> 1)) + (ly >> 1) * pw +
-                    (lx >> 1)];
-    };
+    const TileSweep<MAXC> sweep{P, sm, org, qx, qy};
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
@@ -340,18 +542,17 @@ __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__
         int st = FIT_AMBIG;
         if (covered) {
             if constexpr (ICI) {
-                st = ici<ORDER, false>(P, c, qx, qy, fetch, R);
+                st = ici<ORDER, false>(P, c, sweep, R);
             } else {
-                AccFor<ORDER, false> acc;
-                accumulate<ORDER, false>(P, c, 0, qx, qy, P.r[c][0], P.r2[c][0], fetch, acc);
+                Acc<PN> acc;
+                accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
                 if (st == FIT_OK) {
                     R.count = acc.count;
                     R.val = fit.c0;
-                    const double nan = __longlong_as_double(0x7ff8000000000000ll);
-                    R.gx = ORDER >= 1 ? fit.c1 : nan;
-                    R.gy = ORDER >= 1 ? fit.c2 : nan;
+                    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                    R.gy = ORDER >= 1 ? fit.c2 : qnan();
                     R.outcome = ORDER * 16;
                 }
             }
@@ -362,6 +563,35 @@ __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__
             const uint32_t slot = atomicAdd(P.work_count, 1u);
             P.work_items[slot] = ((uint32_t)pix << 2) | (uint32_t)c;
         }
+    }
+}
+
+template <int ORDER, bool ICI, int MAXC>
+__global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__ DevParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int s_org[2][MAXS][2];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int ntiles = P.tiles_x * P.tiles_y;
+    int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (P.use_tma) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        if (t < ntiles) stage_issue(P, smem, t, 0, s_org[0], &s_bar[0]);
+    }
+    __syncthreads();
+    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
+        const int b = it & 1;
+        const int tn = t + gridDim.x;
+        // prefetch the next tile while this one is converted and fitted
+        if (threadIdx.x == 0 && tn < ntiles) stage_issue(P, smem, tn, b ^ 1, s_org[b ^ 1], &s_bar[b ^ 1]);
+        if (P.use_tma) mbar_wait(&s_bar[b], (uint32_t)((it >> 1) & 1));
+        stage_convert(P, smem, b, s_org[b]);
+        __syncthreads();
+        tile_compute<ORDER, ICI, MAXC>(P, smem, t, s_org[b]);
+        __syncthreads();
     }
 }
 
@@ -455,6 +685,16 @@ static int fill_sensor(const HdrSensor &h, DevSensor &d) {
     d.inv_denom2 = 1.0 / (denom * denom);
     d.c_shot = h.gain * h.gain * h.exposure_time * h.nonuniformity * h.exposure_scaling;
     d.qv = (1.0 / 12.0) / (denom * denom);
+    d.bias_f = (float)d.bias;
+    d.readvar_f = (float)d.readvar;
+    d.inv_denom_f = (float)d.inv_denom;
+    d.inv_denom2_f = (float)d.inv_denom2;
+    d.c_shot_f = (float)d.c_shot;
+    d.qv_f = (float)d.qv;
+    d.Tf[0] = (float)T[0];
+    d.Tf[1] = (float)T[1];
+    d.Tf[2] = (float)T[3];
+    d.Tf[3] = (float)T[4];
     return HDR_OK;
 }
 
@@ -463,16 +703,62 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
 }
 
-template <int ORDER>
-static int launch_all(const DevParams &P, int tiles, int smem_bytes, cudaStream_t st) {
-    const void *fn = P.n_scales > 1 ? (const void *)lpa_fast_kernel<ORDER, true>
-                                    : (const void *)lpa_fast_kernel<ORDER, false>;
+template <int ORDER, bool ICI, int MAXC>
+static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream_t st) {
+    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
+    int dev = 0, nsm = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem_bytes) != cudaSuccess ||
+        per_sm < 1)
+        return HDR_ERR_CUDA;
+    const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
+    lpa_fast_kernel<ORDER, ICI, MAXC><<<grid, NT, smem_bytes, st>>>(P);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 2-D uint16 tensor map over a raw frame whose box is the staged region.
+static bool encode_raw_map(const DevSensor &d, CUtensorMap *map) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    if (((uintptr_t)d.raw & 15) || ((size_t)d.pitch * 2) % 16 || d.rw > 256 || d.rh > 256 ||
+        (d.rw * 2) % 16)
+        return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)d.width, (cuuint64_t)d.height};
+    const cuuint64_t strides[1] = {(cuuint64_t)d.pitch * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)d.rw, (cuuint32_t)d.rh};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void *)d.raw, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int ORDER>
+static int launch_all(const DevParams &P, int tiles, int smem_bytes, int maxc, cudaStream_t st) {
+    int rc;
     if (P.n_scales > 1)
-        lpa_fast_kernel<ORDER, true><<<tiles, NT, smem_bytes, st>>>(P);
+        rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, true, 8>(P, tiles, smem_bytes, st);
     else
-        lpa_fast_kernel<ORDER, false><<<tiles, NT, smem_bytes, st>>>(P);
-    if (cudaPeekAtLastError() != cudaSuccess) return HDR_ERR_CUDA;
+        rc = maxc <= 4 ? launch_fast<ORDER, false, 4>(P, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, false, 8>(P, tiles, smem_bytes, st);
+    if (rc != HDR_OK) return rc;
     if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -573,34 +859,52 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.work_count = (uint32_t *)workspace;
     P.work_items = (uint32_t *)((char *)workspace + WS_HEADER);
 
-    // staged region per sensor: tile extent in sensor space + 2 x window half-width
-    int smem_f2 = 0;
+    // Staged region per sensor: tile extent in sensor space + 2 x window
+    // half-width (+ rounding/alignment slack).  Shared memory per sensor:
+    // f64 values and f32 1/den of the four phase planes, f64 coordinate tables.
+    int smem = 0, maxc = 1;
+    auto take = [&](int bytes) {
+        const int off = smem;
+        smem += (bytes + 127) & ~127;  // 128-B aligned (TMA destinations)
+        return off;
+    };
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
         const double ex = (TW - 1) * P.sx, ey = (TH - 1) * P.sy;
         const double wx = fabs(d.N[0]) * ex + fabs(d.N[1]) * ey + 2.0 * fastR * d.nrow0;
         const double wy = fabs(d.N[2]) * ex + fabs(d.N[3]) * ey + 2.0 * fastR * d.nrow1;
-        int rw = (int)ceil(wx) + 8, rh = (int)ceil(wy) + 8;
-        rw += rw & 1;
+        int rw = (int)ceil(wx) + 12, rh = (int)ceil(wy) + 6;  // + floor/ceil + alignment
+        rw = (rw + 7) & ~7;  // TMA box inner extent: multiple of 16 bytes
         rh += rh & 1;
         d.rw = rw;
         d.rh = rh;
-        d.smem_off = smem_f2;
-        smem_f2 += rw * rh;
+        d.off_raw[0] = take(rw * rh * 2);
+        d.off_raw[1] = take(rw * rh * 2);
+        d.off_val = take(rw * rh * 8);
+        d.off_iv = take(rw * rh * 4);
+        d.off_tx0 = take(rw * 8);
+        d.off_tx3 = take(rw * 8);
+        d.off_ty1 = take(rh * 8);
+        d.off_ty4 = take(rh * 8);
+        // columns of one Bayer phase inside a window bbox: <= floor(r |N row 0|) + 2
+        maxc = max(maxc, (int)floor(fastR * d.nrow0) + 2);
     }
-    const int smem_bytes = smem_f2 * (int)sizeof(float2);
+    const int smem_bytes = smem;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
+    P.use_tma = 1;
+    for (int s = 0; s < n_sensors && P.use_tma; ++s)
+        if (!encode_raw_map(P.s[s], &P.tmap[s])) P.use_tma = 0;
 
     cudaStream_t st = (cudaStream_t)stream;
-    const int tiles_y = (row_end - row_begin + TH - 1) / TH;
+    P.tiles_y = (row_end - row_begin + TH - 1) / TH;
     P.tiles_x = (out_w + TW - 1) / TW;
-    const int tiles = P.tiles_x * tiles_y;
+    const int tiles = P.tiles_x * P.tiles_y;
     if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess) return HDR_ERR_CUDA;
     int rc;
     switch (P.order) {
-        case 0: rc = launch_all<0>(P, tiles, smem_bytes, st); break;
-        case 1: rc = launch_all<1>(P, tiles, smem_bytes, st); break;
-        default: rc = launch_all<2>(P, tiles, smem_bytes, st); break;
+        case 0: rc = launch_all<0>(P, tiles, smem_bytes, maxc, st); break;
+        case 1: rc = launch_all<1>(P, tiles, smem_bytes, maxc, st); break;
+        default: rc = launch_all<2>(P, tiles, smem_bytes, maxc, st); break;
     }
     return rc;
 }

@@ -12,6 +12,7 @@
 //     -- SURVEY.md s6.3 measured that fp32 sums break the 1e-4 parity bar --
 //     and solved by an in-register fp64 Cholesky.  Order 0 accumulates fp32.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,18 +42,23 @@ struct DevSensor {
     const uint8_t *defective;
     double g, t, n;
     double inv_denom, inv_denom2, c_shot, qv;  // scalar-calibration constants
+    float bias_f, readvar_f, inv_denom_f, inv_denom2_f, c_shot_f, qv_f;
     int planes;               // any calibration plane present
     // fast-path staging geometry
     int rw, rh;               // staged region (even), phase planes are (rh/2) x (rw/2)
-    int smem_off;             // float2 offset of this sensor's 4 phase planes
-    int pad_;
+    int off_raw[2];           // byte offsets of the two raw uint16 staging buffers (TMA dst)
+    int off_val, off_iv;      // byte offsets in shared memory: f64 values, f32 1/den
+    int off_tx0, off_tx3;     // f64 tables fl(T00*x), fl(T10*x) over the region's columns
+    int off_ty1, off_ty4;     // f64 tables fl(T01*y), fl(T11*y) over the region's rows
+    float Tf[4];              // fp32 linear part (pre-test of rotated sensors)
 };
 
 struct DevParams {
+    CUtensorMap tmap[MAXS];   // per-sensor 2-D uint16 tensor maps (box = staged region)
     DevSensor s[MAXS];
     int n_sensors, order, n_scales, use_sigma;
     int out_w, out_h, row_begin, row_end;
-    int tiles_x, pad0;
+    int tiles_x, tiles_y, use_tma, pad0;
     double sx, sy;            // ref_w / out_w, ref_h / out_h  (lpa.py:222-223)
     double r[3][MAXJ];        // min(3 sqrt(h), max_radius)     (lpa.py:353, _kernels.py:276-277)
     double r2[3][MAXJ];       // r * r
@@ -87,50 +93,65 @@ __device__ __forceinline__ double qcoord(int j, double s) {
 // .x = f_hat (electrons/s), .y = 1/den with den = sigma^2 (variance mode) or
 // sigma (sigma mode, _kernels.py:166-167); .y == 0 marks "no sample"
 // (saturated, defective or outside the frame).
-__device__ __forceinline__ float2 radiance_sample(const DevSensor &S, int x, int y, int use_sigma) {
-    if (x < 0 || y < 0 || x >= S.width || y >= S.height) return make_float2(0.f, 0.f);
-    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+// Radiometric conversion of one raw digital value at sensor pixel (x, y),
+// which the caller has checked lies inside the frame.
+__device__ __forceinline__ float2 radiance_from_raw(const DevSensor &S, int raw, int x, int y,
+                                                    int use_sigma) {
     if (raw >= S.sat) return make_float2(0.f, 0.f);                       // :298-300
     const size_t i = (size_t)y * S.width + x;
     if (S.defective && __ldg(S.defective + i)) return make_float2(0.f, 0.f);  // :316-317
-    double f, var;
+    float f, var;
     if (!S.planes) {
-        f = ((double)raw - S.bias) * S.inv_denom;                          // :279
-        const double shot = S.c_shot * fmax(f, 0.0);                       // :294
-        var = (shot + S.readvar) * S.inv_denom2;                           // :295
-        var = fmax(var, S.qv);                                             // :327-328
+        // scalar calibration: fp32 with precomputed reciprocals (values are
+        // rounded to fp32 anyway; relative error ~2 ulp of fp32)
+        f = ((float)raw - S.bias_f) * S.inv_denom_f;                       // :279
+        const float shot = S.c_shot_f * fmaxf(f, 0.f);                     // :294
+        var = fmaxf((shot + S.readvar_f) * S.inv_denom2_f, S.qv_f);        // :295, :327-328
     } else {
         const double b = S.bias_p ? __ldg(S.bias_p + i) : S.bias;
         const double a = S.nonuni_p ? __ldg(S.nonuni_p + i) : S.nonuni;
         const double vr = S.readvar_p ? __ldg(S.readvar_p + i) : S.readvar;
         const double denom = S.g * S.t * S.n * a;                          // :265
-        f = ((double)raw - b) / denom;
+        const double fd = ((double)raw - b) / denom;
         const double d2 = denom * denom;
-        const double shot = S.g * S.g * S.t * a * S.n * fmax(f, 0.0);
-        var = fmax((shot + vr) / d2, (1.0 / 12.0) / d2);
+        const double shot = S.g * S.g * S.t * a * S.n * fmax(fd, 0.0);
+        f = (float)fd;
+        var = (float)fmax((shot + vr) / d2, (1.0 / 12.0) / d2);
     }
-    const float iv = use_sigma ? (float)rsqrt(var) : (float)(1.0 / var);
-    return make_float2((float)f, iv);
+    const float iv = use_sigma ? rsqrtf(var) : __frcp_rn(var);
+    return make_float2(f, iv);
 }
 
-// Sensor-space bounding box of the support disk |X - q| <= r (padded by one
-// pixel; membership is decided exactly afterwards).
+// Radiance sample of one sensor pixel (radiometry.py:271-336), rounded to fp32:
+// .x = f_hat (electrons/s), .y = 1/den with den = sigma^2 (variance mode) or
+// sigma (sigma mode, _kernels.py:166-167); .y == 0 marks "no sample"
+// (saturated, defective or outside the frame).
+__device__ __forceinline__ float2 radiance_sample(const DevSensor &S, int x, int y, int use_sigma) {
+    if (x < 0 || y < 0 || x >= S.width || y >= S.height) return make_float2(0.f, 0.f);
+    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+    return radiance_from_raw(S, raw, x, y, use_sigma);
+}
+
+// Sensor-space bounding box of the support disk |X - q| <= r.  In real
+// arithmetic the ellipse T^{-1}(disk) lies in [c - h, c + h]; the rounding of
+// c and h (~1e-13 px) can only add candidates, which the exact float64
+// membership test then rejects.
 __device__ __forceinline__ void window_bbox(const DevSensor &S, double qx, double qy, double r,
                                             int &xlo, int &xhi, int &ylo, int &yhi) {
     const double u = qx - S.T[2], v = qy - S.T[5];
     const double cx = S.N[0] * u + S.N[1] * v;
     const double cy = S.N[2] * u + S.N[3] * v;
     const double hx = r * S.nrow0, hy = r * S.nrow1;
-    xlo = (int)floor(cx - hx) - 1;
-    xhi = (int)ceil(cx + hx) + 1;
-    ylo = (int)floor(cy - hy) - 1;
-    yhi = (int)ceil(cy + hy) + 1;
+    xlo = (int)floor(cx - hx);
+    xhi = (int)ceil(cx + hx);
+    ylo = (int)floor(cy - hy);
+    yhi = (int)ceil(cy + hy);
 }
 
 // ---------------------------------------------------------------------------
 // Moment accumulators (_kernels.py:155-182).  P = number of coefficients.
 // ---------------------------------------------------------------------------
-template <int P, bool F32 = (P == 1)>
+template <int P>
 struct Acc {
     static constexpr int NA = P * (P + 1) / 2;
     double A[NA];   // upper triangle, row-major packed
@@ -143,7 +164,8 @@ struct Acc {
         for (int i = 0; i < P; ++i) b[i] = 0.0;
         count = 0;
     }
-    __device__ __forceinline__ void add(double wd, float val, double dx, double dy, double dxx,
+    // A += w phi phi^T, b += w phi y with phi = [1, dx, dy, dx^2, dx dy, dy^2][:P]
+    __device__ __forceinline__ void add(double wd, double yd, double dx, double dy, double dxx,
                                         double dyy) {
         double phi[6];
         phi[0] = 1.0;
@@ -156,7 +178,6 @@ struct Acc {
             phi[4] = __dmul_rn(dx, dy);
             phi[5] = dyy;
         }
-        const double yd = (double)val;
         int k = 0;
 #pragma unroll
         for (int a = 0; a < P; ++a) {
@@ -168,24 +189,6 @@ struct Acc {
                 ++k;
             }
         }
-        ++count;
-    }
-};
-
-// order 0 on the fast path: fp32 weighted mean (max rel. error 6.4e-7)
-template <>
-struct Acc<1, true> {
-    float A[1];
-    float b[1];
-    int count;
-    __device__ __forceinline__ void zero() {
-        A[0] = 0.f;
-        b[0] = 0.f;
-        count = 0;
-    }
-    __device__ __forceinline__ void add(float w, float val, double, double, double, double) {
-        A[0] += w;
-        b[0] = fmaf(w, val, b[0]);
         ++count;
     }
 };
@@ -286,14 +289,14 @@ __device__ __forceinline__ void chol_finish(const double *A, const double *b, co
 
 // Fast decision: OK / FAIL / AMBIG, with the reference's tests
 // (_kernels.py:184-199): count < p, A00 <= 0 (p == 1), cond > threshold, pivot <= 0.
-template <int P, bool F32>
-__device__ __forceinline__ int solve_fast(const Acc<P, F32> &acc, double cond, Fit &fit) {
+template <int P>
+__device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &fit) {
     if (acc.count < P) return FIT_FAIL;
     if constexpr (P == 1) {
         if (!(acc.A[0] > 0)) return FIT_FAIL;
-        fit.c0 = (double)(acc.b[0] / acc.A[0]);
+        fit.c0 = acc.b[0] / acc.A[0];
         fit.c1 = fit.c2 = 0.0;
-        fit.g[0] = 1.0 / (double)acc.A[0];
+        fit.g[0] = 1.0 / acc.A[0];
         return FIT_OK;
     } else {
         double L[P * (P + 1) / 2], inv[P];
@@ -387,14 +390,14 @@ __device__ __noinline__ void eig_range6(const double *A, double &lmin, double &l
 }
 
 // Exact decision (slow path), mirroring _fit_at's tail (_kernels.py:184-200).
-template <int P, bool F32>
-__device__ __forceinline__ int solve_exact(const Acc<P, F32> &acc, double cond, Fit &fit) {
+template <int P>
+__device__ __forceinline__ int solve_exact(const Acc<P> &acc, double cond, Fit &fit) {
     if (acc.count < P) return FIT_FAIL;
     if constexpr (P == 1) {
         if (!(acc.A[0] > 0)) return FIT_FAIL;
-        fit.c0 = (double)(acc.b[0] / acc.A[0]);
+        fit.c0 = acc.b[0] / acc.A[0];
         fit.c1 = fit.c2 = 0.0;
-        fit.g[0] = 1.0 / (double)acc.A[0];
+        fit.g[0] = 1.0 / acc.A[0];
         return FIT_OK;
     } else {
         double lmin, lmax;

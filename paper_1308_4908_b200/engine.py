@@ -72,7 +72,12 @@ class DeviceRig:
         for f, cfg, cal in zip(frames, configs, cals):
             data = np.ascontiguousarray(getattr(f, "data", f), dtype=np.uint16)
             h, w = data.shape
-            raws.append(torch.from_numpy(data.view(np.int16)).to(device))
+            # rows padded to a multiple of 8 elements (16 bytes) so the kernels
+            # can stage tiles with TMA bulk tensor copies
+            pw = (w + 7) // 8 * 8
+            buf = torch.empty((h, pw), dtype=torch.int16, device=device)
+            buf[:, :w].copy_(torch.from_numpy(data.view(np.int16)))
+            raws.append(buf[:, :w])
             entry = {}
             for name in ("bias", "readout_variance", "nonuniformity"):
                 plane = np.asarray(getattr(getattr(cal, name), "data", getattr(cal, name)),

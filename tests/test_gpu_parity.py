@@ -123,6 +123,24 @@ def test_sparse_ladder_and_nan(cuda):
     assert slow > 0
 
 
+def test_unaligned_pitch_staging(cuda):
+    """Row pitch not a multiple of 16 bytes: staging falls back from TMA to
+    cooperative loads; results must be unchanged."""
+    import torch
+    from paper_1308_4908_b200.engine import DeviceRig
+
+    frames, cfgs, cals = _case("misaligned", 90, 54, seed=14)
+    raws = [torch.from_numpy(f.data.view(np.int16)).to(cuda) for f in frames]  # pitch 90
+    dev = DeviceRig.from_device(raws, cfgs, cals)
+    p = hl.ReconstructionParams(order=2, scale=0.7, ici_scales=2)
+    out = dev.reconstruct((90, 54), p, want_scale_idx=True, want_outcome=True)
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    ref = oracle.reconstruct(frames, cfgs, cals, (90, 54), p)
+    _check(got, ref, max_tol=1e-2, max_sidx_mismatch=2)
+    aligned = hl.frames_to_samples(frames, cfgs, cals).device().reconstruct((90, 54), p)
+    assert np.array_equal(aligned["rgb"].cpu().numpy(), got["rgb"], equal_nan=True)
+
+
 def test_band_split_bit_identical(cuda):
     frames, cfgs, cals = _case("misaligned", 128, 96, seed=9)
     raw = hl.frames_to_samples(frames, cfgs, cals)
@@ -152,8 +170,9 @@ def test_radiance_planes_match_oracle_samples(cuda):
     pos, ch, val, sig, sid = hl.frames_to_samples(frames, cfgs, cals).materialize()
     opos, och, oval, osig, osid = oracle.frames_to_samples(frames, cfgs, cals)
     assert np.array_equal(pos, opos) and np.array_equal(ch, och) and np.array_equal(sid, osid)
-    np.testing.assert_allclose(val, oval, rtol=2e-7, atol=1e-3)
-    np.testing.assert_allclose(sig, osig, rtol=2e-7)
+    # staging radiometry is fp32: a few fp32 ulp
+    np.testing.assert_allclose(val, oval, rtol=1e-6, atol=1e-3)
+    np.testing.assert_allclose(sig, osig, rtol=1e-6)
 
 
 def test_reference_api_shapes(cuda):
