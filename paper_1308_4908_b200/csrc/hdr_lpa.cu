@@ -77,7 +77,7 @@ struct GlobalSweep {
                         const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                         const double d2 = __dadd_rn(dxx, dyy);
                         if (d2 > r2) continue;  // _kernels.py:162
-                        body((double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                        body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
                     }
                 }
             }
@@ -128,8 +128,9 @@ struct TileSweep {
                                 cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx);  // X(x) - qx
                                 cdxx[i] = __dmul_rn(cdx[i], cdx[i]);
                             } else {
+                                // finite sentinel: never inside, and 0 * phi stays 0
                                 cdx[i] = 0.0;
-                                cdxx[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+                                cdxx[i] = 1e300;
                             }
                         }
                         const int colbase = ph * plane + ((xs - ox) >> 1);
@@ -139,14 +140,14 @@ struct TileSweep {
                             const double dyy = __dmul_rn(dy, dy);
                             if (dyy > r2) continue;
                             const int rb = colbase + (ly >> 1) * pw;
+                            // branch-free over the row: candidates outside the disk or
+                            // without a sample contribute with weight 0 (ok = false)
 #pragma unroll
                             for (int i = 0; i < MAXC; ++i) {
                                 const double d2 = __dadd_rn(cdxx[i], dyy);
-                                if (d2 <= r2) {
-                                    const float iv = ivs[rb + i];
-                                    if (iv > 0.f)
-                                        body(vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
-                                }
+                                const float iv = ivs[rb + i];
+                                const bool ok = (d2 <= r2) && (iv > 0.f);
+                                body(ok, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
                             }
                         }
                     }
@@ -184,7 +185,7 @@ struct TileSweep {
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);
                             if (d2 > r2) continue;
-                            body(vals[k], iv, dx, dy, dxx, dyy, (float)d2);
+                            body(true, vals[k], iv, dx, dy, dxx, dyy, (float)d2);
                         }
                     }
                 }
@@ -213,14 +214,22 @@ template <int ORDER, bool EXACT, class Sweep>
 __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, double r, double r2,
                                            const Sweep &sweep, Acc<NC<ORDER>::P> &acc) {
     acc.zero();
-    sweep(c, r, r2, [&](double v, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
-        if constexpr (EXACT) {
-            acc.add(window_w<true>(P, c, k, dx, dy, d2f) * (double)iv, v, dx, dy, dxx, dyy);
-        } else {
-            const float w = ex2_approx(-P.hl[c][k] * d2f) * iv;  // w = W / den
-            acc.add((double)w, v, dx, dy, dxx, dyy);
-        }
-    });
+    if constexpr (EXACT) {
+        const double hi = P.hinv[c][k];
+        sweep(c, r, r2, [&](bool, double v, float iv, double dx, double dy, double dxx, double dyy,
+                            float) {
+            const double q =
+                __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
+            acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
+        });
+    } else {
+        const float hl = P.hl[c][k];
+        sweep(c, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
+                            double dyy, float d2f) {
+            const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;  // w = W / den
+            acc.add((double)w, ok ? v : 0.0, dx, dy, dxx, dyy, ok ? 1 : 0);
+        });
+    }
 }
 
 // Variance of the constant term (ICI spec): v = sum w^2 var (phi . g)^2,
@@ -229,21 +238,26 @@ template <int ORDER, bool EXACT, class Sweep>
 __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, const Sweep &sweep,
                                                const double *g) {
     const bool sig = P.use_sigma;
+    const double hi = P.hinv[c][k];
+    const float hl = P.hl[c][k];
+    const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4], g5 = g[5];
     double v = 0.0;
     sweep(c, P.r[c][k], P.r2[c][k],
-          [&](double, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
+          [&](bool ok, double, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
               double t;
               if constexpr (EXACT) {
-                  const double W = window_w<true>(P, c, k, dx, dy, d2f);
+                  const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx),
+                                             __dmul_rn(__dmul_rn(hi, dy), dy));
+                  const double W = exp(-q);
                   t = sig ? W * W : W * W * (double)iv;
               } else {
-                  const float W = ex2_approx(-P.hl[c][k] * d2f);
+                  const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
                   t = (double)(sig ? W * W : W * W * iv);
               }
-              double pg = g[0];
-              if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
-              if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
-              v = fma(t, pg * pg, v);
+              double pg = g0;
+              if (ORDER >= 1) pg += dx * g1 + dy * g2;
+              if (ORDER >= 2) pg += dxx * g3 + __dmul_rn(dx, dy) * g4 + dyy * g5;
+              if (ok) v = fma(t, pg * pg, v);  // select: unused columns carry sentinels
           });
     return v;
 }
@@ -865,7 +879,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     int smem = 0, maxc = 1;
     auto take = [&](int bytes) {
         const int off = smem;
-        smem += (bytes + 127) & ~127;  // 128-B aligned (TMA destinations)
+        smem += (bytes + 64 + 127) & ~127;  // 128-B aligned (TMA destinations) + read slack
         return off;
     };
     for (int s = 0; s < n_sensors; ++s) {

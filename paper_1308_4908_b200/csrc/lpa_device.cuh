@@ -166,7 +166,7 @@ struct Acc {
     }
     // A += w phi phi^T, b += w phi y with phi = [1, dx, dy, dx^2, dx dy, dy^2][:P]
     __device__ __forceinline__ void add(double wd, double yd, double dx, double dy, double dxx,
-                                        double dyy) {
+                                        double dyy, int inc = 1) {
         double phi[6];
         phi[0] = 1.0;
         if (P >= 3) {
@@ -189,7 +189,7 @@ struct Acc {
                 ++k;
             }
         }
-        ++count;
+        count += inc;
     }
 };
 
