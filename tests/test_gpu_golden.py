@@ -1,0 +1,34 @@
+"""The CUDA path on the reference-generated golden cases (tests/golden):
+against the reference's own stored output where present and against the
+bit-exact oracle everywhere (NaN map, ladder outcome, 1e-4 radiance)."""
+
+import numpy as np
+import pytest
+
+from golden_cases import load, names
+from oracle import compare, oracle
+
+import paper_1308_4908_b200 as hl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", names())
+def test_gpu_matches_reference_golden(cuda, name):
+    frames, cfgs, cals, out_size, params, ref_size, case, arrays = load(name)
+    raw = hl.frames_to_samples(frames, cfgs, cals)
+    out = raw.device().reconstruct(out_size, params, ref_size=ref_size, want_outcome=True,
+                                   want_grad=True)
+    rgb = out["rgb"].cpu().numpy()
+    ref = oracle.reconstruct(frames, cfgs, cals, out_size, params, ref_size=ref_size)
+    s = compare.summary(rgb, ref["rgb"])
+    print(name, s)
+    assert s["nan_map_equal"]
+    assert s["frac_over"] <= 1e-3 and s["max"] <= (1e-2 if params.order == 2 else 1e-3)
+    assert int((out["outcome"].cpu().numpy() != ref["outcome"]).sum()) == 0
+    if "rgb" in arrays:  # the reference's own float32 output
+        s2 = compare.summary(rgb, arrays["rgb"])
+        assert s2["nan_map_equal"] and s2["frac_over"] <= 1e-3
+    g = out["grad"].cpu().numpy()
+    sg = compare.summary(g[:, 0], ref["gx"], floor=1e3)
+    assert sg["nan_map_equal"] and sg["p99"] < 1e-3
