@@ -22,6 +22,9 @@
 #include <cuda_runtime.h>
 #include <climits>
 #include <math.h>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
 #include <stdio.h>
 #include <string.h>
 
@@ -31,6 +34,9 @@
 namespace hdrlpa {
 
 constexpr int TW = 32, TH = 8, NT = TW * TH;
+// workspace layout: [header: work counter][pre-computed taps][work items]
+static const size_t WS_HEADER = 256;
+static const size_t WS_TAPS = 64 * 1024;  // <= 2730 taps
 
 template <int ORDER>
 struct NC {
@@ -92,7 +98,7 @@ struct GlobalSweep {
 // test is then one float64 add per candidate.  Rotated sensors pre-test
 // |d|^2 in fp32 (error < 1e-5 px^2, margin 1e-3) and run the exact float64
 // test only for candidates near or inside the disk.
-template <int MAXC>
+template <int MAXC, bool BRANCHY>
 struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
@@ -140,14 +146,24 @@ struct TileSweep {
                             const double dyy = __dmul_rn(dy, dy);
                             if (dyy > r2) continue;
                             const int rb = colbase + (ly >> 1) * pw;
-                            // branch-free over the row: candidates outside the disk or
-                            // without a sample contribute with weight 0 (ok = false)
+                            // orders 0-1: branch-free over the row (candidates outside the
+                            // disk or without a sample contribute with weight 0); order 2
+                            // (27 DFMA per sample) only visits the samples inside.
 #pragma unroll
                             for (int i = 0; i < MAXC; ++i) {
                                 const double d2 = __dadd_rn(cdxx[i], dyy);
-                                const float iv = ivs[rb + i];
-                                const bool ok = (d2 <= r2) && (iv > 0.f);
-                                body(ok, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                if constexpr (BRANCHY) {
+                                    if (d2 <= r2) {
+                                        const float iv = ivs[rb + i];
+                                        if (iv > 0.f)
+                                            body(true, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy,
+                                                 (float)d2);
+                                    }
+                                } else {
+                                    const float iv = ivs[rb + i];
+                                    const bool ok = (d2 <= r2) && (iv > 0.f);
+                                    body(ok, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                }
                             }
                         }
                     }
@@ -527,7 +543,41 @@ __device__ __forceinline__ void stage_convert(const DevParams &P, unsigned char 
     }
 }
 
-template <int ORDER, bool ICI, int MAXC>
+// Fixed-scale accumulation from the pre-computed taps: the window of every
+// output pixel of a parity class visits the same sensor offsets with the same
+// weights, so there is no membership test, no exp and no loop control beyond
+// the tap list (the samples and weights are the reference's: DESIGN.md s3).
+template <int ORDER>
+__device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
+                                                const int (*org)[2], int c, int px, int py,
+                                                Acc<NC<ORDER>::P> &acc) {
+    acc.zero();
+    const Tap *taps = (const Tap *)(sm + P.off_taps);
+    const int cls = ((py & 1) << 1) | (px & 1);
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const int n = P.pat_cnt[s][c][py & 1];
+        if (!n) continue;
+        const DevSensor &S = P.s[s];
+        const Tap *tp = taps + P.pat_off[s][c][cls];
+        const double *vals = (const double *)(sm + S.off_val);
+        const float *ivs = (const float *)(sm + S.off_iv);
+        const int pw = S.rw >> 1;
+        // base: the pixel's own position in its phase plane (origins are even)
+        const int base = ((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1);
+        for (int t = 0; t < n; ++t) {
+            const Tap T = tp[t];
+            const int k = base + T.delta;
+            const float iv = ivs[k];
+            const bool ok = iv > 0.f && T.W > 0.f;
+            const float w = ok ? T.W * iv : 0.f;
+            const double dxx = ORDER >= 2 ? __dmul_rn(T.dx, T.dx) : 0.0;
+            const double dyy = ORDER >= 2 ? __dmul_rn(T.dy, T.dy) : 0.0;
+            acc.add((double)w, ok ? vals[k] : 0.0, T.dx, T.dy, dxx, dyy, ok ? 1 : 0);
+        }
+    }
+}
+
+template <int ORDER, bool ICI, int MAXC, bool PAT>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm, int t,
                                              const int (*org)[2]) {
     constexpr int PN = NC<ORDER>::P;
@@ -548,7 +598,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
                    yhi < org[s][1] + S.rh;
     }
-    const TileSweep<MAXC> sweep{P, sm, org, qx, qy};
+    const TileSweep<MAXC, (ORDER >= 2)> sweep{P, sm, org, qx, qy};
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
@@ -559,7 +609,10 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                 st = ici<ORDER, false>(P, c, sweep, R);
             } else {
                 Acc<PN> acc;
-                accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
+                if constexpr (PAT)
+                    accumulate_taps<ORDER>(P, sm, org, c, px, py, acc);
+                else
+                    accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
                 if (st == FIT_OK) {
@@ -580,13 +633,18 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     }
 }
 
-template <int ORDER, bool ICI, int MAXC>
+template <int ORDER, bool ICI, int MAXC, bool PAT>
 __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
     __shared__ __align__(8) uint64_t s_bar[2];
     const int ntiles = P.tiles_x * P.tiles_y;
     int t = blockIdx.x;
+    if (PAT) {
+        const uint32_t *src = (const uint32_t *)P.taps;
+        uint32_t *dst = (uint32_t *)(smem + P.off_taps);
+        for (int i = threadIdx.x; i < P.n_taps * (int)(sizeof(Tap) / 4); i += NT) dst[i] = src[i];
+    }
     if (threadIdx.x == 0) {
         if (P.use_tma) {
             mbar_init(&s_bar[0], 1);
@@ -604,7 +662,7 @@ __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__
         if (P.use_tma) mbar_wait(&s_bar[b], (uint32_t)((it >> 1) & 1));
         stage_convert(P, smem, b, s_org[b]);
         __syncthreads();
-        tile_compute<ORDER, ICI, MAXC>(P, smem, t, s_org[b]);
+        tile_compute<ORDER, ICI, MAXC, PAT>(P, smem, t, s_org[b]);
         __syncthreads();
     }
 }
@@ -717,9 +775,9 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
 }
 
-template <int ORDER, bool ICI, int MAXC>
+template <int ORDER, bool ICI, int MAXC, bool PAT = false>
 static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream_t st) {
-    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC>;
+    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -728,7 +786,7 @@ static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream
         per_sm < 1)
         return HDR_ERR_CUDA;
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
-    lpa_fast_kernel<ORDER, ICI, MAXC><<<grid, NT, smem_bytes, st>>>(P);
+    lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
 }
 
@@ -766,7 +824,9 @@ static bool encode_raw_map(const DevSensor &d, CUtensorMap *map) {
 template <int ORDER>
 static int launch_all(const DevParams &P, int tiles, int smem_bytes, int maxc, cudaStream_t st) {
     int rc;
-    if (P.n_scales > 1)
+    if (P.pat)
+        rc = launch_fast<ORDER, false, 4, true>(P, tiles, smem_bytes, st);
+    else if (P.n_scales > 1)
         rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, tiles, smem_bytes, st)
                        : launch_fast<ORDER, true, 8>(P, tiles, smem_bytes, st);
     else
@@ -782,13 +842,110 @@ static int launch_all(const DevParams &P, int tiles, int smem_bytes, int maxc, c
     return HDR_OK;
 }
 
+// Pre-computed-weight mode: applies when the output grid is the
+// reference grid and every sensor is translation-only.  Then, for an output
+// pixel q = (j, i), sensor pixel x = j + k maps to X = fl(x + T02) and
+// dx = X - j = k + T02 up to the rounding of fl(x + T02) (< 3e-13 for
+// |x| < 2^12): the window of every pixel of a parity class (j & 1, i & 1)
+// contains the same offsets with the same weights.  The tables are built with
+// the reference's arithmetic at a representative pixel; a tap closer than
+// 1e-9 r^2 to the support boundary (where that rounding could flip the
+// membership test) disables the mode.
+static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
+    taps.clear();
+    if (P.n_scales != 1 || P.sx != 1.0 || P.sy != 1.0) return false;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const DevSensor &S = P.s[s];
+        if (!(S.T[0] == 1.0 && S.T[1] == 0.0 && S.T[3] == 0.0 && S.T[4] == 1.0)) return false;
+        if (fabs(S.T[2]) > 64 || fabs(S.T[5]) > 64 || S.width > 4096 || S.height > 4096)
+            return false;
+    }
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const DevSensor &S = P.s[s];
+        int tile[4];
+        for (int ph = 0; ph < 4; ++ph)
+            for (int c = 0; c < 3; ++c)
+                if ((S.phmask[c] >> ph) & 1) tile[ph] = c;
+        for (int c = 0; c < 3; ++c) {
+            const double r = P.r[c][0], r2 = P.r2[c][0], hi = P.hinv[c][0];
+            const int R = (int)ceil(r + fabs(S.T[2]) + fabs(S.T[5])) + 1;
+            std::vector<Tap> cls[4];
+            for (int cl = 0; cl < 4; ++cl) {
+                const int j = 64 + (cl & 1), i = 64 + (cl >> 1);  // representative pixel
+                const double qx = (double)j, qy = (double)i;      // qcoord(j, 1.0) == j
+                for (int m = -R; m <= R; ++m)
+                    for (int k = -R; k <= R; ++k) {
+                        const int x = j + k, y = i + m;
+                        if (tile[((y & 1) << 1) | (x & 1)] != c) continue;
+                        const double X = (1.0 * (double)x + 0.0 * (double)y) + S.T[2];
+                        const double Y = (0.0 * (double)x + 1.0 * (double)y) + S.T[5];
+                        const double dx = X - qx, dy = Y - qy;
+                        const double d2 = dx * dx + dy * dy;
+                        if (fabs(d2 - r2) <= 1e-9 * r2) return false;  // near-tie: general path
+                        if (d2 > r2) continue;
+                        const double q = hi * dx * dx + hi * dy * dy;
+                        // sample (x, y) lives in phase plane ((y&1), (x&1)) at
+                        // ((y-oy)>>1, (x-ox)>>1); the pixel (j, i) has base
+                        // ((i-oy)>>1)*pw + ((j-ox)>>1).  With ox, oy even the
+                        // difference depends only on (k, m) and the class.
+                        const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
+                        const int ph = ((y & 1) << 1) | (x & 1);
+                        Tap t;
+                        t.dx = dx;
+                        t.dy = dy;
+                        t.W = (float)exp(-q);
+                        t.delta = ph * plane + ((y >> 1) - (i >> 1)) * pw + ((x >> 1) - (j >> 1));
+                        cls[cl].push_back(t);
+                    }
+            }
+            for (int py = 0; py < 2; ++py) {
+                const size_t n = std::max(cls[py * 2].size(), cls[py * 2 + 1].size());
+                P.pat_cnt[s][c][py] = (int)n;
+                for (int px = 0; px < 2; ++px) {
+                    std::vector<Tap> &v = cls[py * 2 + px];
+                    Tap pad;
+                    memset(&pad, 0, sizeof(pad));  // W = 0: no contribution, not counted
+                    while (v.size() < n) v.push_back(pad);
+                    P.pat_off[s][c][py * 2 + px] = (int)taps.size();
+                    taps.insert(taps.end(), v.begin(), v.end());
+                }
+            }
+        }
+    }
+    if (taps.size() * sizeof(Tap) > WS_TAPS) return false;
+    P.n_taps = (int)taps.size();
+    return true;
+}
+
+static uint64_t fnv1a(const void *p, size_t n) {
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < n; ++i) h = (h ^ ((const unsigned char *)p)[i]) * 1099511628211ull;
+    return h;
+}
+
+// Upload the tap table into the workspace unless this workspace already holds it.
+static int upload_taps(const std::vector<Tap> &taps, void *dst, cudaStream_t st) {
+    static std::mutex mu;
+    static std::unordered_map<void *, uint64_t> last;
+    const size_t bytes = taps.size() * sizeof(Tap);
+    const uint64_t sig = fnv1a(taps.data(), bytes) ^ (uint64_t)bytes;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = last.find(dst);
+    if (it != last.end() && it->second == sig) return HDR_OK;
+    // pageable source: the copy is staged before cudaMemcpyAsync returns
+    if (cudaMemcpyAsync(dst, taps.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return HDR_ERR_CUDA;
+    last[dst] = sig;
+    return HDR_OK;
+}
+
 }  // namespace hdrlpa
 
 using namespace hdrlpa;
 
 extern "C" {
 
-static const size_t WS_HEADER = 256;
+
 
 int hdr_lpa_abi_version(void) { return HDR_LPA_ABI_VERSION; }
 
@@ -808,7 +965,7 @@ int hdr_lpa_workspace_bytes(int out_w, int out_h, size_t *bytes) {
     if (out_w <= 0 || out_h <= 0 || !bytes) return HDR_ERR_ARG;
     const size_t items = (size_t)out_w * out_h * 3;
     if ((size_t)out_w * out_h >= (1ull << 30)) return HDR_ERR_ARG;  // item packing
-    *bytes = WS_HEADER + items * sizeof(uint32_t);
+    *bytes = WS_HEADER + WS_TAPS + items * sizeof(uint32_t);
     return HDR_OK;
 }
 
@@ -871,7 +1028,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.count = out->count;
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
-    P.work_items = (uint32_t *)((char *)workspace + WS_HEADER);
+    P.work_items = (uint32_t *)((char *)workspace + WS_HEADER + WS_TAPS);
 
     // Staged region per sensor: tile extent in sensor space + 2 x window
     // half-width (+ rounding/alignment slack).  Shared memory per sensor:
@@ -887,7 +1044,9 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         const double ex = (TW - 1) * P.sx, ey = (TH - 1) * P.sy;
         const double wx = fabs(d.N[0]) * ex + fabs(d.N[1]) * ey + 2.0 * fastR * d.nrow0;
         const double wy = fabs(d.N[2]) * ex + fabs(d.N[3]) * ey + 2.0 * fastR * d.nrow1;
-        int rw = (int)ceil(wx) + 12, rh = (int)ceil(wy) + 6;  // + floor/ceil + alignment
+        // + 2 for floor/ceil of the bbox ends, + 7 / + 1 for aligning the origin
+        // down to a multiple of 8 columns / 2 rows
+        int rw = (int)ceil(wx) + 2 + 7, rh = (int)ceil(wy) + 2 + 1;
         rw = (rw + 7) & ~7;  // TMA box inner extent: multiple of 16 bytes
         rh += rh & 1;
         d.rw = rw;
@@ -903,6 +1062,12 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         // columns of one Bayer phase inside a window bbox: <= floor(r |N row 0|) + 2
         maxc = max(maxc, (int)floor(fastR * d.nrow0) + 2);
     }
+    std::vector<Tap> taps;
+    P.pat = build_taps(P, taps) ? 1 : 0;
+    if (P.pat) {
+        P.off_taps = take((int)(taps.size() * sizeof(Tap)));
+        P.taps = (const Tap *)((char *)workspace + WS_HEADER);
+    }
     const int smem_bytes = smem;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
     P.use_tma = 1;
@@ -914,6 +1079,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.tiles_x = (out_w + TW - 1) / TW;
     const int tiles = P.tiles_x * P.tiles_y;
     if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess) return HDR_ERR_CUDA;
+    if (P.pat && upload_taps(taps, (char *)workspace + WS_HEADER, st) != HDR_OK) return HDR_ERR_CUDA;
     int rc;
     switch (P.order) {
         case 0: rc = launch_all<0>(P, tiles, smem_bytes, maxc, st); break;

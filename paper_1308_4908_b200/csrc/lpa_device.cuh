@@ -53,6 +53,15 @@ struct DevSensor {
     float Tf[4];              // fp32 linear part (pre-test of rotated sensors)
 };
 
+// Pre-computed window tap (aligned / translation-only rigs on the reference
+// grid): sensor offset (k, m) from the output pixel, exact float64 offset
+// d = X - q and window weight W = exp(-|d|^2 / h).  W == 0 marks padding.
+struct Tap {
+    double dx, dy;
+    float W;
+    int delta;  // offset of the sample in the sensor's phase planes relative to the pixel's base
+};
+
 struct DevParams {
     CUtensorMap tmap[MAXS];   // per-sensor 2-D uint16 tensor maps (box = staged region)
     DevSensor s[MAXS];
@@ -73,6 +82,12 @@ struct DevParams {
     float *value;
     uint16_t *count;
     int flags, pad1;
+    // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
+    int pat, n_taps, off_taps, pad2;
+    const Tap *taps;                // device copy (in the workspace), staged into shared memory
+    int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
+    int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
+    int pat_base[MAXS][2];          // offset (ox, oy) of the tap window's origin: see build_taps
     uint32_t *work_count;
     uint32_t *work_items;
 };
@@ -217,9 +232,9 @@ __device__ __forceinline__ bool cholesky(const double *A, double *L, double *inv
             for (int k = 0; k < j; ++k) s -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
             if (i == j) {
                 if (!(s > 0.0)) return false;
-                const double d = sqrt(s);
-                L[i * (i + 1) / 2 + i] = d;
-                inv[i] = 1.0 / d;
+                const double ri = rsqrt(s);
+                L[i * (i + 1) / 2 + i] = s * ri;
+                inv[i] = ri;
             } else {
                 L[i * (i + 1) / 2 + j] = s * inv[j];
             }

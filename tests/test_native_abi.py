@@ -65,7 +65,7 @@ def test_abi_version_and_status_strings():
 def test_workspace_size():
     n = ctypes.c_size_t()
     assert N.lib().hdr_lpa_workspace_bytes(2400, 1700, ctypes.byref(n)) == 0
-    assert n.value == 256 + 2400 * 1700 * 3 * 4
+    assert n.value == 256 + 64 * 1024 + 2400 * 1700 * 3 * 4
     assert N.lib().hdr_lpa_workspace_bytes(0, 10, ctypes.byref(n)) == N.HDR_ERR_ARG
 
 
