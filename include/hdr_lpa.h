@@ -42,7 +42,7 @@ extern "C" {
 
 #define HDR_LPA_MAX_SENSORS 8
 #define HDR_LPA_MAX_SCALES 8
-#define HDR_LPA_ABI_VERSION 1
+#define HDR_LPA_ABI_VERSION 2
 
 /* status codes */
 #define HDR_OK 0
@@ -119,15 +119,18 @@ typedef struct HdrOutputs {
                                    (selected ICI scale; 0 where NaN) */
 } HdrOutputs;
 
-/* Bytes of device workspace hdr_lpa_reconstruct needs for this output size. */
-int hdr_lpa_workspace_bytes(int out_w, int out_h, size_t *bytes);
+/* Bytes of device workspace hdr_lpa_reconstruct needs for these sensors and
+ * this output size (work list + per-frame radiometric phase planes). */
+int hdr_lpa_workspace_bytes(const HdrSensor *sensors, int n_sensors, int out_w, int out_h,
+                            size_t *bytes);
 
 /*
  * Reconstruct one HDR frame on the output grid (out_w x out_h) whose pixel
  * centres are x_j = (j + 0.5) * ref_w / out_w - 0.5 in reference coordinates
  * (lpa.py:213-224).  Row band: only output rows [row_begin, row_end) are
  * computed (row_end <= 0 means out_h); outputs are still indexed over the
- * full frame.  `workspace` is device memory of hdr_lpa_workspace_bytes().
+ * full frame.  `workspace` is device memory of hdr_lpa_workspace_bytes(),
+ * 256-byte aligned.
  */
 int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
                         int out_w, int out_h, double ref_w, double ref_h,
@@ -163,6 +166,8 @@ int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream);
 int hdr_fp64_peak_probe(double *flops_per_s, void *stream);
 
 const char *hdr_lpa_status_string(int status);
+/* Detail of the last HDR_ERR_CUDA on the calling thread (CUDA error text). */
+const char *hdr_lpa_last_error(void);
 int hdr_lpa_abi_version(void);
 
 #ifdef __cplusplus

@@ -38,6 +38,7 @@ EXPORTED = (
     "hdr_lpa_slow_items",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
+    "hdr_lpa_last_error",
     "hdr_lpa_abi_version",
 )
 
@@ -118,7 +119,8 @@ def lib():
     with _lock:
         if _lib is None:
             L = ctypes.CDLL(str(build()))
-            L.hdr_lpa_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int,
+            L.hdr_lpa_workspace_bytes.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_int,
+                                                  ctypes.c_int, ctypes.c_int,
                                                   ctypes.POINTER(ctypes.c_size_t)]
             L.hdr_lpa_reconstruct.argtypes = [
                 ctypes.POINTER(HdrSensor), ctypes.c_int, ctypes.POINTER(HdrParams),
@@ -135,10 +137,11 @@ def lib():
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
             L.hdr_lpa_status_string.restype = ctypes.c_char_p
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]
+            L.hdr_lpa_last_error.restype = ctypes.c_char_p
             for name in EXPORTED:
-                if name != "hdr_lpa_status_string":
+                if name not in ("hdr_lpa_status_string", "hdr_lpa_last_error"):
                     getattr(L, name).restype = ctypes.c_int
-            if L.hdr_lpa_abi_version() != 1:
+            if L.hdr_lpa_abi_version() != 2:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L
         return _lib
@@ -155,4 +158,4 @@ def check(status: int, what: str) -> None:
         raise ShapeMismatchError(msg)
     if status in (HDR_ERR_ARG, HDR_ERR_WORKSPACE):
         raise ValueError(msg)
-    raise RuntimeError(msg)
+    raise RuntimeError(f"{msg} ({lib().hdr_lpa_last_error().decode()})")

@@ -33,7 +33,8 @@
 
 namespace hdrlpa {
 
-constexpr int TW = 32, TH = 8, NT = TW * TH;
+constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per tile pixel
+
 // workspace layout: [header: work counter][pre-computed taps][work items]
 static const size_t WS_HEADER = 256;
 static const size_t WS_TAPS = 64 * 1024;  // <= 2730 taps
@@ -111,8 +112,7 @@ struct TileSweep {
             const int pm = S.phmask[c];
             if (!pm) continue;
             const int ox = org[s][0], oy = org[s][1];
-            const double *vals = (const double *)(sm + S.off_val);
-            const float *ivs = (const float *)(sm + S.off_iv);
+            const float2 *vi = (const float2 *)(sm + S.off_vi);
             const double *tx0 = (const double *)(sm + S.off_tx0);
             const double *ty4 = (const double *)(sm + S.off_ty4);
             const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
@@ -154,15 +154,15 @@ struct TileSweep {
                                 const double d2 = __dadd_rn(cdxx[i], dyy);
                                 if constexpr (BRANCHY) {
                                     if (d2 <= r2) {
-                                        const float iv = ivs[rb + i];
-                                        if (iv > 0.f)
-                                            body(true, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy,
+                                        const float2 e = vi[rb + i];
+                                        if (e.y > 0.f)
+                                            body(true, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy,
                                                  (float)d2);
                                     }
                                 } else {
-                                    const float iv = ivs[rb + i];
-                                    const bool ok = (d2 <= r2) && (iv > 0.f);
-                                    body(ok, vals[rb + i], iv, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                    const float2 e = vi[rb + i];
+                                    const bool ok = (d2 <= r2) && (e.y > 0.f);
+                                    body(ok, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy, (float)d2);
                                 }
                             }
                         }
@@ -192,8 +192,8 @@ struct TileSweep {
                             const float fx = fmaf(a0, ex, a1 * ey), fy = fmaf(a3, ex, a4 * ey);
                             if (fmaf(fx, fx, fy * fy) > r2hi) continue;
                             const int k = rb + (x >> 1);
-                            const float iv = ivs[k];
-                            if (!(iv > 0.f)) continue;
+                            const float2 e = vi[k];
+                            if (!(e.y > 0.f)) continue;
                             const int lx = x - ox;
                             const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
                             const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
@@ -201,7 +201,7 @@ struct TileSweep {
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);
                             if (d2 > r2) continue;
-                            body(true, vals[k], iv, dx, dy, dxx, dyy, (float)d2);
+                            body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
                         }
                     }
                 }
@@ -419,6 +419,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
         "r"(bytes)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(
+                     smem_addr(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -465,76 +470,49 @@ __device__ __forceinline__ void tile_bounds(const DevParams &P, int t, int &tx0,
     ty1 = min(ty0 + TH, P.row_end) - 1;
 }
 
-// Thread 0: origins of tile t's staged regions and, with TMA, one bulk tensor
-// copy per sensor into raw buffer b, completing on mbarrier b.
-__device__ __forceinline__ void stage_issue(const DevParams &P, unsigned char *sm, int t, int b,
-                                            int (*org)[2], uint64_t *bar) {
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// Thread 0: region origins of tile t and one 3-D TMA copy per sensor of the
+// four (f_hat, 1/den) phase planes' staged regions into plane buffer `pb`,
+// completing on `full` (arrive + expect_tx).
+__device__ __forceinline__ void stage_issue(const DevParams &P, unsigned char *pb, int t,
+                                            int (*org)[2], uint64_t *full) {
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
     uint32_t bytes = 0;
     for (int s = 0; s < P.n_sensors; ++s) {
         region_origin(P.s[s], P, tx0, ty0, tx1, ty1, org[s][0], org[s][1]);
-        bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 2);
+        bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
     }
-    if (P.use_tma) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, bytes);
-        for (int s = 0; s < P.n_sensors; ++s)
-            tma_load_2d(sm + P.s[s].off_raw[b], &P.tmap[s], org[s][0], org[s][1], bar);
-    }
+    mbar_expect_tx(full, bytes);
+    for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
+        tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
 }
 
-// All threads: raw buffer b -> (f_hat, 1/den) Bayer phase planes + exact
-// float64 coordinate tables of the regions.
-__device__ __forceinline__ void stage_convert(const DevParams &P, unsigned char *sm, int b,
-                                              const int (*org)[2]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = NT / 32;
+// All threads: exact float64 coordinate tables of the staged regions.
+__device__ __forceinline__ void stage_tables(const DevParams &P, unsigned char *pb,
+                                             const int (*org)[2]) {
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
         const int ox = org[s][0], oy = org[s][1];
-        const int rw = S.rw, rh = S.rh, pw = rw >> 1, plane = pw * (rh >> 1);
-        const uint16_t *rawb = (const uint16_t *)(sm + S.off_raw[b]);
-        double *vals = (double *)(sm + S.off_val);
-        float *ivs = (float *)(sm + S.off_iv);
-        if (!P.use_tma) {  // unaligned pitch: cooperative copy into the raw buffer first
-            uint16_t *rw_b = (uint16_t *)(sm + S.off_raw[b]);
-            for (int ly = warp; ly < rh; ly += NW) {
-                const int y = oy + ly;
-                for (int lx = lane; lx < rw; lx += 32) {
-                    const int x = ox + lx;
-                    uint16_t v = 0;
-                    if (x >= 0 && y >= 0 && x < S.width && y < S.height)
-                        v = __ldg(S.raw + (size_t)y * S.pitch + x);
-                    rw_b[ly * rw + lx] = v;
-                }
-            }
-            __syncwarp();
-        }
-        for (int ly = warp; ly < rh; ly += NW) {
-            const int y = oy + ly;
-            const bool yin = y >= 0 && y < S.height;
-            for (int lx = lane; lx < rw; lx += 32) {
-                const int x = ox + lx;
-                float2 e = make_float2(0.f, 0.f);
-                if (yin && x >= 0 && x < S.width)
-                    e = radiance_from_raw(S, (int)rawb[ly * rw + lx], x, y, P.use_sigma);
-                const int k = ((ly & 1) * 2 + (lx & 1)) * plane + (ly >> 1) * pw + (lx >> 1);
-                vals[k] = (double)e.x;
-                ivs[k] = e.y;
-            }
-        }
         // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y) (exact,
         // since fl(T01*y) = fl(T10*x) = 0); otherwise the four partial products.
-        double *tx0t = (double *)(sm + S.off_tx0), *tx3t = (double *)(sm + S.off_tx3);
-        double *ty1t = (double *)(sm + S.off_ty1), *ty4t = (double *)(sm + S.off_ty4);
-        for (int i = threadIdx.x; i < rw; i += NT) {
+        double *tx0t = (double *)(pb + S.off_tx0), *tx3t = (double *)(pb + S.off_tx3);
+        double *ty1t = (double *)(pb + S.off_ty1), *ty4t = (double *)(pb + S.off_ty4);
+        for (int i = threadIdx.x; i < S.rw; i += NT) {
             const double xd = (double)(ox + i);
             const double a = __dmul_rn(S.T[0], xd);
             tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
             tx3t[i] = __dmul_rn(S.T[3], xd);
         }
-        for (int i = threadIdx.x; i < rh; i += NT) {
+        for (int i = threadIdx.x; i < S.rh; i += NT) {
             const double yd = (double)(oy + i);
             const double bb = __dmul_rn(S.T[4], yd);
             ty1t[i] = __dmul_rn(S.T[1], yd);
@@ -549,37 +527,35 @@ __device__ __forceinline__ void stage_convert(const DevParams &P, unsigned char 
 // the tap list (the samples and weights are the reference's: DESIGN.md s3).
 template <int ORDER>
 __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
-                                                const int (*org)[2], int c, int px, int py,
-                                                Acc<NC<ORDER>::P> &acc) {
+                                                const Tap *taps, const int (*org)[2], int c,
+                                                int px, int py, Acc<NC<ORDER>::P> &acc) {
     acc.zero();
-    const Tap *taps = (const Tap *)(sm + P.off_taps);
     const int cls = ((py & 1) << 1) | (px & 1);
     for (int s = 0; s < P.n_sensors; ++s) {
         const int n = P.pat_cnt[s][c][py & 1];
         if (!n) continue;
         const DevSensor &S = P.s[s];
         const Tap *tp = taps + P.pat_off[s][c][cls];
-        const double *vals = (const double *)(sm + S.off_val);
-        const float *ivs = (const float *)(sm + S.off_iv);
+        const float2 *vi = (const float2 *)(sm + S.off_vi);
         const int pw = S.rw >> 1;
         // base: the pixel's own position in its phase plane (origins are even)
         const int base = ((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1);
         for (int t = 0; t < n; ++t) {
             const Tap T = tp[t];
             const int k = base + T.delta;
-            const float iv = ivs[k];
-            const bool ok = iv > 0.f && T.W > 0.f;
-            const float w = ok ? T.W * iv : 0.f;
+            const float2 e = vi[k];
+            const bool ok = e.y > 0.f && T.W > 0.f;
+            const float w = ok ? T.W * e.y : 0.f;
             const double dxx = ORDER >= 2 ? __dmul_rn(T.dx, T.dx) : 0.0;
             const double dyy = ORDER >= 2 ? __dmul_rn(T.dy, T.dy) : 0.0;
-            acc.add((double)w, ok ? vals[k] : 0.0, T.dx, T.dy, dxx, dyy, ok ? 1 : 0);
+            acc.add((double)w, ok ? (double)e.x : 0.0, T.dx, T.dy, dxx, dyy, ok ? 1 : 0);
         }
     }
 }
 
 template <int ORDER, bool ICI, int MAXC, bool PAT>
-__device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm, int t,
-                                             const int (*org)[2]) {
+__device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
+                                             const Tap *taps, int t, const int (*org)[2]) {
     constexpr int PN = NC<ORDER>::P;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
@@ -610,7 +586,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
             } else {
                 Acc<PN> acc;
                 if constexpr (PAT)
-                    accumulate_taps<ORDER>(P, sm, org, c, px, py, acc);
+                    accumulate_taps<ORDER>(P, sm, taps, org, c, px, py, acc);
                 else
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 Fit fit;
@@ -633,38 +609,57 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     }
 }
 
+// Persistent kernel.  The raw frames were converted once per frame into
+// (f_hat, 1/den) phase planes by radiance_phase_kernel; each tile's staged
+// regions are TMA-loaded from them, double-buffered: while tile t is fitted
+// from buffer b, the copies for tile t+1 land in buffer b^1.
 template <int ORDER, bool ICI, int MAXC, bool PAT>
 __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
-    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t bar_full[2];
     const int ntiles = P.tiles_x * P.tiles_y;
-    int t = blockIdx.x;
+    const Tap *taps = (const Tap *)(smem + P.off_taps);
+    unsigned char *planes = smem + P.plane_base;
     if (PAT) {
         const uint32_t *src = (const uint32_t *)P.taps;
         uint32_t *dst = (uint32_t *)(smem + P.off_taps);
         for (int i = threadIdx.x; i < P.n_taps * (int)(sizeof(Tap) / 4); i += NT) dst[i] = src[i];
     }
+    int t = blockIdx.x;
     if (threadIdx.x == 0) {
-        if (P.use_tma) {
-            mbar_init(&s_bar[0], 1);
-            mbar_init(&s_bar[1], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        if (t < ntiles) stage_issue(P, smem, t, 0, s_org[0], &s_bar[0]);
+        mbar_init(&bar_full[0], 1);
+        mbar_init(&bar_full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (t < ntiles) stage_issue(P, planes, t, s_org[0], &bar_full[0]);
     }
     __syncthreads();
-    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
-        const int b = it & 1;
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        const int b = i & 1;
+        unsigned char *pb = planes + b * P.buf_stride;
         const int tn = t + gridDim.x;
-        // prefetch the next tile while this one is converted and fitted
-        if (threadIdx.x == 0 && tn < ntiles) stage_issue(P, smem, tn, b ^ 1, s_org[b ^ 1], &s_bar[b ^ 1]);
-        if (P.use_tma) mbar_wait(&s_bar[b], (uint32_t)((it >> 1) & 1));
-        stage_convert(P, smem, b, s_org[b]);
+        // buffer b^1 was last read in iteration i-1 (closed by its trailing barrier)
+        if (threadIdx.x == 0 && tn < ntiles)
+            stage_issue(P, planes + (b ^ 1) * P.buf_stride, tn, s_org[b ^ 1], &bar_full[b ^ 1]);
+        stage_tables(P, pb, s_org[b]);
+        mbar_wait(&bar_full[b], (uint32_t)((i >> 1) & 1));
         __syncthreads();
-        tile_compute<ORDER, ICI, MAXC, PAT>(P, smem, t, s_org[b]);
+        tile_compute<ORDER, ICI, MAXC, PAT>(P, pb, taps, t, s_org[b]);
         __syncthreads();
     }
+}
+
+// Per-frame radiometric pre-pass: every raw pixel converted once into the
+// de-interleaved phase planes (radiometry.py:303-336 for the whole frame);
+// out-of-frame padding gets 1/den = 0 (no sample).  HBM-bound.
+__global__ void radiance_phase_kernel(const __grid_constant__ DevParams P) {
+    const int s = blockIdx.z >> 2, ph = blockIdx.z & 3;
+    const DevSensor &S = P.s[s];
+    const int j = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S.pwg || j >= S.phg) return;
+    const int x = 2 * i + (ph & 1), y = 2 * j + (ph >> 1);
+    S.phase[((size_t)ph * S.phg + j) * S.pwg + i] = radiance_sample(S, x, y, P.use_sigma);
 }
 
 // ---------------------------------------------------------------------------
@@ -770,9 +765,17 @@ static int fill_sensor(const HdrSensor &h, DevSensor &d) {
     return HDR_OK;
 }
 
+static thread_local char g_last_error[256] = "";
+
+static int cuda_fail(const char *where) {
+    const cudaError_t e = cudaGetLastError();
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+    return HDR_ERR_CUDA;
+}
+
 static int set_smem_attr(const void *fn, int bytes) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    return e == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+    return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
 template <int ORDER, bool ICI, int MAXC, bool PAT = false>
@@ -784,10 +787,10 @@ static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem_bytes) != cudaSuccess ||
         per_sm < 1)
-        return HDR_ERR_CUDA;
+        return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
     lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P);
-    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_fast_kernel launch");
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -805,18 +808,18 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 2-D uint16 tensor map over a raw frame whose box is the staged region.
-static bool encode_raw_map(const DevSensor &d, CUtensorMap *map) {
+// 3-D float32 tensor map over one sensor's phase planes [4][phg][2*pwg]
+// (float2 = 2 floats); the box is the staged region (rw floats = rw/2 float2,
+// rh/2 rows, 4 phases).  The planes live in the workspace, 16-B aligned with
+// 16-B row pitch, so TMA is always applicable.
+static bool encode_phase_map(const DevSensor &d, CUtensorMap *map) {
     auto enc = tensor_map_encoder();
-    if (!enc) return false;
-    if (((uintptr_t)d.raw & 15) || ((size_t)d.pitch * 2) % 16 || d.rw > 256 || d.rh > 256 ||
-        (d.rw * 2) % 16)
-        return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)d.width, (cuuint64_t)d.height};
-    const cuuint64_t strides[1] = {(cuuint64_t)d.pitch * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)d.rw, (cuuint32_t)d.rh};
-    const cuuint32_t estr[2] = {1, 1};
-    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void *)d.raw, dims, strides, box, estr,
+    if (!enc || d.rw > 256 || (d.rh >> 1) > 256) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)d.pwg * 2, (cuuint64_t)d.phg, 4};
+    const cuuint64_t strides[2] = {(cuuint64_t)d.pwg * 8, (cuuint64_t)d.pwg * 8 * d.phg};
+    const cuuint32_t box[3] = {(cuuint32_t)d.rw, (cuuint32_t)(d.rh >> 1), 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)d.phase, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -838,7 +841,7 @@ static int launch_all(const DevParams &P, int tiles, int smem_bytes, int maxc, c
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     lpa_slow_kernel<ORDER><<<nsm * 4, 128, 0, st>>>(P);
-    if (cudaPeekAtLastError() != cudaSuccess) return HDR_ERR_CUDA;
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_slow_kernel launch");
     return HDR_OK;
 }
 
@@ -949,6 +952,8 @@ extern "C" {
 
 int hdr_lpa_abi_version(void) { return HDR_LPA_ABI_VERSION; }
 
+const char *hdr_lpa_last_error(void) { return g_last_error; }
+
 const char *hdr_lpa_status_string(int status) {
     switch (status) {
         case HDR_OK: return "ok";
@@ -961,11 +966,25 @@ const char *hdr_lpa_status_string(int status) {
     }
 }
 
-int hdr_lpa_workspace_bytes(int out_w, int out_h, size_t *bytes) {
+// Workspace layout: [header][pre-computed taps][phase planes of every sensor]
+// [work items].  Phase planes: per sensor [4][phg][pwg] float2 with
+// pwg = ceil(w/2) rounded up to even (16-B rows), phg = ceil(h/2).
+static size_t phase_bytes(const HdrSensor &s) {
+    const size_t pwg = (size_t)(((s.width + 1) / 2 + 1) & ~1), phg = (size_t)((s.height + 1) / 2);
+    return 4 * pwg * phg * sizeof(float2);
+}
+
+int hdr_lpa_workspace_bytes(const HdrSensor *sensors, int n_sensors, int out_w, int out_h,
+                            size_t *bytes) {
+    if (!sensors || n_sensors < 1 || n_sensors > MAXS) return HDR_ERR_ARG;
     if (out_w <= 0 || out_h <= 0 || !bytes) return HDR_ERR_ARG;
-    const size_t items = (size_t)out_w * out_h * 3;
     if ((size_t)out_w * out_h >= (1ull << 30)) return HDR_ERR_ARG;  // item packing
-    *bytes = WS_HEADER + WS_TAPS + items * sizeof(uint32_t);
+    size_t planes = 0;
+    for (int s = 0; s < n_sensors; ++s) {
+        if (sensors[s].width <= 0 || sensors[s].height <= 0) return HDR_ERR_ARG;
+        planes += phase_bytes(sensors[s]);
+    }
+    *bytes = WS_HEADER + WS_TAPS + planes + (size_t)out_w * out_h * 3 * sizeof(uint32_t);
     return HDR_OK;
 }
 
@@ -983,9 +1002,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     if (!(params->max_radius > 0) || !(params->cond_threshold > 0)) return HDR_ERR_ARG;
     if (row_end <= 0 || row_end > out_h) row_end = out_h;
     if (row_begin < 0 || row_begin >= row_end) return HDR_ERR_ARG;
-    size_t need = 0;
-    if (hdr_lpa_workspace_bytes(out_w, out_h, &need) != HDR_OK) return HDR_ERR_ARG;
-    if (workspace_bytes < need) return HDR_ERR_WORKSPACE;
+    if ((uintptr_t)workspace & 255) return HDR_ERR_ARG;
 
     DevParams P;
     memset(&P, 0, sizeof(P));
@@ -993,6 +1010,10 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         const int rc = fill_sensor(sensors[s], P.s[s]);
         if (rc != HDR_OK) return rc;
     }
+    size_t need = 0;
+    if (hdr_lpa_workspace_bytes(sensors, n_sensors, out_w, out_h, &need) != HDR_OK)
+        return HDR_ERR_ARG;
+    if (workspace_bytes < need) return HDR_ERR_WORKSPACE;
     P.n_sensors = n_sensors;
     P.order = params->order;
     P.n_scales = params->n_scales;
@@ -1028,11 +1049,20 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.count = out->count;
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
-    P.work_items = (uint32_t *)((char *)workspace + WS_HEADER + WS_TAPS);
+    char *wsp = (char *)workspace + WS_HEADER + WS_TAPS;
+    for (int s = 0; s < n_sensors; ++s) {
+        DevSensor &d = P.s[s];
+        d.phase = (float2 *)wsp;
+        d.pwg = ((d.width + 1) / 2 + 1) & ~1;
+        d.phg = (d.height + 1) / 2;
+        wsp += phase_bytes(sensors[s]);
+    }
+    P.work_items = (uint32_t *)wsp;
 
     // Staged region per sensor: tile extent in sensor space + 2 x window
-    // half-width (+ rounding/alignment slack).  Shared memory per sensor:
-    // f64 values and f32 1/den of the four phase planes, f64 coordinate tables.
+    // half-width (+ rounding/alignment slack).  Shared memory: pre-computed
+    // taps, then two plane buffers, each holding per sensor the four staged
+    // (f_hat, 1/den) phase planes and the f64 coordinate tables.
     int smem = 0, maxc = 1;
     auto take = [&](int bytes) {
         const int off = smem;
@@ -1051,14 +1081,6 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         rh += rh & 1;
         d.rw = rw;
         d.rh = rh;
-        d.off_raw[0] = take(rw * rh * 2);
-        d.off_raw[1] = take(rw * rh * 2);
-        d.off_val = take(rw * rh * 8);
-        d.off_iv = take(rw * rh * 4);
-        d.off_tx0 = take(rw * 8);
-        d.off_tx3 = take(rw * 8);
-        d.off_ty1 = take(rh * 8);
-        d.off_ty4 = take(rh * 8);
         // columns of one Bayer phase inside a window bbox: <= floor(r |N row 0|) + 2
         maxc = max(maxc, (int)floor(fastR * d.nrow0) + 2);
     }
@@ -1068,18 +1090,43 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         P.off_taps = take((int)(taps.size() * sizeof(Tap)));
         P.taps = (const Tap *)((char *)workspace + WS_HEADER);
     }
-    const int smem_bytes = smem;
+    P.plane_base = smem;
+    smem = 0;
+    for (int s = 0; s < n_sensors; ++s) {
+        DevSensor &d = P.s[s];
+        d.off_vi = take(d.rw * d.rh * 8);  // [4][rh/2][rw/2] float2
+        d.off_tx0 = take(d.rw * 8);
+        d.off_tx3 = take(d.rw * 8);
+        d.off_ty1 = take(d.rh * 8);
+        d.off_ty4 = take(d.rh * 8);
+    }
+    P.buf_stride = smem;
+    const int smem_bytes = P.plane_base + 2 * P.buf_stride;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
-    P.use_tma = 1;
-    for (int s = 0; s < n_sensors && P.use_tma; ++s)
-        if (!encode_raw_map(P.s[s], &P.tmap[s])) P.use_tma = 0;
+    for (int s = 0; s < n_sensors; ++s)
+        if (!encode_phase_map(P.s[s], &P.tmap[s])) {
+            snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled failed (sensor %d)", s);
+            return HDR_ERR_CUDA;
+        }
 
     cudaStream_t st = (cudaStream_t)stream;
     P.tiles_y = (row_end - row_begin + TH - 1) / TH;
     P.tiles_x = (out_w + TW - 1) / TW;
     const int tiles = P.tiles_x * P.tiles_y;
-    if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess) return HDR_ERR_CUDA;
-    if (P.pat && upload_taps(taps, (char *)workspace + WS_HEADER, st) != HDR_OK) return HDR_ERR_CUDA;
+    if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess)
+        return cuda_fail("cudaMemsetAsync");
+    if (P.pat && upload_taps(taps, (char *)workspace + WS_HEADER, st) != HDR_OK)
+        return cuda_fail("tap upload");
+    {  // per-frame radiometric pre-pass into the phase planes
+        int maxpw = 0, maxph = 0;
+        for (int s = 0; s < n_sensors; ++s) {
+            maxpw = max(maxpw, P.s[s].pwg);
+            maxph = max(maxph, P.s[s].phg);
+        }
+        dim3 grid((maxpw + 127) / 128, maxph, 4 * n_sensors);
+        radiance_phase_kernel<<<grid, 128, 0, st>>>(P);
+        if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("radiance_phase_kernel launch");
+    }
     int rc;
     switch (P.order) {
         case 0: rc = launch_all<0>(P, tiles, smem_bytes, maxc, st); break;

@@ -46,8 +46,9 @@ struct DevSensor {
     int planes;               // any calibration plane present
     // fast-path staging geometry
     int rw, rh;               // staged region (even), phase planes are (rh/2) x (rw/2)
-    int off_raw[2];           // byte offsets of the two raw uint16 staging buffers (TMA dst)
-    int off_val, off_iv;      // byte offsets in shared memory: f64 values, f32 1/den
+    int off_vi;               // byte offset (in a plane buffer) of the 4 staged phase planes
+    float2 *phase;            // global phase planes [4][phg][pwg] of (f_hat, 1/den) (workspace)
+    int pwg, phg;             // their padded width (float2 elements) and height
     int off_tx0, off_tx3;     // f64 tables fl(T00*x), fl(T10*x) over the region's columns
     int off_ty1, off_ty4;     // f64 tables fl(T01*y), fl(T11*y) over the region's rows
     float Tf[4];              // fp32 linear part (pre-test of rotated sensors)
@@ -63,11 +64,11 @@ struct Tap {
 };
 
 struct DevParams {
-    CUtensorMap tmap[MAXS];   // per-sensor 2-D uint16 tensor maps (box = staged region)
+    CUtensorMap tmap[MAXS];   // per-sensor 3-D maps over the phase planes (box = staged region)
     DevSensor s[MAXS];
     int n_sensors, order, n_scales, use_sigma;
     int out_w, out_h, row_begin, row_end;
-    int tiles_x, tiles_y, use_tma, pad0;
+    int tiles_x, tiles_y, pad0, pad1b;
     double sx, sy;            // ref_w / out_w, ref_h / out_h  (lpa.py:222-223)
     double r[3][MAXJ];        // min(3 sqrt(h), max_radius)     (lpa.py:353, _kernels.py:276-277)
     double r2[3][MAXJ];       // r * r
@@ -84,6 +85,7 @@ struct DevParams {
     int flags, pad1;
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, pad2;
+    int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
     const Tap *taps;                // device copy (in the workspace), staged into shared memory
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded

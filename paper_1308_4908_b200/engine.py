@@ -181,7 +181,8 @@ class DeviceRig:
         key = (out_w, out_h)
         if key not in self._workspaces:
             nbytes = ctypes.c_size_t()
-            N.check(N.lib().hdr_lpa_workspace_bytes(out_w, out_h, ctypes.byref(nbytes)),
+            N.check(N.lib().hdr_lpa_workspace_bytes(self._sensors, len(self.raws), out_w, out_h,
+                                                     ctypes.byref(nbytes)),
                     "hdr_lpa_workspace_bytes")
             self._workspaces[key] = torch.empty(int(nbytes.value), dtype=torch.uint8,
                                                 device=self.device)

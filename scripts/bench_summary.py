@@ -1,0 +1,19 @@
+"""Print the key fields of bench.py JSON lines (file or stdin)."""
+import json
+import sys
+
+src = open(sys.argv[1]) if len(sys.argv) > 1 else sys.stdin
+for line in src:
+    line = line.strip()
+    if not line.startswith("{"):
+        continue
+    j = json.loads(line)
+    if j.get("impl") == "reference":
+        print("reference", j["config"]["workload"], f"{j['value']:.4f} fps", j["cpu_baseline"]["cores"], "cores")
+        continue
+    r = j["roofline"]
+    print(f"{j['config']['workload']}: {j['value']:.1f} fps ({j['mpix_per_s']:.0f} Mpx/s) "
+          f"e2e {j['e2e']['value']:.1f} fps | kernel {r['kernel_ms']:.3f} ms, {r['bound']} "
+          f"{r['achieved']:.2f}/{r['peak']:.2f} {r['unit']} frac {r['frac']:.3f} | hbm frac "
+          f"{r['hbm']['frac']:.4f} | slow {j['slow_path_items']} | clocks {j['clocks']} | "
+          f"cpu {j['cpu_baseline']}")

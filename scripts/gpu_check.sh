@@ -1,5 +1,7 @@
 set -x
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -4
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-1200
-timeout 600 python bench.py --steps 10 --warmup 3 --workload cfg3 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-700
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_cfg2.json 2>gpurun_out/bench_cfg2.err
+timeout 600 python bench.py --steps 10 --warmup 3 --workload cfg3 --no-cpu-baseline > gpurun_out/bench_cfg3.json 2>gpurun_out/bench_cfg3.err
+python scripts/bench_summary.py gpurun_out/bench_cfg2.json
+python scripts/bench_summary.py gpurun_out/bench_cfg3.json

@@ -56,7 +56,7 @@ def test_struct_layouts_match_the_header(tmp_path):
 
 def test_abi_version_and_status_strings():
     L = N.lib()
-    assert L.hdr_lpa_abi_version() == 1
+    assert L.hdr_lpa_abi_version() == 2
     for code, text in ((0, "ok"), (1, "invalid argument"), (2, "invalid sensor configuration"),
                        (3, "dimension mismatch"), (4, "workspace too small"), (5, "CUDA error")):
         assert L.hdr_lpa_status_string(code).decode() == text
@@ -64,9 +64,16 @@ def test_abi_version_and_status_strings():
 
 def test_workspace_size():
     n = ctypes.c_size_t()
-    assert N.lib().hdr_lpa_workspace_bytes(2400, 1700, ctypes.byref(n)) == 0
-    assert n.value == 256 + 64 * 1024 + 2400 * 1700 * 3 * 4
-    assert N.lib().hdr_lpa_workspace_bytes(0, 10, ctypes.byref(n)) == N.HDR_ERR_ARG
+    s = (N.HdrSensor * 3)()
+    for k in range(3):
+        s[k].width, s[k].height = 2400, 1700
+    assert N.lib().hdr_lpa_workspace_bytes(s, 3, 2400, 1700, ctypes.byref(n)) == 0
+    phase = 4 * 1200 * 850 * 8  # four (f_hat, 1/den) float2 phase planes per sensor
+    assert n.value == 256 + 64 * 1024 + 3 * phase + 2400 * 1700 * 3 * 4
+    s[0].width = 2399  # odd width: phase planes padded to an even float2 count
+    assert N.lib().hdr_lpa_workspace_bytes(s, 1, 2400, 1700, ctypes.byref(n)) == 0
+    assert n.value == 256 + 64 * 1024 + 4 * 1200 * 850 * 8 + 2400 * 1700 * 3 * 4
+    assert N.lib().hdr_lpa_workspace_bytes(s, 3, 0, 10, ctypes.byref(n)) == N.HDR_ERR_ARG
 
 
 def _sensor(**kw):
