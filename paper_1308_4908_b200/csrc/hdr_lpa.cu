@@ -74,8 +74,12 @@ struct GlobalSweep {
                 for (int y = ys; y <= yhi; y += 2) {
                     const double yd = (double)y;
                     const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
+                    const bool yin = y >= 0 && y < S.height;
+                    const float2 *row = S.phase + ((size_t)ph * S.phg + (y >> 1)) * S.pwg;
                     for (int x = xs; x <= xhi; x += 2) {
-                        const float2 e = radiance_sample(S, x, y, P.use_sigma);
+                        // the per-frame phase planes hold radiance_sample(S, x, y)
+                        const float2 e = (yin && x >= 0 && x < S.width) ? __ldg(row + (x >> 1))
+                                                                         : make_float2(0.f, 0.f);
                         if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
                         const double xd = (double)x;
                         const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
@@ -484,16 +488,20 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 // completing on `full` (arrive + expect_tx).
 __device__ __forceinline__ void stage_issue(const DevParams &P, unsigned char *pb, int t,
                                             int (*org)[2], uint64_t *full) {
+    // warp 0: lane s computes sensor s's region origin, lane 0 issues the copies
+    const int lane = threadIdx.x & 31;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
-    uint32_t bytes = 0;
-    for (int s = 0; s < P.n_sensors; ++s) {
-        region_origin(P.s[s], P, tx0, ty0, tx1, ty1, org[s][0], org[s][1]);
-        bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
+    if (lane < P.n_sensors)
+        region_origin(P.s[lane], P, tx0, ty0, tx1, ty1, org[lane][0], org[lane][1]);
+    __syncwarp();
+    if (lane == 0) {
+        uint32_t bytes = 0;
+        for (int s = 0; s < P.n_sensors; ++s) bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
+        mbar_expect_tx(full, bytes);
+        for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
+            tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
     }
-    mbar_expect_tx(full, bytes);
-    for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
-        tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
 }
 
 // All threads: exact float64 coordinate tables of the staged regions.
@@ -631,15 +639,16 @@ __global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__
         mbar_init(&bar_full[0], 1);
         mbar_init(&bar_full[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (t < ntiles) stage_issue(P, planes, t, s_org[0], &bar_full[0]);
     }
     __syncthreads();
+    if (threadIdx.x < 32 && t < ntiles) stage_issue(P, planes, t, s_org[0], &bar_full[0]);
+    __syncthreads();  // s_org[0] visible to every thread
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
         const int b = i & 1;
         unsigned char *pb = planes + b * P.buf_stride;
         const int tn = t + gridDim.x;
         // buffer b^1 was last read in iteration i-1 (closed by its trailing barrier)
-        if (threadIdx.x == 0 && tn < ntiles)
+        if (threadIdx.x < 32 && tn < ntiles)
             stage_issue(P, planes + (b ^ 1) * P.buf_stride, tn, s_org[b ^ 1], &bar_full[b ^ 1]);
         stage_tables(P, pb, s_org[b]);
         mbar_wait(&bar_full[b], (uint32_t)((i >> 1) & 1));
