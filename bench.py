@@ -66,53 +66,68 @@ def _dist_init():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every ~2 ms in a
+    background thread while the timed region runs (nvidia-smi's 100 ms period
+    is longer than a short timed region)."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.path = Path(f"/tmp/hdrlpa_clocks_{os.getpid()}.csv")
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, device_index: int):
+        self.index = device_index
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
-        time.sleep(0.3)
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # pragma: no cover - NVML is in the image
+            self.error = str(e)
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if bits & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+                time.sleep(0.002)
+
+        self._thread = threading.Thread(target=poll, daemon=True)
+        self._thread.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait()
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join()
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in self.path.read_text().strip().splitlines()]
-        except OSError:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            try:
-                sm.append(float(r[0]))
-                smax = float(r[1])
-                for n, v in zip(names, r[3:7]):
-                    if "Active" in v and "Not" not in v:
-                        reasons.add(n)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = self.samples
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml"}
 
 
-REF_BAND_ROWS = {"cfg1": None, "cfg2": 400, "cfg3": 32, "cfg4": 32}
+REF_BAND_ROWS = {"cfg1": None, "cfg2": 200, "cfg3": 24, "cfg4": 24}
 _SIM_CACHE = {}
 
 
@@ -269,7 +284,16 @@ def run_ours(args, wl, world, rank, local):
         bound, peak, peak_src = "fp64", peak64, "measured in-run DFMA probe (hdr_fp64_peak_probe)"
     in_bytes = sum(t.numel() * 2 for t in frame_sets[0])
     out_bytes = out_w * out_h * 12
-    hbm_achieved = (in_bytes + out_bytes) / (ms_fast * 1e-3) / 1e9
+    # the fast kernel reads the per-frame (f_hat, 1/den) phase planes (8 B per sensor pixel)
+    # written by the radiometric pre-pass, and writes the RGB frame
+    planes_bytes = sum(t.numel() * 8 for t in frame_sets[0])
+    traffic, traffic_src = None, None
+    tpath = ROOT / "profiles" / "r01_traffic.json"
+    if tpath.exists():
+        tj = json.loads(tpath.read_text()).get(args.workload)
+        if tj:
+            traffic, traffic_src = tj["traffic_bytes"], tj["source"]
+    hbm_achieved = (planes_bytes + out_bytes) / (ms_fast * 1e-3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
 
@@ -320,13 +344,16 @@ def run_ours(args, wl, world, rank, local):
                        "parallelism": f"frame-parallel x{world}"},
             "mpix_per_s": mpx,
             "roofline": {"bound": bound, "achieved": achieved / 1e12, "peak": peak / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "bytes/launch (DRAM read+write, ncu)",
+                         "traffic_source": traffic_src,
                          "peak_source": peak_src, "kernel": "lpa_fast_kernel",
                          "kernel_ms": ms_fast, "inside_samples_per_launch": n_inside,
                          "flop64_per_launch": flop64, "flop32_per_launch": flop32,
                          "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": peaks["hbm_gbs"],
                                  "frac": hbm_achieved / peaks["hbm_gbs"],
-                                 "algorithmic_bytes": in_bytes + out_bytes}},
+                                 "algorithmic_bytes": planes_bytes + out_bytes,
+                                 "pipeline_bytes_per_frame": in_bytes + 2 * planes_bytes + out_bytes}},
             "slow_path_items": slow_items,
             "cpu_baseline": cpu,
             "e2e": {"value": fps_e2e, "unit": "frames/s", "h2d_bytes_per_step": pipe.h2d_bytes,
@@ -350,8 +377,8 @@ def ctypes_probe(N, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
