@@ -114,11 +114,13 @@ def build(force: bool = False) -> Path:
 
 
 def lib():
-    """The loaded library (built first if missing or stale)."""
+    """The loaded library (built first if missing or stale).  HDR_LPA_LIB may
+    point at an alternative build of the same sources (experiments)."""
     global _lib
     with _lock:
         if _lib is None:
-            L = ctypes.CDLL(str(build()))
+            alt = os.environ.get("HDR_LPA_LIB")
+            L = ctypes.CDLL(alt if alt else str(build()))
             L.hdr_lpa_workspace_bytes.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_int,
                                                   ctypes.c_int, ctypes.c_int,
                                                   ctypes.POINTER(ctypes.c_size_t)]

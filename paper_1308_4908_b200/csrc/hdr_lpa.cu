@@ -103,14 +103,40 @@ struct GlobalSweep {
 // test is then one float64 add per candidate.  Rotated sensors pre-test
 // |d|^2 in fp32 (error < 1e-5 px^2, margin 1e-3) and run the exact float64
 // test only for candidates near or inside the disk.
+// Adapter: a per-sample body as a traversal policy (no row hooks).
+template <class Body>
+struct PerSample {
+    Body &body;
+    __device__ __forceinline__ void begin_row(double, double) {}
+    __device__ __forceinline__ void end_row(double, double) {}
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
+                                           double dxx, double dyy, float d2f) {
+        body(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        body(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+};
+
 template <int MAXC, bool BRANCHY>
 struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
     const int (*org)[2];
     double qx, qy;
+    // Per-sample traversal (same interface as GlobalSweep).
     template <class Body>
     __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
+        PerSample<Body> pol{body};
+        rows(c, r, r2, pol);
+    }
+
+    // Traversal with row hooks: for separable sensors every sample of a row
+    // shares dy, so a policy can accumulate per-row sums (begin_row / sample /
+    // end_row); rotated sensors go through pol.general() per sample.
+    template <class Pol>
+    __device__ __forceinline__ void rows(int c, double r, double r2, Pol &pol) const {
         for (int s = 0; s < P.n_sensors; ++s) {
             const DevSensor &S = P.s[s];
             const int pm = S.phmask[c];
@@ -150,6 +176,7 @@ struct TileSweep {
                             const double dyy = __dmul_rn(dy, dy);
                             if (dyy > r2) continue;
                             const int rb = colbase + (ly >> 1) * pw;
+                            pol.begin_row(dy, dyy);
                             // orders 0-1: branch-free over the row (candidates outside the
                             // disk or without a sample contribute with weight 0); order 2
                             // (27 DFMA per sample) only visits the samples inside.
@@ -160,15 +187,17 @@ struct TileSweep {
                                     if (d2 <= r2) {
                                         const float2 e = vi[rb + i];
                                         if (e.y > 0.f)
-                                            body(true, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy,
-                                                 (float)d2);
+                                            pol.sample(true, (double)e.x, e.y, cdx[i], dy, cdxx[i],
+                                                       dyy, (float)d2);
                                     }
                                 } else {
                                     const float2 e = vi[rb + i];
                                     const bool ok = (d2 <= r2) && (e.y > 0.f);
-                                    body(ok, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                    pol.sample(ok, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy,
+                                               (float)d2);
                                 }
                             }
+                            pol.end_row(dy, dyy);
                         }
                     }
                 }
@@ -205,7 +234,7 @@ struct TileSweep {
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);
                             if (d2 > r2) continue;
-                            body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                            pol.general(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
                         }
                     }
                 }
@@ -230,9 +259,126 @@ __device__ __forceinline__ double window_w(const DevParams &P, int c, int k, dou
     }
 }
 
+// Row-factored moments (fast path, separable sensors).  Along a sensor row
+// dy is constant, so with phi_a = dx^i_a dy^j_a the row contributes
+//   A_ab += dy^(j_a+j_b) * S_(i_a+i_b),  b_a += dy^j_a * T_i_a,
+//   S_n = sum w dx^n (n <= 2*ORDER),  T_n = sum w y dx^n (n <= ORDER),
+// i.e. 2*ORDER+1 + ORDER+1 sums per sample instead of P(P+1)/2 + P.
+// Rotated sensors accumulate per sample.
+template <int ORDER>
+struct RowMoments {
+    static constexpr int PN = NC<ORDER>::P;
+    Acc<PN> &acc;
+    float hl;
+    double S[2 * ORDER + 1], T[ORDER + 1];
+    int cnt;
+    __device__ __forceinline__ void begin_row(double, double) {
+#pragma unroll
+        for (int n = 0; n <= 2 * ORDER; ++n) S[n] = 0.0;
+#pragma unroll
+        for (int n = 0; n <= ORDER; ++n) T[n] = 0.0;
+        cnt = 0;
+    }
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double,
+                                           double, double, float d2f) {
+        const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
+        const double w = (double)w32, y = ok ? v : 0.0;
+        double p = w;
+#pragma unroll
+        for (int n = 0; n <= 2 * ORDER; ++n) {
+            S[n] += p;
+            if (n <= ORDER) T[n] = fma(p, y, T[n]);
+            if (n < 2 * ORDER) p *= dx;
+        }
+        cnt += ok ? 1 : 0;
+    }
+    __device__ __forceinline__ void end_row(double dy, double dyy) {
+        // basis exponents (i, j): order 1: (0,0) (1,0) (0,1); order 2 adds (2,0) (1,1) (0,2)
+        constexpr int I[6] = {0, 1, 0, 2, 1, 0}, J[6] = {0, 0, 1, 0, 1, 2};
+        double dp[5];
+        dp[0] = 1.0;
+        dp[1] = dy;
+        dp[2] = dyy;
+        dp[3] = dyy * dy;
+        dp[4] = dyy * dyy;
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < PN; ++a) {
+            acc.b[a] = (J[a] == 0) ? acc.b[a] + T[I[a]] : fma(T[I[a]], dp[J[a]], acc.b[a]);
+#pragma unroll
+            for (int bb = a; bb < PN; ++bb) {
+                const int jj = J[a] + J[bb];
+                acc.A[k] = jj == 0 ? acc.A[k] + S[I[a] + I[bb]] : fma(S[I[a] + I[bb]], dp[jj], acc.A[k]);
+                ++k;
+            }
+        }
+        acc.count += cnt;
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
+        acc.add((double)w, ok ? v : 0.0, dx, dy, dxx, dyy, ok ? 1 : 0);
+    }
+};
+
+// Row-factored variance sweep (ICI, fast path): phi.g = c0(dy) + dx (c1(dy) + g3 dx).
+template <int ORDER>
+struct RowVariance {
+    const double *g;
+    float hl;
+    bool sig;
+    double v, c0, c1;
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        c0 = g[0];
+        c1 = 0.0;
+        if (ORDER >= 1) {
+            c0 += g[2] * dy;
+            c1 = g[1];
+        }
+        if (ORDER >= 2) {
+            c0 += g[5] * dyy;
+            c1 += g[4] * dy;
+        }
+    }
+    __device__ __forceinline__ void end_row(double, double) {}
+    __device__ __forceinline__ void sample(bool ok, double, float iv, double dx, double, double,
+                                           double, float d2f) {
+        const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+        const double t = (double)(sig ? W * W : W * W * iv);
+        double pg = c0;
+        if (ORDER == 1) pg = fma(dx, c1, c0);
+        if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
+        if (ok) v = fma(t, pg * pg, v);
+    }
+    __device__ __forceinline__ void general(bool ok, double, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+        const double t = (double)(sig ? W * W : W * W * iv);
+        double pg = g[0];
+        if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
+        if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
+        if (ok) v = fma(t, pg * pg, v);
+    }
+};
+
+template <class Sweep>
+struct HasRows {
+    static constexpr bool value = false;
+};
+template <int MAXC, bool BRANCHY>
+struct HasRows<TileSweep<MAXC, BRANCHY>> {
+    static constexpr bool value = true;
+};
+
 template <int ORDER, bool EXACT, class Sweep>
 __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, double r, double r2,
                                            const Sweep &sweep, Acc<NC<ORDER>::P> &acc) {
+    if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
+        acc.zero();
+        RowMoments<ORDER> pol{acc, P.hl[c][k]};
+        sweep.rows(c, r, r2, pol);
+        return;
+    }
     acc.zero();
     if constexpr (EXACT) {
         const double hi = P.hinv[c][k];
@@ -257,6 +403,11 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
 template <int ORDER, bool EXACT, class Sweep>
 __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, const Sweep &sweep,
                                                const double *g) {
+    if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
+        RowVariance<ORDER> pol{g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0};
+        sweep.rows(c, P.r[c][k], P.r2[c][k], pol);
+        return pol.v;
+    }
     const bool sig = P.use_sigma;
     const double hi = P.hinv[c][k];
     const float hl = P.hl[c][k];
@@ -621,8 +772,12 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 // (f_hat, 1/den) phase planes by radiance_phase_kernel; each tile's staged
 // regions are TMA-loaded from them, double-buffered: while tile t is fitted
 // from buffer b, the copies for tile t+1 land in buffer b^1.
+#ifndef HDR_O2_MINBLOCKS
+#define HDR_O2_MINBLOCKS 2
+#endif
 template <int ORDER, bool ICI, int MAXC, bool PAT>
-__global__ void __launch_bounds__(NT, 2) lpa_fast_kernel(const __grid_constant__ DevParams P) {
+__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : 2))
+    lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
     __shared__ __align__(8) uint64_t bar_full[2];
