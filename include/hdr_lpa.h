@@ -138,6 +138,40 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
                         void *workspace, size_t workspace_bytes, void *stream);
 
 /*
+ * CALPA (reference steering.py:214-248): the steering field of the
+ * structure-adaptive second pass, device float64 planes over the output grid.
+ */
+typedef struct HdrSteering {
+    const double *theta;        /* orientation (rad) */
+    const double *sigma;        /* elongation >= 1   */
+    const double *gamma;        /* scaling > 0       */
+} HdrSteering;
+
+/*
+ * Steered reconstruction (replaces lpa.py:379-408 reconstruct_channel with
+ * steering=SteeringField.kernel_inputs(...) and _kernels.py:203-300
+ * lpa_evaluate two_phase=True): per pixel and channel the anisotropic window
+ * Hinv = C/h, r0 = 3 sqrt(h sigma/gamma) is tried first, then the isotropic
+ * one, each with the radius ladder, for order M..0.  params->n_scales must be 1.
+ */
+int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
+                                const HdrParams *params, const HdrSteering *steering, int out_w,
+                                int out_h, double ref_w, double ref_h, int row_begin, int row_end,
+                                const HdrOutputs *out, void *workspace, size_t workspace_bytes,
+                                void *stream);
+
+/*
+ * Steering field from gradient planes (replaces _kernels.py:310-392
+ * steering_field_kernel via steering.py:177-203 compute_steering_field):
+ * gx, gy are float32 [height][width] (divided by gradient_scale inside);
+ * theta, sigma, gamma float64 outputs.
+ */
+int hdr_steering_field(const float *gx, const float *gy, int width, int height,
+                       int gradient_window, double lambda1, double lambda2, double alpha,
+                       double sigma_max, double gradient_scale, double *theta, double *sigma,
+                       double *gamma, void *stream);
+
+/*
  * Saturation (+ defective) mask of one sensor as bit-planes: bit (x % 32) of
  * out_bits[y * words_per_row + x / 32] is set where the pixel is discarded.
  * words_per_row >= ceil(width / 32).

@@ -166,7 +166,41 @@ def main():
            ReconstructionParams(order=2, scale=0.5),
            note="saturated scene: radius ladder, order fallback, NaN pixels")
 
+    # 7. CALPA (structure-adaptive second pass): fig6 rig, 96x64, order 1, alpha 0.005
+    from hdrfuse.steering import AdaptiveParams, calpa_reconstruct
+    W, H = 96, 64
+    gt = hdr_test_scene(W, H)
+    rig = fig6_rig(W, H, seed=11)
+    frames, cals, _ = simulate_and_sample(gt, rig)
+    samples = hf.frames_to_samples(frames, list(rig.sensors), cals)
+    ap = AdaptiveParams(alpha=0.005, base=ReconstructionParams(order=1, scale=0.7))
+    img, fld = calpa_reconstruct(samples, (W, H), ap, return_field=True)
+    np.savez_compressed(OUT / "calpa_fig6_96x64_o1.npz",
+                        **{f"raw{k}": f.data for k, f in enumerate(frames)}, rgb=img.data,
+                        theta=fld.theta, sigma=fld.sigma, gamma=fld.gamma)
+    calpa_case = {
+        "note": "calpa_reconstruct (steering.py:214-248), fig6 rig",
+        "sensors": [{
+            "sensor_id": int(c.sensor_id), "exposure_time": c.exposure_time, "gain": c.gain,
+            "exposure_scaling": c.exposure_scaling, "transform": c.transform.ravel().tolist(),
+            "saturation_level": int(c.saturation_level), "bit_depth": int(c.bit_depth),
+            "pattern": c.pattern.value, "black_level": c.black_level, "defective": None,
+        } for c in rig.sensors],
+        "calibration": [{"bias": float(c.bias.data.flat[0]),
+                         "readout_variance": float(c.readout_variance.data.flat[0]),
+                         "nonuniformity": float(c.nonuniformity.data.flat[0])} for c in cals],
+        "out_size": [W, H], "ref_size": None,
+        "params": {"order": 1, "scale": 0.7, "per_channel_scale": True,
+                   "max_support_radius": None, "cond_threshold": 1e8, "weight_mode": "variance"},
+        "adaptive": {"alpha": 0.005, "lambda1": 1.0, "lambda2": 0.001, "gradient_window": 9,
+                     "sigma_max": 50.0, "share_steering": True, "gradient_scale": None},
+        "sha256_rgb": sha(img.data), "sha256_theta": sha(fld.theta),
+        "sha256_sigma": sha(fld.sigma), "sha256_gamma": sha(fld.gamma),
+    }
+    print("calpa_fig6_96x64_o1", calpa_case["sha256_rgb"][:16])
+
     (OUT / "golden.json").write_text(json.dumps({
+        "calpa_cases": {"calpa_fig6_96x64_o1": calpa_case},
         "generator": "oracle/gen_golden.py (reference hdrfuse imported from /root/reference)",
         "pin9_sha256_reference_test": "ea1f273c7f4269a32d447bf53aede42b63b0c9f9ef74f9a0d044d5a75b8849af",
         "cases": cases}, indent=1))

@@ -583,3 +583,161 @@ int oracle_reconstruct_channel(const OSensor *sensors, int n_sensors, int channe
     free_index(&ix);
     return 0;
 }
+
+
+/* ==========================================================================
+ * CALPA (structure-adaptive second pass, reference steering.py)
+ * ======================================================================== */
+
+/* steering_field_kernel (_kernels.py:310-392): per output pixel, weighted
+ * gradient energy over a (2 half + 1)^2 window -> (theta, sigma, gamma).
+ * gx, gy are the gradient planes already divided by gradient_scale. */
+void oracle_steering_field(const double *gx, const double *gy, int w, int h, int half,
+                           double wstd, double lam1, double lam2, double alpha,
+                           double sigma_max, double *theta, double *sigma, double *gamma,
+                           int n_threads) {
+#ifdef _OPENMP
+    if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int yy = 0; yy < h; ++yy) {
+        for (int xx = 0; xx < w; ++xx) {
+            double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+            int n = 0;
+            for (int dy = -half; dy <= half; ++dy) {
+                int iy = yy + dy;
+                if (iy < 0 || iy >= h) continue;
+                for (int dx = -half; dx <= half; ++dx) {
+                    int ix = xx + dx;
+                    if (ix < 0 || ix >= w) continue;
+                    double g1 = gx[(int64_t)iy * w + ix], g2 = gy[(int64_t)iy * w + ix];
+                    if (!(isfinite(g1) && isfinite(g2))) continue;
+                    double wgt = exp(-(double)(dx * dx + dy * dy) / (2.0 * wstd * wstd));
+                    s11 += wgt * g1 * g1;
+                    s12 += wgt * g1 * g2;
+                    s22 += wgt * g2 * g2;
+                    ++n;
+                }
+            }
+            int64_t o = (int64_t)yy * w + xx;
+            if (n == 0) {
+                theta[o] = 0.0;
+                sigma[o] = 1.0;
+                gamma[o] = 1.0;
+                continue;
+            }
+            /* _eig2_minmax (_kernels.py:303-307) */
+            double m = 0.5 * (s11 + s22);
+            double d = hypot(0.5 * (s11 - s22), s12);
+            double lmin = m - d, lmax = m + d;
+            if (lmin < 0.0) lmin = 0.0;
+            double s1 = sqrt(lmax), s2 = sqrt(lmin);
+            double v1, v2;
+            if (fabs(s12) > 1e-300) {
+                v1 = s12;
+                v2 = lmin - s11;
+                if (v1 == 0.0 && v2 == 0.0) v1 = 1.0;
+            } else if (s11 <= s22) {
+                v1 = 1.0;
+                v2 = 0.0;
+            } else {
+                v1 = 0.0;
+                v2 = 1.0;
+            }
+            double th = atan2(v1, v2);
+            if (th <= -0.5 * M_PI)
+                th += M_PI;
+            else if (th > 0.5 * M_PI)
+                th -= M_PI;
+            double denom = s2 + lam1, sg;
+            if (denom == 0.0)
+                sg = (s1 + lam1 == 0.0) ? 1.0 : sigma_max;
+            else
+                sg = (s1 + lam1) / denom;
+            if (sg > sigma_max) sg = sigma_max;
+            theta[o] = th;
+            sigma[o] = sg;
+            gamma[o] = pow((s1 * s2 + lam2) / n, alpha);
+        }
+    }
+}
+
+/* lpa_evaluate with two_phase (_kernels.py:257-300): per order, the
+ * anisotropic window (per-query Hinv, r0) then the isotropic one, each with
+ * the radius ladder. */
+int oracle_reconstruct_channel_steered(const OSensor *sensors, int n_sensors, int channel,
+                                       const double *xs, int out_w, const double *ys,
+                                       int out_h, int order0, const double *an_h11,
+                                       const double *an_h12, const double *an_h22,
+                                       const double *an_r0, double iso_hinv, double iso_r0,
+                                       double max_radius, double cond_threshold,
+                                       int use_sigma, int n_threads, double *val, double *gx,
+                                       double *gy, uint8_t *outcome) {
+    OIndex ix;
+    build_index(sensors, n_sensors, channel, &ix);
+    int64_t m = (int64_t)out_w * out_h;
+    if (ix.n == 0) {
+        for (int64_t i = 0; i < m; ++i) {
+            val[i] = gx[i] = gy[i] = NAN;
+            outcome[i] = OUT_NAN;
+        }
+        free_index(&ix);
+        return 0;
+    }
+#ifdef _OPENMP
+    if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel
+    {
+        FitScratch S;
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t i = 0; i < m; ++i) {
+            double qx = xs[i % out_w], qy = ys[i / out_w];
+            int done = 0;
+            for (int order = order0; order >= 0 && !done; --order) {
+                for (int phase = 0; phase < 2 && !done; ++phase) {
+                    double h11, h12, h22, r;
+                    if (phase == 0) {
+                        h11 = an_h11[i];
+                        h12 = an_h12[i];
+                        h22 = an_h22[i];
+                        r = an_r0[i];
+                    } else {
+                        h11 = iso_hinv;
+                        h12 = 0.0;
+                        h22 = iso_hinv;
+                        r = iso_r0;
+                    }
+                    if (r > max_radius) r = max_radius;
+                    int step = 0;
+                    for (;;) {
+                        int st = fit_at(qx, qy, h11, h12, h22, r, order, cond_threshold, &ix,
+                                        use_sigma, &S);
+                        if (st == OK) {
+                            val[i] = S.coef[0];
+                            if (order >= 1) {
+                                gx[i] = S.coef[1];
+                                gy[i] = S.coef[2];
+                            } else {
+                                gx[i] = gy[i] = NAN;
+                            }
+                            outcome[i] = (uint8_t)(order * 16 + phase * 8 + (step < 7 ? step : 7));
+                            done = 1;
+                            break;
+                        }
+                        if (r >= max_radius * (1.0 - 1e-12)) break;
+                        r = r * 1.5;
+                        if (r > max_radius) r = max_radius;
+                        ++step;
+                    }
+                }
+            }
+            if (!done) {
+                val[i] = gx[i] = gy[i] = NAN;
+                outcome[i] = OUT_NAN;
+            }
+        }
+    }
+    free_index(&ix);
+    return 0;
+}

@@ -306,3 +306,116 @@ def reconstruct(frames, configs, cals, out_size, params, ref_size=None, threads=
         rgb[:, :, c] = np.maximum(val[c], 0.0).astype(np.float32)
     return {"rgb": rgb, "val": val, "gx": gx, "gy": gy, "outcome": outcome, "scale_idx": sidx,
             "count": count}
+
+
+# ---------------------------------------------------------------------------
+# CALPA (reference steering.py) -- structure-adaptive second pass
+# ---------------------------------------------------------------------------
+def _load_calpa(lib):
+    if getattr(lib, "_calpa_ready", False):
+        return lib
+    lib.oracle_steering_field.argtypes = [
+        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+    ]
+    lib.oracle_reconstruct_channel_steered.argtypes = [
+        ctypes.POINTER(OSensor), ctypes.c_int, ctypes.c_int,
+        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+        ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+    ]
+    lib._calpa_ready = True
+    return lib
+
+
+def steering_field(gx, gy, adaptive, gradient_scale=1.0, threads=None):
+    """(theta, sigma, gamma) planes: compute_steering_field (steering.py:177-203)
+    with _kernels.steering_field_kernel (_kernels.py:310-392)."""
+    lib = _load_calpa(_load())
+    scale = float(gradient_scale)
+    gxs = np.ascontiguousarray(np.asarray(gx, dtype=np.float64) / scale)
+    gys = np.ascontiguousarray(np.asarray(gy, dtype=np.float64) / scale)
+    h, w = gxs.shape
+    theta, sigma, gamma = (np.empty_like(gxs) for _ in range(3))
+    lib.oracle_steering_field(gxs.ctypes.data, gys.ctypes.data, w, h,
+                              adaptive.gradient_window // 2, adaptive.gradient_window / 4.0,
+                              float(adaptive.lambda1), float(adaptive.lambda2),
+                              float(adaptive.alpha), float(adaptive.sigma_max),
+                              theta.ctypes.data, sigma.ctypes.data, gamma.ctypes.data,
+                              int(threads) if threads else 0)
+    return theta, sigma, gamma
+
+
+def kernel_inputs(theta, sigma, gamma, scale):
+    """SteeringField.covariance_entries + kernel_inputs (steering.py:80-107), in
+    numpy exactly as the reference evaluates them."""
+    ct = np.cos(theta)
+    st = np.sin(theta)
+    s = sigma
+    c11 = gamma * (s * ct * ct + st * st / s)
+    c12 = gamma * (ct * st) * (1.0 / s - s)
+    c22 = gamma * (s * st * st + ct * ct / s)
+    r0 = SUPPORT_SIGMAS * np.sqrt(scale * sigma / gamma)
+    return ((c11 / scale).ravel(), (c12 / scale).ravel(), (c22 / scale).ravel(), r0.ravel())
+
+
+def auto_gradient_scale(values):
+    """steering.py:206-211."""
+    finite = values[np.isfinite(values)]
+    if not len(finite):
+        return 1.0
+    s = float(np.percentile(np.abs(finite), 99.5))
+    return s if s > 0 else 1.0
+
+
+def reconstruct_channel_steered(frames, configs, cals, out_size, base, channel, steering,
+                                ref_size=None, threads=None):
+    """reconstruct_channel(..., steering=...) (lpa.py:379-408, two-phase)."""
+    lib = _load_calpa(_load())
+    arr, keep = make_sensors(frames, configs, cals)
+    out_w, out_h = out_size
+    xs, ys = grid_coordinates(out_size, ref_size or out_size)
+    m = out_w * out_h
+    h = channel_scale(base, channel)
+    an = [np.ascontiguousarray(a, dtype=np.float64) for a in steering]
+    bufs = [np.empty(m) for _ in range(3)] + [np.empty(m, np.uint8)]
+    lib.oracle_reconstruct_channel_steered(
+        arr, len(frames), int(channel), xs.ctypes.data, out_w, ys.ctypes.data, out_h,
+        int(base.order), an[0].ctypes.data, an[1].ctypes.data, an[2].ctypes.data,
+        an[3].ctypes.data, 1.0 / h, SUPPORT_SIGMAS * math.sqrt(h),
+        resolved_max_radius(base), float(base.cond_threshold),
+        1 if base.weight_mode == "sigma" else 0, int(threads) if threads else 0,
+        *[b.ctypes.data for b in bufs])
+    del keep
+    return tuple(b.reshape(out_h, out_w) for b in bufs)
+
+
+def calpa(frames, configs, cals, out_size, adaptive, ref_size=None, threads=None):
+    """calpa_reconstruct (steering.py:214-248): isotropic G pass -> gradient scale
+    -> steering field -> steered pass per channel.  Returns a dict with rgb
+    (float32 HWC), the field and the per-channel outcome codes."""
+    base = adaptive.base
+    out_w, out_h = out_size
+
+    def field_for(c):
+        o = reconstruct(frames, configs, cals, out_size, base, ref_size=ref_size,
+                        threads=threads, channels=(c,))
+        val, gx, gy = o["val"][c], o["gx"][c], o["gy"][c]
+        scale = adaptive.gradient_scale or auto_gradient_scale(val)
+        return steering_field(gx, gy, adaptive, scale, threads), scale
+
+    shared = field_for(1) if adaptive.share_steering else None
+    rgb = np.empty((out_h, out_w, 3), np.float32)
+    outcome = np.empty((3, out_h, out_w), np.uint8)
+    for c in range(3):
+        (theta, sigma, gamma), scale = shared if shared is not None else field_for(c)
+        steering = kernel_inputs(theta, sigma, gamma, channel_scale(base, c))
+        val, _, _, oc = reconstruct_channel_steered(frames, configs, cals, out_size, base, c,
+                                                    steering, ref_size, threads)
+        rgb[:, :, c] = np.maximum(val, 0.0).astype(np.float32)
+        outcome[c] = oc
+    theta, sigma, gamma = shared[0] if shared is not None else (None, None, None)
+    return {"rgb": rgb, "theta": theta, "sigma": sigma, "gamma": gamma, "outcome": outcome,
+            "gradient_scale": shared[1] if shared is not None else None}

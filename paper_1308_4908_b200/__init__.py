@@ -30,10 +30,21 @@ from .radiometry import (
 )
 from .validation import ShapeMismatchError
 
+# CALPA (structure-adaptive pass) imports torch lazily on first use of its functions
+from .steering import (  # noqa: E402
+    AdaptiveParams,
+    SteeringField,
+    calpa_reconstruct,
+    compute_steering_field,
+    gradient_field,
+)
+
 __all__ = [
     "BayerPattern", "CFAImage", "ColorChannel", "ConfigurationError", "FloatFrame", "HDRImage",
     "NoiseCalibration", "RawFrameSet", "ReconstructionParams", "SUPPORT_SIGMAS", "SensorConfig",
     "ShapeMismatchError", "basis_row", "channel_at", "channel_map", "channel_masks",
     "estimate_radiance", "estimate_variance", "frame_to_samples", "frames_to_samples",
     "grid_coordinates", "reconstruct_channel", "reconstruct_frame", "saturation_mask",
+    "AdaptiveParams", "SteeringField", "calpa_reconstruct", "compute_steering_field",
+    "gradient_field",
 ]

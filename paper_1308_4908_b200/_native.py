@@ -33,6 +33,8 @@ HDR_FLAG_FAST_ONLY = 1
 EXPORTED = (
     "hdr_lpa_workspace_bytes",
     "hdr_lpa_reconstruct",
+    "hdr_lpa_reconstruct_steered",
+    "hdr_steering_field",
     "hdr_saturation_mask",
     "hdr_radiance_planes",
     "hdr_lpa_slow_items",
@@ -89,6 +91,10 @@ class HdrOutputs(ctypes.Structure):
     ]
 
 
+class HdrSteering(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_void_p), ("sigma", ctypes.c_void_p), ("gamma", ctypes.c_void_p)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -129,6 +135,18 @@ def lib():
                 ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                 ctypes.c_int, ctypes.c_int, ctypes.POINTER(HdrOutputs),
                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+            ]
+            L.hdr_lpa_reconstruct_steered.argtypes = [
+                ctypes.POINTER(HdrSensor), ctypes.c_int, ctypes.POINTER(HdrParams),
+                ctypes.POINTER(HdrSteering), ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(HdrOutputs),
+                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+            ]
+            L.hdr_steering_field.argtypes = [
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.c_void_p,
             ]
             L.hdr_saturation_mask.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_void_p,
                                               ctypes.c_int, ctypes.c_void_p]

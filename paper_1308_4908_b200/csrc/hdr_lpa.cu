@@ -827,6 +827,155 @@ __global__ void radiance_phase_kernel(const __grid_constant__ DevParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// CALPA: steering field and steered (anisotropic, two-phase) pass
+// (reference steering.py:72-248, _kernels.py:262-275, :303-392)
+// ---------------------------------------------------------------------------
+struct SteerConsts {
+    int half;
+    double wstd, lam1, lam2, alpha, sigma_max, inv_scale;
+};
+
+// steering_field_kernel (_kernels.py:310-392), float64, one thread per pixel.
+__global__ void steering_field_kernel(const float *gx, const float *gy, int w, int h,
+                                      SteerConsts K, double *theta, double *sigma,
+                                      double *gamma) {
+    const int xx = blockIdx.x * blockDim.x + threadIdx.x, yy = blockIdx.y;
+    if (xx >= w) return;
+    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+    int n = 0;
+    const double den = 2.0 * K.wstd * K.wstd;
+    for (int dy = -K.half; dy <= K.half; ++dy) {
+        const int iy = yy + dy;
+        if (iy < 0 || iy >= h) continue;
+        for (int dx = -K.half; dx <= K.half; ++dx) {
+            const int ix = xx + dx;
+            if (ix < 0 || ix >= w) continue;
+            const double g1 = (double)gx[(size_t)iy * w + ix] * K.inv_scale;
+            const double g2 = (double)gy[(size_t)iy * w + ix] * K.inv_scale;
+            if (!(isfinite(g1) && isfinite(g2))) continue;
+            const double wgt = exp(-(double)(dx * dx + dy * dy) / den);
+            s11 += wgt * g1 * g1;
+            s12 += wgt * g1 * g2;
+            s22 += wgt * g2 * g2;
+            ++n;
+        }
+    }
+    const size_t o = (size_t)yy * w + xx;
+    if (n == 0) {
+        theta[o] = 0.0;
+        sigma[o] = 1.0;
+        gamma[o] = 1.0;
+        return;
+    }
+    const double m = 0.5 * (s11 + s22), dd = hypot(0.5 * (s11 - s22), s12);
+    const double lmax = m + dd, lmin = fmax(m - dd, 0.0);
+    const double s1 = sqrt(lmax), s2 = sqrt(lmin);
+    double v1, v2;
+    if (fabs(s12) > 1e-300) {
+        v1 = s12;
+        v2 = lmin - s11;
+        if (v1 == 0.0 && v2 == 0.0) v1 = 1.0;
+    } else if (s11 <= s22) {
+        v1 = 1.0;
+        v2 = 0.0;
+    } else {
+        v1 = 0.0;
+        v2 = 1.0;
+    }
+    double th = atan2(v1, v2);
+    if (th <= -0.5 * M_PI)
+        th += M_PI;
+    else if (th > 0.5 * M_PI)
+        th -= M_PI;
+    const double dn = s2 + K.lam1;
+    double sg = dn == 0.0 ? ((s1 + K.lam1 == 0.0) ? 1.0 : K.sigma_max) : (s1 + K.lam1) / dn;
+    if (sg > K.sigma_max) sg = K.sigma_max;
+    theta[o] = th;
+    sigma[o] = sg;
+    gamma[o] = pow((s1 * s2 + K.lam2) / n, K.alpha);
+}
+
+// Exact accumulation with an arbitrary SPD window Hinv (two-phase CALPA).
+template <int ORDER, class Sweep>
+__device__ __forceinline__ void accumulate_hinv(const Sweep &sweep, int c, double h11, double h12,
+                                                double h22, double r, double r2,
+                                                Acc<NC<ORDER>::P> &acc) {
+    acc.zero();
+    const double h12x2 = 2.0 * h12;
+    sweep(c, r, r2, [&](bool, double v, float iv, double dx, double dy, double dxx, double dyy,
+                        float) {
+        // q = h11*dx*dx + 2.0*h12*dx*dy + h22*dy*dy (_kernels.py:164)
+        const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(h11, dx), dx),
+                                             __dmul_rn(__dmul_rn(h12x2, dx), dy)),
+                                   __dmul_rn(__dmul_rn(h22, dy), dy));
+        acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
+    });
+}
+
+template <int ORDER, class Sweep>
+__device__ bool steered_order(const DevParams &P, int c, const Sweep &sweep, const double *an,
+                              PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    Acc<PN> acc;
+    for (int phase = 0; phase < 2; ++phase) {
+        const double h11 = phase ? P.hinv[c][0] : an[0];
+        const double h12 = phase ? 0.0 : an[1];
+        const double h22 = phase ? P.hinv[c][0] : an[2];
+        double r = phase ? P.r[c][0] : fmin(an[3], P.max_radius);
+        int step = 0;
+        for (;;) {
+            accumulate_hinv<ORDER>(sweep, c, h11, h12, h22, r, __dmul_rn(r, r), acc);
+            Fit fit;
+            if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
+                R.count = acc.count;
+                R.val = fit.c0;
+                R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                R.gy = ORDER >= 1 ? fit.c2 : qnan();
+                R.outcome = ORDER * 16 + phase * 8 + (step < 7 ? step : 7);
+                return true;
+            }
+            if (r >= P.max_radius * (1.0 - 1e-12)) break;
+            r = fmin(r * 1.5, P.max_radius);
+            ++step;
+        }
+    }
+    return false;
+}
+
+// Steered pass (lpa_evaluate two_phase, _kernels.py:257-300): per pixel and
+// channel, Hinv = C/h and r0 = 3 sqrt(h sigma/gamma) from the steering field
+// (SteeringField.kernel_inputs, steering.py:94-107).
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_steered_kernel(const __grid_constant__ DevParams P) {
+    const int n = P.out_w * (P.row_end - P.row_begin) * 3;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n; it += gridDim.x * blockDim.x) {
+        const int c = it % 3, pl = it / 3;
+        const int ox = pl % P.out_w, oy = P.row_begin + pl / P.out_w;
+        const int pix = oy * P.out_w + ox;
+        const GlobalSweep sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
+        const double ct = cos(th), st = sin(th);
+        const double h = P.h[c][0];  // channel scale
+        // covariance_entries (steering.py:80-87), same operation order
+        const double c11 = g * (s * ct * ct + st * st / s);
+        const double c12 = g * (ct * st) * (1.0 / s - s);
+        const double c22 = g * (s * st * st + ct * ct / s);
+        const double an[4] = {c11 / h, c12 / h, c22 / h, 3.0 * sqrt(h * s / g)};
+        PixelResult R;
+        R.sidx = 0;
+        bool ok = steered_order<ORDER>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 1) ok = steered_order<(ORDER >= 1 ? ORDER - 1 : 0)>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 2) ok = steered_order<0>(P, c, sweep, an, R);
+        if (!ok) {
+            R.val = R.gx = R.gy = qnan();
+            R.outcome = HDR_OUTCOME_NAN;
+            R.count = 0;
+        }
+        write_result(P, pix, c, R);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Saturation mask bit-planes (radiometry.py:298-300, :316-317)
 // ---------------------------------------------------------------------------
 __global__ void saturation_mask_kernel(const DevSensor S, uint32_t *bits, int wpr) {
@@ -1152,10 +1301,11 @@ int hdr_lpa_workspace_bytes(const HdrSensor *sensors, int n_sensors, int out_w, 
     return HDR_OK;
 }
 
-int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
+// Validation and DevParams set-up shared by the plain and steered entry points.
+static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
                         int out_w, int out_h, double ref_w, double ref_h, int row_begin,
                         int row_end, const HdrOutputs *out, void *workspace,
-                        size_t workspace_bytes, void *stream) {
+                        size_t workspace_bytes, DevParams &P, double &fastR) {
     if (!sensors || !params || !out || !out->rgb || !workspace) return HDR_ERR_ARG;
     if (n_sensors < 1 || n_sensors > MAXS) return HDR_ERR_ARG;
     if (out_w <= 0 || out_h <= 0 || !(ref_w > 0) || !(ref_h > 0)) return HDR_ERR_ARG;
@@ -1168,7 +1318,6 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     if (row_begin < 0 || row_begin >= row_end) return HDR_ERR_ARG;
     if ((uintptr_t)workspace & 255) return HDR_ERR_ARG;
 
-    DevParams P;
     memset(&P, 0, sizeof(P));
     for (int s = 0; s < n_sensors; ++s) {
         const int rc = fill_sensor(sensors[s], P.s[s]);
@@ -1191,7 +1340,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.max_radius = params->max_radius;
     P.cond = params->cond_threshold;
     P.gamma = params->ici_gamma;
-    double fastR = 0.0;
+    fastR = 0.0;
     for (int c = 0; c < 3; ++c)
         for (int k = 0; k < P.n_scales; ++k) {
             const double h = params->scale[c][k];
@@ -1202,6 +1351,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
             P.r2[c][k] = r * r;
             P.hl[c][k] = (float)(1.4426950408889634 / h);
             P.hinv[c][k] = 1.0 / h;  // iso Hinv = 1/scale (lpa.py:351)
+            P.h[c][k] = h;
             fastR = fmax(fastR, r);
         }
     P.fast_R = fastR;
@@ -1223,6 +1373,31 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     }
     P.work_items = (uint32_t *)wsp;
 
+    return HDR_OK;
+}
+
+static int launch_prepass(const DevParams &P, cudaStream_t st) {
+    int maxpw = 0, maxph = 0;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        maxpw = max(maxpw, P.s[s].pwg);
+        maxph = max(maxph, P.s[s].phg);
+    }
+    dim3 grid((maxpw + 127) / 128, maxph, 4 * P.n_sensors);
+    radiance_phase_kernel<<<grid, 128, 0, st>>>(P);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("radiance_phase_kernel launch");
+}
+
+int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
+                        int out_w, int out_h, double ref_w, double ref_h, int row_begin,
+                        int row_end, const HdrOutputs *out, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+    DevParams P;
+    double fastR = 0.0;
+    {
+        const int rc = setup_params(sensors, n_sensors, params, out_w, out_h, ref_w, ref_h,
+                                    row_begin, row_end, out, workspace, workspace_bytes, P, fastR);
+        if (rc != HDR_OK) return rc;
+    }
     // Staged region per sensor: tile extent in sensor space + 2 x window
     // half-width (+ rounding/alignment slack).  Shared memory: pre-computed
     // taps, then two plane buffers, each holding per sensor the four staged
@@ -1281,16 +1456,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         return cuda_fail("cudaMemsetAsync");
     if (P.pat && upload_taps(taps, (char *)workspace + WS_HEADER, st) != HDR_OK)
         return cuda_fail("tap upload");
-    {  // per-frame radiometric pre-pass into the phase planes
-        int maxpw = 0, maxph = 0;
-        for (int s = 0; s < n_sensors; ++s) {
-            maxpw = max(maxpw, P.s[s].pwg);
-            maxph = max(maxph, P.s[s].phg);
-        }
-        dim3 grid((maxpw + 127) / 128, maxph, 4 * n_sensors);
-        radiance_phase_kernel<<<grid, 128, 0, st>>>(P);
-        if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("radiance_phase_kernel launch");
-    }
+    if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;  // per-frame radiometry
     int rc;
     switch (P.order) {
         case 0: rc = launch_all<0>(P, tiles, smem_bytes, maxc, st); break;
@@ -1298,6 +1464,57 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         default: rc = launch_all<2>(P, tiles, smem_bytes, maxc, st); break;
     }
     return rc;
+}
+
+int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
+                                const HdrParams *params, const HdrSteering *steering, int out_w,
+                                int out_h, double ref_w, double ref_h, int row_begin, int row_end,
+                                const HdrOutputs *out, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+    if (!steering || !steering->theta || !steering->sigma || !steering->gamma) return HDR_ERR_ARG;
+    if (params && params->n_scales != 1) return HDR_ERR_ARG;  // CALPA is fixed-scale
+    DevParams P;
+    double fastR = 0.0;
+    const int rc = setup_params(sensors, n_sensors, params, out_w, out_h, ref_w, ref_h, row_begin,
+                                row_end, out, workspace, workspace_bytes, P, fastR);
+    if (rc != HDR_OK) return rc;
+    P.st_theta = steering->theta;
+    P.st_sigma = steering->sigma;
+    P.st_gamma = steering->gamma;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = nsm * 8;
+    switch (P.order) {
+        case 0: lpa_steered_kernel<0><<<grid, 128, 0, st>>>(P); break;
+        case 1: lpa_steered_kernel<1><<<grid, 128, 0, st>>>(P); break;
+        default: lpa_steered_kernel<2><<<grid, 128, 0, st>>>(P); break;
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_steered_kernel launch");
+}
+
+int hdr_steering_field(const float *gx, const float *gy, int width, int height,
+                       int gradient_window, double lambda1, double lambda2, double alpha,
+                       double sigma_max, double gradient_scale, double *theta, double *sigma,
+                       double *gamma, void *stream) {
+    if (!gx || !gy || !theta || !sigma || !gamma || width <= 0 || height <= 0) return HDR_ERR_ARG;
+    if (gradient_window < 3 || gradient_window % 2 == 0) return HDR_ERR_ARG;
+    if (!(gradient_scale > 0) || !isfinite(gradient_scale)) return HDR_ERR_ARG;
+    if (alpha < 0 || lambda1 < 0 || !(lambda2 > 0)) return HDR_ERR_ARG;
+    SteerConsts K;
+    K.half = gradient_window / 2;
+    K.wstd = gradient_window / 4.0;
+    K.lam1 = lambda1;
+    K.lam2 = lambda2;
+    K.alpha = alpha;
+    K.sigma_max = sigma_max;
+    K.inv_scale = 1.0 / gradient_scale;
+    dim3 grid((width + 127) / 128, height);
+    steering_field_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(gx, gy, width, height, K, theta,
+                                                                  sigma, gamma);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("steering_field_kernel launch");
 }
 
 int hdr_saturation_mask(const HdrSensor *sensor, uint32_t *out_bits, int words_per_row,

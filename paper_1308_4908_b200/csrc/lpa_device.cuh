@@ -74,6 +74,7 @@ struct DevParams {
     double r2[3][MAXJ];       // r * r
     float hl[3][MAXJ];        // log2(e) / h  (window exponent in exp2 form, fast path)
     double hinv[3][MAXJ];     // 1 / h (float64 window exponent, exact path)
+    double h[3][MAXJ];        // the window scales themselves
     double max_radius, cond, gamma;
     double fast_R;            // radius the staged tiles cover
     float *rgb;
@@ -92,6 +93,8 @@ struct DevParams {
     int pat_base[MAXS][2];          // offset (ox, oy) of the tap window's origin: see build_taps
     uint32_t *work_count;
     uint32_t *work_items;
+    // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)
+    const double *st_theta, *st_sigma, *st_gamma;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {

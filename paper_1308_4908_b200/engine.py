@@ -238,6 +238,37 @@ class DeviceRig:
         N.check(rc, "hdr_lpa_reconstruct")
         return out
 
+    def reconstruct_steered(self, out_size, params: ReconstructionParams, field, ref_size=None,
+                            rows=None, out=None, want_outcome=False, raw_value=False,
+                            stream=None):
+        """CALPA second pass with a steering field (theta, sigma, gamma float64
+        device tensors over the output grid): hdr_lpa_reconstruct_steered."""
+        out_w, out_h = int(out_size[0]), int(out_size[1])
+        if ref_size is None:
+            ref_size = (out_w, out_h)
+        if out is None:
+            out = self.allocate_outputs((out_w, out_h), want_outcome=want_outcome,
+                                        raw_value=raw_value)
+        th, sg, gm = (t.contiguous() for t in field)
+        for t in (th, sg, gm):
+            if t.dtype != torch.float64 or tuple(t.shape) != (out_h, out_w) or t.device != self.device:
+                raise ValueError("steering planes must be float64 (out_h, out_w) device tensors")
+        steer = N.HdrSteering(th.data_ptr(), sg.data_ptr(), gm.data_ptr())
+        o = N.HdrOutputs()
+        o.rgb = out["rgb"].data_ptr()
+        o.outcome = out["outcome"].data_ptr() if "outcome" in out else None
+        o.value = out["value"].data_ptr() if "value" in out else None
+        ws = self.workspace(out_w, out_h)
+        r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            rc = N.lib().hdr_lpa_reconstruct_steered(
+                self._sensors, len(self.raws), ctypes.byref(hdr_params(params)),
+                ctypes.byref(steer), out_w, out_h, float(ref_size[0]), float(ref_size[1]), r0, r1,
+                ctypes.byref(o), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        N.check(rc, "hdr_lpa_reconstruct_steered")
+        return out
+
     def slow_items(self, out_size) -> int:
         """Work items the last reconstruct on this output size sent to the slow path."""
         ws = self.workspace(int(out_size[0]), int(out_size[1]))

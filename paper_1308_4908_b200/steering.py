@@ -1,0 +1,148 @@
+"""Structure-adaptive second pass (CALPA) -- reference pkg/src/hdrfuse/steering.py.
+
+An isotropic first pass (order >= 1) gives the gradient field of the G
+channel on the output grid; a 9x9 weighted structure tensor per pixel gives
+an orientation theta, an elongation sigma and a scaling gamma
+(``hdr_steering_field``); the second pass then fits every channel with the
+per-pixel anisotropic window H^{-1} = C/h, C = gamma U_theta diag(sigma,
+1/sigma) U_theta^T, falling back per pixel to the isotropic window before
+the radius/order ladder (``hdr_lpa_reconstruct_steered``).  Same API, fields
+and validation as the reference; everything runs on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .bayer import ColorChannel
+from .images import HDRImage
+from .lpa import SUPPORT_SIGMAS, ReconstructionParams, _device_rig
+from .validation import check_positive
+
+
+@dataclass(frozen=True)
+class AdaptiveParams:
+    """Steering knobs on top of a base reconstruction (reference steering.py:38-69)."""
+
+    alpha: float = 0.005
+    lambda1: float = 1.0
+    lambda2: float = 0.001
+    gradient_window: int = 9
+    sigma_max: float = 50.0
+    share_steering: bool = True
+    gradient_scale: Optional[float] = None
+    base: ReconstructionParams = field(default_factory=ReconstructionParams)
+
+    def __post_init__(self):
+        if self.alpha < 0:
+            raise ValueError(f"alpha must be >= 0, got {self.alpha}")
+        if self.lambda1 < 0:
+            raise ValueError(f"lambda1 must be >= 0, got {self.lambda1}")
+        check_positive("lambda2", self.lambda2)
+        if self.gradient_window < 3 or self.gradient_window % 2 == 0:
+            raise ValueError(f"gradient_window must be odd and >= 3, got {self.gradient_window}")
+        if self.base.order < 1:
+            raise ValueError("steering needs a base reconstruction of order >= 1")
+        if self.base.ici_scales != 1:
+            raise ValueError("the steered pass is fixed-scale (ici_scales must be 1)")
+
+
+@dataclass(frozen=True)
+class SteeringField:
+    """Per output pixel theta (rad), sigma >= 1, gamma > 0 (float64 device tensors)."""
+
+    theta: torch.Tensor
+    sigma: torch.Tensor
+    gamma: torch.Tensor
+
+    def numpy(self):
+        return tuple(t.cpu().numpy() for t in (self.theta, self.sigma, self.gamma))
+
+    def covariance_entries(self):
+        """(C11, C12, C22) of C = gamma U diag(sigma, 1/sigma) U^T (steering.py:80-87)."""
+        ct, st, s, g = torch.cos(self.theta), torch.sin(self.theta), self.sigma, self.gamma
+        return (g * (s * ct * ct + st * st / s), g * (ct * st) * (1.0 / s - s),
+                g * (s * st * st + ct * ct / s))
+
+    def kernel_inputs(self, scale: float):
+        """Per-pixel H^{-1} entries and base radii (steering.py:94-107)."""
+        c11, c12, c22 = self.covariance_entries()
+        r0 = SUPPORT_SIGMAS * torch.sqrt(scale * self.sigma / self.gamma)
+        return c11 / scale, c12 / scale, c22 / scale, r0
+
+
+def gradient_field(samples, out_size, params: ReconstructionParams, channel=ColorChannel.G,
+                   ref_size=None):
+    """Isotropic first pass: (value, grad_x, grad_y) device float32 planes."""
+    if params.order < 1:
+        raise ValueError("gradient estimation needs order >= 1")
+    rig = _device_rig(samples)
+    out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=True, raw_value=True)
+    c = int(channel)
+    return out["value"][c], out["grad"][c, 0], out["grad"][c, 1]
+
+
+def auto_gradient_scale(values: torch.Tensor) -> float:
+    """99.5th percentile of |finite values| (steering.py:206-211)."""
+    v = values[torch.isfinite(values)].abs().double()
+    if v.numel() == 0:
+        return 1.0
+    s = float(torch.quantile(v.flatten()[: 1 << 24], 0.995))
+    return s if s > 0 else 1.0
+
+
+def compute_steering_field(grads, params: AdaptiveParams, gradient_scale: float = 1.0) -> SteeringField:
+    """Steering field for every output pixel (hdr_steering_field)."""
+    gx, gy = (g.contiguous().float() for g in grads)
+    scale = float(gradient_scale)
+    if scale <= 0 or not math.isfinite(scale):
+        raise ValueError(f"gradient_scale must be positive, got {gradient_scale}")
+    h, w = gx.shape
+    theta, sigma, gamma = (torch.empty((h, w), dtype=torch.float64, device=gx.device)
+                           for _ in range(3))
+    st = torch.cuda.current_stream(gx.device)
+    N.check(N.lib().hdr_steering_field(
+        gx.data_ptr(), gy.data_ptr(), w, h, params.gradient_window, float(params.lambda1),
+        float(params.lambda2), float(params.alpha), float(params.sigma_max), scale,
+        theta.data_ptr(), sigma.data_ptr(), gamma.data_ptr(), st.cuda_stream),
+        "hdr_steering_field")
+    return SteeringField(theta, sigma, gamma)
+
+
+def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
+                      return_field: bool = False):
+    """Colour-adaptive reconstruction: isotropic G pass, steering, steered RGB
+    pass (reference steering.py:214-248)."""
+    rig = _device_rig(samples)
+    base = params.base
+
+    def field_for(channel):
+        val, gx, gy = gradient_field(rig, out_size, base, channel, ref_size)
+        scale = params.gradient_scale or auto_gradient_scale(val)
+        return compute_steering_field((gx, gy), params, scale)
+
+    if params.share_steering:
+        fld = field_for(ColorChannel.G)
+        out = rig.reconstruct_steered(out_size, base, (fld.theta, fld.sigma, fld.gamma),
+                                      ref_size=ref_size)
+        img = HDRImage(out["rgb"].cpu().numpy())
+    else:
+        out_w, out_h = out_size
+        planes = np.empty((out_h, out_w, 3), np.float32)
+        fld = None
+        for ch in ColorChannel:
+            f = field_for(ch)
+            o = rig.reconstruct_steered(out_size, base, (f.theta, f.sigma, f.gamma),
+                                        ref_size=ref_size)
+            planes[:, :, int(ch)] = o["rgb"][:, :, int(ch)].cpu().numpy()
+        img = HDRImage(planes)
+    if return_field:
+        return img, fld
+    return img

@@ -21,9 +21,14 @@ def names():
     return sorted(manifest()["cases"])
 
 
+def calpa_names():
+    return sorted(manifest().get("calpa_cases", {}))
+
+
 def load(name):
     """(frames, configs, cals, out_size, params, ref_size, case_json, arrays)."""
-    case = manifest()["cases"][name]
+    m = manifest()
+    case = m["cases"][name] if name in m["cases"] else m["calpa_cases"][name]
     arrays = dict(np.load(GOLDEN / f"{name}.npz"))
     frames, configs, cals = [], [], []
     for k, s in enumerate(case["sensors"]):

@@ -1,0 +1,74 @@
+"""CALPA (structure-adaptive second pass) on the GPU against the oracle (which
+reproduces the reference bit-exactly: tests/test_oracle_golden.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1308_4908_b200 as hl
+from golden_cases import calpa_names, load
+from oracle import compare, oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _case():
+    frames, cfgs, cals, out_size, params, ref_size, case, arrays = load(calpa_names()[0])
+    ap = hl.AdaptiveParams(base=params, **case["adaptive"])
+    return frames, cfgs, cals, out_size, ap, arrays
+
+
+def test_steering_field_kernel_matches_oracle(cuda):
+    frames, cfgs, cals, out_size, ap, arrays = _case()
+    o = oracle.reconstruct(frames, cfgs, cals, out_size, ap.base, channels=(1,))
+    gx32, gy32 = o["gx"][1].astype(np.float32), o["gy"][1].astype(np.float32)
+    scale = oracle.auto_gradient_scale(o["val"][1])
+    th, sg, gm = oracle.steering_field(gx32.astype(np.float64), gy32.astype(np.float64), ap, scale)
+    f = hl.compute_steering_field((torch.from_numpy(gx32).cuda(), torch.from_numpy(gy32).cuda()),
+                                  ap, scale)
+    gth, gsg, ggm = f.numpy()
+    # same float64 formula, device vs libm exp/atan2/pow: a few ulp
+    np.testing.assert_allclose(gsg, sg, rtol=1e-12)
+    np.testing.assert_allclose(ggm, gm, rtol=1e-12)
+    np.testing.assert_allclose(gth, th, rtol=1e-9, atol=1e-12)
+
+
+def test_steered_pass_matches_oracle_on_the_same_field(cuda):
+    frames, cfgs, cals, out_size, ap, arrays = _case()
+    th, sg, gm = (arrays[k] for k in ("theta", "sigma", "gamma"))  # the reference's field
+    rig = hl.frames_to_samples(frames, cfgs, cals).device()
+    field = tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (th, sg, gm))
+    out = rig.reconstruct_steered(out_size, ap.base, field, want_outcome=True)
+    rgb = out["rgb"].cpu().numpy()
+    for c in range(3):
+        steer = oracle.kernel_inputs(th, sg, gm, oracle.channel_scale(ap.base, c))
+        val, _, _, oc = oracle.reconstruct_channel_steered(frames, cfgs, cals, out_size, ap.base,
+                                                           c, steer)
+        ref = np.maximum(val, 0.0).astype(np.float32)
+        s = compare.summary(rgb[:, :, c], ref)
+        print(c, s, "outcome mismatches", int((out["outcome"][c].cpu().numpy() != oc).sum()))
+        assert s["nan_map_equal"] and s["frac_over"] <= 1e-3 and s["max"] <= 1e-3
+        assert int((out["outcome"][c].cpu().numpy() != oc).sum()) == 0
+
+
+def test_calpa_end_to_end_matches_reference(cuda):
+    frames, cfgs, cals, out_size, ap, arrays = _case()
+    img, fld = hl.calpa_reconstruct(hl.frames_to_samples(frames, cfgs, cals), out_size, ap,
+                                    return_field=True)
+    s = compare.summary(img.data, arrays["rgb"])  # the reference's own CALPA output
+    print("calpa vs reference", s)
+    assert s["nan_map_equal"] and s["frac_over"] <= 1e-3 and s["max"] <= 1e-2
+    th, sg, gm = fld.numpy()
+    assert np.abs(sg - arrays["sigma"]).max() / 50.0 < 1e-4
+
+
+def test_calpa_without_adaptation_equals_lpa(cuda):
+    # reference acceptance criterion 8 (test_acceptance.py:324-327): alpha = 0 and
+    # sigma_max = 1 make every window the isotropic one
+    frames, cfgs, cals, out_size, ap, arrays = _case()
+    raw = hl.frames_to_samples(frames, cfgs, cals)
+    eq = hl.calpa_reconstruct(raw, out_size, hl.AdaptiveParams(alpha=0.0, sigma_max=1.0,
+                                                               base=ap.base))
+    iso = hl.reconstruct_frame(raw, out_size, ap.base)
+    s = compare.summary(eq.data, iso.data)
+    assert s["nan_map_equal"] and s["max"] < 1e-5
