@@ -172,6 +172,28 @@ int hdr_steering_field(const float *gx, const float *gy, int width, int height,
                        double *gamma, void *stream);
 
 /*
+ * Scattered-sample mode: the reference's own kernel boundary
+ * (_kernels.py:203-230 lpa_evaluate) over a CSR unit-cell index of packed
+ * (x, y, value, variance) float64 rows (radiometry.py:208-242 SampleIndex),
+ * used by LocalPolynomialRegressor.predict (lpa.py:273-293) and by
+ * reconstruct_frame on RadianceSamples.  Device pointers.  an_* are the
+ * optional per-query anisotropic windows (two-phase mode); NULL = isotropic.
+ */
+typedef struct HdrSampleIndex {
+    const double *packed;       /* n x 4: x, y, value, variance (cell-sorted, stable) */
+    const int64_t *cell_start;  /* nx*ny + 1 */
+    int64_t n;
+    int x0, y0, nx, ny;
+} HdrSampleIndex;
+
+int hdr_lpa_evaluate_samples(const HdrSampleIndex *index, const double *qx, const double *qy,
+                             int m, const double *an_h11, const double *an_h12,
+                             const double *an_h22, const double *an_r0, double iso_hinv,
+                             double iso_r0, int order, double max_radius, double cond_threshold,
+                             int weight_mode, double *out_val, double *out_gx, double *out_gy,
+                             void *stream);
+
+/*
  * Saturation (+ defective) mask of one sensor as bit-planes: bit (x % 32) of
  * out_bits[y * words_per_row + x / 32] is set where the pixel is discarded.
  * words_per_row >= ceil(width / 32).

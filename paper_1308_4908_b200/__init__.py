@@ -30,7 +30,12 @@ from .radiometry import (
 )
 from .validation import ShapeMismatchError
 
-# CALPA (structure-adaptive pass) imports torch lazily on first use of its functions
+from .samples import (  # noqa: E402
+    LocalPolynomialRegressor,
+    RadianceSample,
+    RadianceSamples,
+    SampleIndex,
+)
 from .steering import (  # noqa: E402
     AdaptiveParams,
     SteeringField,
@@ -46,5 +51,6 @@ __all__ = [
     "estimate_radiance", "estimate_variance", "frame_to_samples", "frames_to_samples",
     "grid_coordinates", "reconstruct_channel", "reconstruct_frame", "saturation_mask",
     "AdaptiveParams", "SteeringField", "calpa_reconstruct", "compute_steering_field",
-    "gradient_field",
+    "gradient_field", "LocalPolynomialRegressor", "RadianceSample", "RadianceSamples",
+    "SampleIndex",
 ]

@@ -35,6 +35,7 @@ EXPORTED = (
     "hdr_lpa_reconstruct",
     "hdr_lpa_reconstruct_steered",
     "hdr_steering_field",
+    "hdr_lpa_evaluate_samples",
     "hdr_saturation_mask",
     "hdr_radiance_planes",
     "hdr_lpa_slow_items",
@@ -91,6 +92,12 @@ class HdrOutputs(ctypes.Structure):
     ]
 
 
+class HdrSampleIndex(ctypes.Structure):
+    _fields_ = [("packed", ctypes.c_void_p), ("cell_start", ctypes.c_void_p),
+                ("n", ctypes.c_int64), ("x0", ctypes.c_int), ("y0", ctypes.c_int),
+                ("nx", ctypes.c_int), ("ny", ctypes.c_int)]
+
+
 class HdrSteering(ctypes.Structure):
     _fields_ = [("theta", ctypes.c_void_p), ("sigma", ctypes.c_void_p), ("gamma", ctypes.c_void_p)]
 
@@ -141,6 +148,12 @@ def lib():
                 ctypes.POINTER(HdrSteering), ctypes.c_int, ctypes.c_int, ctypes.c_double,
                 ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(HdrOutputs),
                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+            ]
+            L.hdr_lpa_evaluate_samples.argtypes = [
+                ctypes.POINTER(HdrSampleIndex), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ]
             L.hdr_steering_field.argtypes = [
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -115,16 +115,36 @@ def _device_rig(samples):
     if isinstance(samples, RawFrameSet):
         return samples.device()
     raise TypeError(
-        "reconstruct_frame expects the RawFrameSet returned by frames_to_samples "
-        f"(or a DeviceRig), got {type(samples).__name__}; scattered RadianceSamples "
-        "input is not on this path (DESIGN.md, out of scope)")
+        "reconstruct_frame expects the RawFrameSet returned by frames_to_samples, a "
+        f"DeviceRig or RadianceSamples, got {type(samples).__name__}")
+
+
+def _is_scattered(samples) -> bool:
+    from .samples import RadianceSamples
+
+    return isinstance(samples, RadianceSamples)
 
 
 def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=None,
                       return_gradients: bool = False):
     """LPA reconstruction of R, G and B into an :class:`HDRImage`
     (reference lpa.py:411-433): radiance clamped at zero, NaN where no order
-    succeeds; gradients (when requested) unclamped, per channel."""
+    succeeds; gradients (when requested) unclamped, per channel.
+
+    ``samples`` is the RawFrameSet of :func:`frames_to_samples` (fused raw
+    path) or scattered :class:`~.samples.RadianceSamples` (CSR index path)."""
+    if _is_scattered(samples):
+        from .samples import reconstruct_channel_samples
+
+        out_w, out_h = out_size
+        planes = np.empty((out_h, out_w, 3), dtype=np.float32)
+        grads = {}
+        for ch in ColorChannel:
+            val, gx, gy = reconstruct_channel_samples(samples, out_size, params, ch, ref_size)
+            planes[:, :, int(ch)] = np.maximum(val, 0.0).astype(np.float32)
+            grads[ch] = (gx, gy)
+        img = HDRImage(planes)
+        return (img, grads) if return_gradients else img
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=return_gradients)
     img = HDRImage(out["rgb"].cpu().numpy())
@@ -139,8 +159,13 @@ def reconstruct_channel(samples, out_size, params: ReconstructionParams, channel
                         ref_size=None, steering=None):
     """(value, grad_x, grad_y) planes of one channel (reference lpa.py:379-408).
     ``value`` is unclamped like the reference's; NaN where no fit exists."""
+    if _is_scattered(samples):
+        from .samples import reconstruct_channel_samples
+
+        return reconstruct_channel_samples(samples, out_size, params, channel, ref_size, steering)
     if steering is not None:
-        raise NotImplementedError("steered (CALPA) windows are not on this path (DESIGN.md)")
+        raise ValueError("per-query steering arrays need scattered RadianceSamples; use "
+                         "calpa_reconstruct for raw frames")
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=True, raw_value=True)
     c = int(channel)

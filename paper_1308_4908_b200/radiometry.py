@@ -200,9 +200,11 @@ class RawFrameSet:
         return self.device(device).saturation_masks()
 
     def materialize(self, device=None):
-        """Reference-layout sample columns (positions, channels, values, sigmas,
-        sensor_ids), computed on the GPU from the raw frames."""
-        return self.device(device).materialize_samples()
+        """The reference's ``RadianceSamples`` (sensor-major, raster order),
+        radiometry computed on the GPU from the raw frames (fp32-rounded)."""
+        from .samples import RadianceSamples
+
+        return RadianceSamples(*self.device(device).materialize_samples())
 
 
 def frames_to_samples(frames, configs, cals) -> RawFrameSet:

@@ -173,7 +173,8 @@ def test_saturation_masks_bit_exact(cuda):
 
 def test_radiance_planes_match_oracle_samples(cuda):
     frames, cfgs, cals = _case("misaligned", 80, 60, seed=11)
-    pos, ch, val, sig, sid = hl.frames_to_samples(frames, cfgs, cals).materialize()
+    ms = hl.frames_to_samples(frames, cfgs, cals).materialize()
+    pos, ch, val, sig, sid = ms.positions, ms.channels, ms.values, ms.sigmas, ms.sensor_ids
     opos, och, oval, osig, osid = oracle.frames_to_samples(frames, cfgs, cals)
     assert np.array_equal(pos, opos) and np.array_equal(ch, och) and np.array_equal(sid, osid)
     # staging radiometry is fp32: a few fp32 ulp

@@ -67,9 +67,28 @@ class TestFramesToSamplesHandle:
         raw = hl.frames_to_samples([f], [cfg()], [ucal(6, 4)])
         assert len(raw) == 1 and raw.reference_size == (6, 4)
 
-    def test_scattered_samples_are_rejected_explicitly(self):
+    def test_unknown_sample_containers_are_rejected(self):
         with pytest.raises(TypeError):
             hl.reconstruct_frame(object(), (4, 4), hl.ReconstructionParams())
+
+    def test_radiance_samples_validation(self):
+        with pytest.raises(ValueError):
+            hl.RadianceSamples([[0, 0]], [0], [1.0], [0.0], [0])
+        with pytest.raises(ValueError):
+            hl.RadianceSamples([[np.nan, 0]], [0], [1.0], [1.0], [0])
+        s = hl.RadianceSamples.concatenate([hl.RadianceSamples.empty(),
+                                            hl.RadianceSamples([[1, 2]], [1], [3.0], [0.5], [4])])
+        assert len(s) == 1 and s[0].position == (1.0, 2.0) and s[0].channel == hl.ColorChannel.G
+
+    def test_regressor_validation(self):
+        reg = hl.LocalPolynomialRegressor()
+        with pytest.raises(RuntimeError):
+            reg.predict(np.zeros((1, 2)))
+        with pytest.raises(ValueError):
+            reg.fit(np.zeros((3, 2)), np.zeros(4))
+        from sklearn.base import clone
+        r2 = clone(hl.LocalPolynomialRegressor(order=2, scale=0.3, cond_threshold=1e6))
+        assert r2.get_params()["order"] == 2 and r2.get_params()["scale"] == 0.3
 
 
 class TestParams:
