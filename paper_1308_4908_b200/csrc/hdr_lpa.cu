@@ -53,10 +53,34 @@ struct NC {
 // below select exactly the reference's sample set in the same order.
 // ---------------------------------------------------------------------------
 
-// Slow path: straight from global memory, everything recomputed per candidate.
+// Slow path: straight from global memory (the per-frame phase planes).
+// LANES > 1: the candidates of every window are split over the lanes of a
+// warp (candidate j -> lane j % 32) and the sums are combined by a butterfly
+// reduction, after which every lane holds bitwise-identical totals.
+template <int LANES>
 struct GlobalSweep {
     const DevParams &P;
     double qx, qy;
+    template <int PN>
+    __device__ __forceinline__ void reduce(Acc<PN> &acc) const {
+        if constexpr (LANES > 1) {
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) {
+#pragma unroll
+                for (int i = 0; i < Acc<PN>::NA; ++i) acc.A[i] += __shfl_xor_sync(0xffffffffu, acc.A[i], m);
+#pragma unroll
+                for (int i = 0; i < PN; ++i) acc.b[i] += __shfl_xor_sync(0xffffffffu, acc.b[i], m);
+                acc.count += __shfl_xor_sync(0xffffffffu, acc.count, m);
+            }
+        }
+    }
+    __device__ __forceinline__ double reduce(double v) const {
+        if constexpr (LANES > 1) {
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        }
+        return v;
+    }
     template <class Body>
     __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
         for (int s = 0; s < P.n_sensors; ++s) {
@@ -71,38 +95,33 @@ struct GlobalSweep {
                 if (!((pm >> ph) & 1)) continue;
                 const int py = ph >> 1, px = ph & 1;
                 const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
-                for (int y = ys; y <= yhi; y += 2) {
+                const int nrow = yhi >= ys ? ((yhi - ys) >> 1) + 1 : 0;
+                const int ncol = xhi >= xs ? ((xhi - xs) >> 1) + 1 : 0;
+                const int lane = LANES > 1 ? (int)(threadIdx.x & 31) : 0;
+                for (int j = lane; j < nrow * ncol; j += LANES) {
+                    const int y = ys + 2 * (j / ncol), x = xs + 2 * (j % ncol);
                     const double yd = (double)y;
                     const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
                     const bool yin = y >= 0 && y < S.height;
                     const float2 *row = S.phase + ((size_t)ph * S.phg + (y >> 1)) * S.pwg;
-                    for (int x = xs; x <= xhi; x += 2) {
-                        // the per-frame phase planes hold radiance_sample(S, x, y)
-                        const float2 e = (yin && x >= 0 && x < S.width) ? __ldg(row + (x >> 1))
-                                                                         : make_float2(0.f, 0.f);
-                        if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
-                        const double xd = (double)x;
-                        const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
-                        const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
-                        const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
-                        const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
-                        const double d2 = __dadd_rn(dxx, dyy);
-                        if (d2 > r2) continue;  // _kernels.py:162
-                        body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
-                    }
+                    // the per-frame phase planes hold radiance_sample(S, x, y)
+                    const float2 e = (yin && x >= 0 && x < S.width) ? __ldg(row + (x >> 1))
+                                                                     : make_float2(0.f, 0.f);
+                    if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
+                    const double xd = (double)x;
+                    const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
+                    const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
+                    const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                    const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
+                    const double d2 = __dadd_rn(dxx, dyy);
+                    if (d2 > r2) continue;  // _kernels.py:162
+                    body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
                 }
             }
         }
     }
 };
 
-// Fast path: the tile's staged shared-memory planes and coordinate tables.
-// Sensors whose transform has no rotation/shear (T01 = T10 = 0) are
-// separable: X depends on x only, so the exact column offsets dx, dx^2 are
-// computed once per (sensor, phase) and kept in registers; the membership
-// test is then one float64 add per candidate.  Rotated sensors pre-test
-// |d|^2 in fp32 (error < 1e-5 px^2, margin 1e-3) and run the exact float64
-// test only for candidates near or inside the disk.
 // Adapter: a per-sample body as a traversal policy (no row hooks).
 template <class Body>
 struct PerSample {
@@ -125,6 +144,9 @@ struct TileSweep {
     const unsigned char *sm;
     const int (*org)[2];
     double qx, qy;
+    template <int PN>
+    __device__ __forceinline__ void reduce(Acc<PN> &) const {}
+    __device__ __forceinline__ double reduce(double v) const { return v; }
     // Per-sample traversal (same interface as GlobalSweep).
     template <class Body>
     __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
@@ -388,6 +410,7 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
                 __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
             acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
         });
+        sweep.reduce(acc);
     } else {
         const float hl = P.hl[c][k];
         sweep(c, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
@@ -430,7 +453,7 @@ __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k,
               if (ORDER >= 2) pg += dxx * g3 + __dmul_rn(dx, dy) * g4 + dyy * g5;
               if (ok) v = fma(t, pg * pg, v);  // select: unused columns carry sentinels
           });
-    return v;
+    return sweep.reduce(v);
 }
 
 struct PixelResult {
@@ -540,21 +563,24 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     return FIT_OK;
 }
 
+// One warp per work item: the lanes share every window's candidates.
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
     const uint32_t n = *P.work_count;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = warp; i < n; i += nwarps) {
         const uint32_t item = P.work_items[i];
         const int pix = (int)(item >> 2), c = (int)(item & 3);
         const int ox = pix % P.out_w, oy = pix / P.out_w;
-        const GlobalSweep sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        const GlobalSweep<32> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         PixelResult R;
         if (P.n_scales > 1) {
             if (ici<ORDER, true>(P, c, sweep, R) != FIT_OK) ladder<ORDER>(P, c, sweep, R);
         } else {
             ladder<ORDER>(P, c, sweep, R);
         }
-        write_result(P, pix, c, R);
+        if ((threadIdx.x & 31) == 0) write_result(P, pix, c, R);
     }
 }
 
@@ -702,12 +728,13 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
         for (int t = 0; t < n; ++t) {
             const Tap T = tp[t];
             const int k = base + T.delta;
+            // masked samples carry (0, 0) and padding taps W = 0, so w and the
+            // value are already zero exactly when the tap must not count
             const float2 e = vi[k];
-            const bool ok = e.y > 0.f && T.W > 0.f;
-            const float w = ok ? T.W * e.y : 0.f;
+            const float w = T.W * e.y;
             const double dxx = ORDER >= 2 ? __dmul_rn(T.dx, T.dx) : 0.0;
             const double dyy = ORDER >= 2 ? __dmul_rn(T.dy, T.dy) : 0.0;
-            acc.add((double)w, ok ? (double)e.x : 0.0, T.dx, T.dy, dxx, dyy, ok ? 1 : 0);
+            acc.add((double)w, (double)e.x, T.dx, T.dy, dxx, dyy, w > 0.f ? 1 : 0);
         }
     }
 }
@@ -776,7 +803,9 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #define HDR_O2_MINBLOCKS 2
 #endif
 template <int ORDER, bool ICI, int MAXC, bool PAT>
-__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : 2))
+// Tap-table order<=1 kernels must stay at <= 80 registers: 3 CTAs (768
+// threads) per SM is worth ~8% over 2 on cfg2.
+__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? 3 : 2)))
     lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
@@ -910,6 +939,7 @@ __device__ __forceinline__ void accumulate_hinv(const Sweep &sweep, int c, doubl
                                    __dmul_rn(__dmul_rn(h22, dy), dy));
         acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
     });
+    sweep.reduce(acc);
 }
 
 template <int ORDER, class Sweep>
@@ -948,11 +978,13 @@ __device__ bool steered_order(const DevParams &P, int c, const Sweep &sweep, con
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_steered_kernel(const __grid_constant__ DevParams P) {
     const int n = P.out_w * (P.row_end - P.row_begin) * 3;
-    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n; it += gridDim.x * blockDim.x) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int it = warp; it < n; it += nwarps) {  // one warp per pixel-channel
         const int c = it % 3, pl = it / 3;
         const int ox = pl % P.out_w, oy = P.row_begin + pl / P.out_w;
         const int pix = oy * P.out_w + ox;
-        const GlobalSweep sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        const GlobalSweep<32> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
         const double ct = cos(th), st = sin(th);
         const double h = P.h[c][0];  // channel scale
@@ -971,7 +1003,7 @@ __global__ void __launch_bounds__(128) lpa_steered_kernel(const __grid_constant_
             R.outcome = HDR_OUTCOME_NAN;
             R.count = 0;
         }
-        write_result(P, pix, c, R);
+        if ((threadIdx.x & 31) == 0) write_result(P, pix, c, R);
     }
 }
 
