@@ -605,12 +605,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
                      smem_addr(bar))
                  : "memory");
 }
+// Bounded wait: a barrier that never completes (a lost TMA transaction)
+// traps -- the launch fails with an error -- instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 24)) __trap();
+    }
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
                                             uint64_t *bar) {
@@ -621,11 +629,13 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
-__device__ __forceinline__ void region_origin(const DevSensor &S, const DevParams &P, int tx0,
+__device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParams &P, int tx0,
                                               int ty0, int tx1, int ty1, int &ox, int &oy) {
     // union of the window bboxes of the tile's corner queries at radius fast_R;
-    // the bbox is affine in q, so its minimum is attained at a corner.
-    int xmin = INT_MAX, ymin = INT_MAX;
+    // every bbox bound is a floor/ceil of a correctly rounded affine function
+    // of (qx, qy), monotone in each, so its extremes over the tile are
+    // attained at the corners.
+    int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double qx = qcoord((k & 1) ? tx1 : tx0, P.sx);
@@ -634,6 +644,8 @@ __device__ __forceinline__ void region_origin(const DevSensor &S, const DevParam
         window_bbox(S, qx, qy, P.fast_R, xlo, xhi, ylo, yhi);
         xmin = min(xmin, xlo);
         ymin = min(ymin, ylo);
+        xmax = max(xmax, xhi);
+        ymax = max(ymax, yhi);
     }
     // x: multiple of 8 elements -- a TMA tile copy must start on a 16-byte
     // boundary of the row (measured: unaligned starts raise an illegal-
@@ -641,6 +653,8 @@ __device__ __forceinline__ void region_origin(const DevSensor &S, const DevParam
     // Bayer phase of a staged pixel equals the parity of its coordinates.
     ox = xmin & ~7;
     oy = ymin & ~1;
+    // true: every window of every pixel of the tile lies inside the region
+    return xmax < ox + S.rw && ymax < oy + S.rh;
 }
 
 __device__ __forceinline__ void tile_bounds(const DevParams &P, int t, int &tx0, int &ty0, int &tx1,
@@ -660,49 +674,55 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
-// Thread 0: region origins of tile t and one 3-D TMA copy per sensor of the
-// four (f_hat, 1/den) phase planes' staged regions into plane buffer `pb`,
-// completing on `full` (arrive + expect_tx).
-__device__ __forceinline__ void stage_issue(const DevParams &P, unsigned char *pb, int t,
-                                            int (*org)[2], uint64_t *full) {
-    // warp 0: lane s computes sensor s's region origin, lane 0 issues the copies
+// One warp stages tile t into plane buffer `pb`: region origins + tile
+// coverage (lane s: sensor s), the f64 coordinate tables (rotated path), then
+// lane 0 issues one 3-D TMA copy per sensor of the four (f_hat, 1/den) phase
+// planes' staged regions, completing on `full` (arrive + expect_tx; the
+// arrive releases the origins and tables to the consumers).
+template <bool TABLES>
+__device__ __forceinline__ void stage_tile(const DevParams &P, unsigned char *pb, int t,
+                                           int (*org)[2], int *cov, uint64_t *full) {
     const int lane = threadIdx.x & 31;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
+    bool in = true;
     if (lane < P.n_sensors)
-        region_origin(P.s[lane], P, tx0, ty0, tx1, ty1, org[lane][0], org[lane][1]);
+        in = region_origin(P.s[lane], P, tx0, ty0, tx1, ty1, org[lane][0], org[lane][1]);
+    const bool all_in = __all_sync(0xffffffffu, in);
+    if (lane == 0) *cov = all_in ? 1 : 0;
     __syncwarp();
+    if constexpr (TABLES) {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int ox = org[s][0], oy = org[s][1];
+            // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y)
+            // (exact, since fl(T01*y) = fl(T10*x) = 0); otherwise the four
+            // partial products.
+            double *tx0t = (double *)(pb + S.off_tx0), *tx3t = (double *)(pb + S.off_tx3);
+            double *ty1t = (double *)(pb + S.off_ty1), *ty4t = (double *)(pb + S.off_ty4);
+            for (int i = lane; i < S.rw; i += 32) {
+                const double xd = (double)(ox + i);
+                const double a = __dmul_rn(S.T[0], xd);
+                tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
+                tx3t[i] = __dmul_rn(S.T[3], xd);
+            }
+            for (int i = lane; i < S.rh; i += 32) {
+                const double yd = (double)(oy + i);
+                const double bb = __dmul_rn(S.T[4], yd);
+                ty1t[i] = __dmul_rn(S.T[1], yd);
+                ty4t[i] = S.separable ? __dadd_rn(bb, S.T[5]) : bb;
+            }
+        }
+        __syncwarp();
+    }
     if (lane == 0) {
+        // the buffer's previous contents were read through the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         uint32_t bytes = 0;
         for (int s = 0; s < P.n_sensors; ++s) bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
         mbar_expect_tx(full, bytes);
         for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
             tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
-    }
-}
-
-// All threads: exact float64 coordinate tables of the staged regions.
-__device__ __forceinline__ void stage_tables(const DevParams &P, unsigned char *pb,
-                                             const int (*org)[2]) {
-    for (int s = 0; s < P.n_sensors; ++s) {
-        const DevSensor &S = P.s[s];
-        const int ox = org[s][0], oy = org[s][1];
-        // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y) (exact,
-        // since fl(T01*y) = fl(T10*x) = 0); otherwise the four partial products.
-        double *tx0t = (double *)(pb + S.off_tx0), *tx3t = (double *)(pb + S.off_tx3);
-        double *ty1t = (double *)(pb + S.off_ty1), *ty4t = (double *)(pb + S.off_ty4);
-        for (int i = threadIdx.x; i < S.rw; i += NT) {
-            const double xd = (double)(ox + i);
-            const double a = __dmul_rn(S.T[0], xd);
-            tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
-            tx3t[i] = __dmul_rn(S.T[3], xd);
-        }
-        for (int i = threadIdx.x; i < S.rh; i += NT) {
-            const double yd = (double)(oy + i);
-            const double bb = __dmul_rn(S.T[4], yd);
-            ty1t[i] = __dmul_rn(S.T[1], yd);
-            ty4t[i] = S.separable ? __dadd_rn(bb, S.T[5]) : bb;
-        }
     }
 }
 
@@ -741,7 +761,8 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
 
 template <int ORDER, bool ICI, int MAXC, bool PAT>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
-                                             const Tap *taps, int t, const int (*org)[2]) {
+                                             const Tap *taps, int t, const int (*org)[2],
+                                             bool tile_covered) {
     constexpr int PN = NC<ORDER>::P;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
@@ -751,9 +772,10 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     const int pix = py * P.out_w + px;
     const double qx = qcoord(px, P.sx), qy = qcoord(py, P.sy);
 
-    // every window of this pixel must lie inside the staged region
+    // every window of this pixel must lie inside the staged region (checked
+    // per pixel only when the tile as a whole is not covered)
     bool covered = true;
-    for (int s = 0; s < P.n_sensors; ++s) {
+    for (int s = 0; !tile_covered && s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
         int xlo, xhi, ylo, yhi;
         window_bbox(S, qx, qy, P.fast_R, xlo, xhi, ylo, yhi);
@@ -809,6 +831,8 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? 3 
     lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
+    __shared__ int s_cov[2];
+    __shared__ unsigned s_done[2];
     __shared__ __align__(8) uint64_t bar_full[2];
     const int ntiles = P.tiles_x * P.tiles_y;
     const Tap *taps = (const Tap *)(smem + P.off_taps);
@@ -822,23 +846,42 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? 3 
     if (threadIdx.x == 0) {
         mbar_init(&bar_full[0], 1);
         mbar_init(&bar_full[1], 1);
+        s_done[0] = s_done[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    if (threadIdx.x < 32 && t < ntiles) stage_issue(P, planes, t, s_org[0], &bar_full[0]);
-    __syncthreads();  // s_org[0] visible to every thread
+    __syncthreads();  // barriers initialised, taps staged
+    // prologue: warp 0 stages this CTA's first two tiles
+    if (threadIdx.x < 32) {
+        if (t < ntiles) stage_tile<!PAT>(P, planes, t, s_org[0], &s_cov[0], &bar_full[0]);
+        if (t + (int)gridDim.x < ntiles)
+            stage_tile<!PAT>(P, planes + P.buf_stride, t + gridDim.x, s_org[1], &s_cov[1],
+                             &bar_full[1]);
+    }
+    // No CTA-wide barrier in the loop: a warp waits only for its tile's data.
+    // The LAST warp to finish tile t (buffer b) refills b with tile t + 2G, so
+    // warps that finish early run ahead into tile t + G instead of idling at a
+    // __syncthreads while the slowest warp of the tile completes.
+    constexpr int NWARPS = NT / 32;
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
         const int b = i & 1;
         unsigned char *pb = planes + b * P.buf_stride;
-        const int tn = t + gridDim.x;
-        // buffer b^1 was last read in iteration i-1 (closed by its trailing barrier)
-        if (threadIdx.x < 32 && tn < ntiles)
-            stage_issue(P, planes + (b ^ 1) * P.buf_stride, tn, s_org[b ^ 1], &bar_full[b ^ 1]);
-        stage_tables(P, pb, s_org[b]);
         mbar_wait(&bar_full[b], (uint32_t)((i >> 1) & 1));
-        __syncthreads();
-        tile_compute<ORDER, ICI, MAXC, PAT>(P, pb, taps, t, s_org[b]);
-        __syncthreads();
+        tile_compute<ORDER, ICI, MAXC, PAT>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
+        const int tn = t + 2 * (int)gridDim.x;
+        if (tn < ntiles) {  // CTA-uniform
+            __syncwarp();
+            unsigned last = 0;
+            if ((threadIdx.x & 31) == 0) {
+                __threadfence_block();  // this warp's reads of buffer b precede the count
+                last = atomicAdd(&s_done[b], 1u) == NWARPS - 1;
+                if (last) {
+                    s_done[b] = 0;
+                    __threadfence_block();
+                }
+            }
+            if (__shfl_sync(0xffffffffu, last, 0))
+                stage_tile<!PAT>(P, pb, tn, s_org[b], &s_cov[b], &bar_full[b]);
+        }
     }
 }
 
