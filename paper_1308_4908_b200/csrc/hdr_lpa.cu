@@ -730,39 +730,65 @@ __device__ __forceinline__ void stage_tile(const DevParams &P, unsigned char *pb
 // output pixel of a parity class visits the same sensor offsets with the same
 // weights, so there is no membership test, no exp and no loop control beyond
 // the tap list (the samples and weights are the reference's: DESIGN.md s3).
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
 template <int ORDER>
 __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
-                                                const Tap *taps, const int (*org)[2], int c,
-                                                int px, int py, Acc<NC<ORDER>::P> &acc) {
+                                                const unsigned char *taps, const int (*org)[2],
+                                                int c, int px, int py, Acc<NC<ORDER>::P> &acc) {
     acc.zero();
     const int cls = ((py & 1) << 1) | (px & 1);
+    // shared-window addresses: one LDS.128 (dx, dy), one LDS.64 (W, byte
+    // offset) and one LDS.64 (f_hat, 1/den) per tap
+    const uint32_t txy = smem_addr(taps);
+    const uint32_t tw = txy + (uint32_t)P.n_taps * (uint32_t)sizeof(TapXY);
+    int count = 0;
     for (int s = 0; s < P.n_sensors; ++s) {
         const int n = P.pat_cnt[s][c][py & 1];
         if (!n) continue;
         const DevSensor &S = P.s[s];
-        const Tap *tp = taps + P.pat_off[s][c][cls];
-        const float2 *vi = (const float2 *)(sm + S.off_vi);
+        const int o = P.pat_off[s][c][cls];
         const int pw = S.rw >> 1;
-        // base: the pixel's own position in its phase plane (origins are even)
-        const int base = ((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1);
-        for (int t = 0; t < n; ++t) {
-            const Tap T = tp[t];
-            const int k = base + T.delta;
+        // the pixel's own position in its phase plane (origins are even)
+        const uint32_t vb = smem_addr(sm + S.off_vi) +
+                            8u * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+        for (int t = o; t < o + n; ++t) {
+            const double2 X = lds_d2(txy + 16u * (uint32_t)t);
+            const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
             // masked samples carry (0, 0) and padding taps W = 0, so w and the
             // value are already zero exactly when the tap must not count
-            const float2 e = vi[k];
-            const float w = T.W * e.y;
-            const double dxx = ORDER >= 2 ? __dmul_rn(T.dx, T.dx) : 0.0;
-            const double dyy = ORDER >= 2 ? __dmul_rn(T.dy, T.dy) : 0.0;
-            acc.add((double)w, (double)e.x, T.dx, T.dy, dxx, dyy, w > 0.f ? 1 : 0);
+            const float2 e = lds_f2(vb + Q.y);
+            const float w = __uint_as_float(Q.x) * e.y;
+            const double dxx = ORDER >= 2 ? __dmul_rn(X.x, X.x) : 0.0;
+            const double dyy = ORDER >= 2 ? __dmul_rn(X.y, X.y) : 0.0;
+            acc.add((double)w, (double)e.x, X.x, X.y, dxx, dyy, 0);
+            // predicated increment (setp + @p add): one instruction less than a select
+            asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, 0f00000000;\n @p add.s32 %0, %0, 1;\n}"
+                : "+r"(count)
+                : "f"(w));
         }
     }
+    acc.count = count;
 }
 
 template <int ORDER, bool ICI, int MAXC, bool PAT>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
-                                             const Tap *taps, int t, const int (*org)[2],
-                                             bool tile_covered) {
+                                             const unsigned char *taps, int t,
+                                             const int (*org)[2], bool tile_covered) {
     constexpr int PN = NC<ORDER>::P;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
@@ -835,7 +861,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? 3 
     __shared__ unsigned s_done[2];
     __shared__ __align__(8) uint64_t bar_full[2];
     const int ntiles = P.tiles_x * P.tiles_y;
-    const Tap *taps = (const Tap *)(smem + P.off_taps);
+    const unsigned char *taps = smem + P.off_taps;
     unsigned char *planes = smem + P.plane_base;
     if (PAT) {
         const uint32_t *src = (const uint32_t *)P.taps;
@@ -1502,13 +1528,23 @@ static uint64_t fnv1a(const void *p, size_t n) {
 static int upload_taps(const std::vector<Tap> &taps, void *dst, cudaStream_t st) {
     static std::mutex mu;
     static std::unordered_map<void *, uint64_t> last;
-    const size_t bytes = taps.size() * sizeof(Tap);
-    const uint64_t sig = fnv1a(taps.data(), bytes) ^ (uint64_t)bytes;
+    const size_t n = taps.size(), bytes = n * (sizeof(TapXY) + sizeof(TapW));
+    static std::vector<unsigned char> soa;
+    const uint64_t sig = fnv1a(taps.data(), n * sizeof(Tap)) ^ (uint64_t)bytes;
     std::lock_guard<std::mutex> lock(mu);
     auto it = last.find(dst);
     if (it != last.end() && it->second == sig) return HDR_OK;
+    soa.resize(bytes);
+    TapXY *xy = (TapXY *)soa.data();
+    TapW *w = (TapW *)(soa.data() + n * sizeof(TapXY));
+    for (size_t i = 0; i < n; ++i) {
+        xy[i].dx = taps[i].dx;
+        xy[i].dy = taps[i].dy;
+        w[i].W = taps[i].W;
+        w[i].off = taps[i].delta * (int)sizeof(float2);
+    }
     // pageable source: the copy is staged before cudaMemcpyAsync returns
-    if (cudaMemcpyAsync(dst, taps.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    if (cudaMemcpyAsync(dst, soa.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return HDR_ERR_CUDA;
     last[dst] = sig;
     return HDR_OK;
@@ -1686,7 +1722,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.pat = build_taps(P, taps) ? 1 : 0;
     if (P.pat) {
         P.off_taps = take((int)(taps.size() * sizeof(Tap)));
-        P.taps = (const Tap *)((char *)workspace + WS_HEADER);
+        P.taps = (const void *)((char *)workspace + WS_HEADER);
     }
     P.plane_base = smem;
     smem = 0;

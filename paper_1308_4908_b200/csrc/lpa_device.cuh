@@ -62,6 +62,15 @@ struct Tap {
     float W;
     int delta;  // offset of the sample in the sensor's phase planes relative to the pixel's base
 };
+// Device layout of the tap table (structure of arrays, one LDS.128 + one
+// LDS.64 per tap): n x TapXY, then n x TapW.
+struct __align__(16) TapXY {
+    double dx, dy;
+};
+struct TapW {
+    float W;
+    int off;  // delta in bytes (float2 elements x 8)
+};
 
 struct DevParams {
     CUtensorMap tmap[MAXS];   // per-sensor 3-D maps over the phase planes (box = staged region)
@@ -87,7 +96,7 @@ struct DevParams {
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, pad2;
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
-    const Tap *taps;                // device copy (in the workspace), staged into shared memory
+    const void *taps;               // device copy (in the workspace), staged into shared memory
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
     int pat_base[MAXS][2];          // offset (ox, oy) of the tap window's origin: see build_taps
