@@ -850,10 +850,13 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #ifndef HDR_O2_MINBLOCKS
 #define HDR_O2_MINBLOCKS 2
 #endif
+#ifndef HDR_PAT_MINBLOCKS
+#define HDR_PAT_MINBLOCKS 3
+#endif
 template <int ORDER, bool ICI, int MAXC, bool PAT>
-// Tap-table order<=1 kernels must stay at <= 80 registers: 3 CTAs (768
-// threads) per SM is worth ~8% over 2 on cfg2.
-__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? 3 : 2)))
+// Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
+// by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
+__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
     lpa_fast_kernel(const __grid_constant__ DevParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
