@@ -21,9 +21,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <climits>
+#include <type_traits>
 #include <math.h>
-#include <mutex>
-#include <unordered_map>
 #include <vector>
 #include <stdio.h>
 #include <string.h>
@@ -37,7 +36,7 @@ constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per ti
 
 // workspace layout: [header: work counter][pre-computed taps][work items]
 static const size_t WS_HEADER = 256;
-static const size_t WS_TAPS = 64 * 1024;  // <= 2730 taps
+static const size_t LUT_BYTES = 65536 * sizeof(double2);
 
 template <int ORDER>
 struct NC {
@@ -47,13 +46,14 @@ struct NC {
 // ---------------------------------------------------------------------------
 // Window sweeps.  A sweep enumerates the samples of one channel inside the
 // support disk |X - q| <= r, in the order (sensor, Bayer phase, row, column),
-// and calls body(value, 1/den, dx, dy, dx^2, dy^2, |d|^2 as fp32) for each.
+// and calls body(value, 1/den, dx, dy, dx^2, dy^2, |d|^2 as fp32) for each
+// (value and 1/den: fp32 in the tile sweeps, float64 in the global sweep).
 // Offsets and the membership test are float64 in the reference's exact
 // operation order (radiometry.py:84, _kernels.py:160-163), so both sweeps
 // below select exactly the reference's sample set in the same order.
 // ---------------------------------------------------------------------------
 
-// Slow path: straight from global memory (the per-frame phase planes).
+// Slow path: straight from the raw frames in global memory, float64 radiometry.
 // LANES > 1: the candidates of every window are split over the lanes of a
 // warp (candidate j -> lane j % 32) and the sums are combined by a butterfly
 // reduction, after which every lane holds bitwise-identical totals.
@@ -102,12 +102,8 @@ struct GlobalSweep {
                     const int y = ys + 2 * (j / ncol), x = xs + 2 * (j % ncol);
                     const double yd = (double)y;
                     const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
-                    const bool yin = y >= 0 && y < S.height;
-                    const float2 *row = S.phase + ((size_t)ph * S.phg + (y >> 1)) * S.pwg;
-                    // the per-frame phase planes hold radiance_sample(S, x, y)
-                    const float2 e = (yin && x >= 0 && x < S.width) ? __ldg(row + (x >> 1))
-                                                                     : make_float2(0.f, 0.f);
-                    if (!(e.y > 0.f)) continue;  // saturated / defective / off-frame
+                    double f, iv;  // float64 radiometry straight from the raw frame
+                    if (!radiance_exact(S, x, y, P.use_sigma, f, iv)) continue;
                     const double xd = (double)x;
                     const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
                     const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
@@ -115,7 +111,7 @@ struct GlobalSweep {
                     const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                     const double d2 = __dadd_rn(dxx, dyy);
                     if (d2 > r2) continue;  // _kernels.py:162
-                    body(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                    body(true, f, iv, dx, dy, dxx, dyy, (float)d2);
                 }
             }
         }
@@ -305,6 +301,7 @@ struct RowMoments {
                                            double, double, float d2f) {
         const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double w = (double)w32, y = ok ? v : 0.0;
+        acc.sabs = fmaf(w32, fabsf((float)y), acc.sabs);
         double p = w;
 #pragma unroll
         for (int n = 0; n <= 2 * ORDER; ++n) {
@@ -339,17 +336,22 @@ struct RowMoments {
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f) {
         const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
-        acc.add((double)w, ok ? v : 0.0, dx, dy, dxx, dyy, ok ? 1 : 0);
+        const double y = ok ? v : 0.0;
+        acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+        acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
     }
 };
 
 // Row-factored variance sweep (ICI, fast path): phi.g = c0(dy) + dx (c1(dy) + g3 dx).
+// Also accumulates T = sum w |phi.g| |y| (fp32): the sharp precision bound of
+// c0 (fit_precise_sharp).
 template <int ORDER>
 struct RowVariance {
     const double *g;
     float hl;
     bool sig;
     double v, c0, c1;
+    float T;
     __device__ __forceinline__ void begin_row(double dy, double dyy) {
         c0 = g[0];
         c1 = 0.0;
@@ -363,23 +365,29 @@ struct RowVariance {
         }
     }
     __device__ __forceinline__ void end_row(double, double) {}
-    __device__ __forceinline__ void sample(bool ok, double, float iv, double dx, double, double,
+    __device__ __forceinline__ void sample(bool ok, double y, float iv, double dx, double, double,
                                            double, float d2f) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
         const double t = (double)(sig ? W * W : W * W * iv);
         double pg = c0;
         if (ORDER == 1) pg = fma(dx, c1, c0);
         if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
-        if (ok) v = fma(t, pg * pg, v);
+        if (ok) {
+            v = fma(t, pg * pg, v);
+            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+        }
     }
-    __device__ __forceinline__ void general(bool ok, double, float iv, double dx, double dy,
+    __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
         const double t = (double)(sig ? W * W : W * W * iv);
         double pg = g[0];
         if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
         if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
-        if (ok) v = fma(t, pg * pg, v);
+        if (ok) {
+            v = fma(t, pg * pg, v);
+            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+        }
     }
 };
 
@@ -404,7 +412,7 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
     acc.zero();
     if constexpr (EXACT) {
         const double hi = P.hinv[c][k];
-        sweep(c, r, r2, [&](bool, double v, float iv, double dx, double dy, double dxx, double dyy,
+        sweep(c, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
                             float) {
             const double q =
                 __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
@@ -416,7 +424,9 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
         sweep(c, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
                             double dyy, float d2f) {
             const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;  // w = W / den
-            acc.add((double)w, ok ? v : 0.0, dx, dy, dxx, dyy, ok ? 1 : 0);
+            const double y = ok ? v : 0.0;
+            acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+            acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
         });
     }
 }
@@ -425,10 +435,11 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
 // with w^2 var = W^2/den for variance weights and W^2 for sigma weights.
 template <int ORDER, bool EXACT, class Sweep>
 __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, const Sweep &sweep,
-                                               const double *g) {
+                                               const double *g, float *tsum = nullptr) {
     if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
-        RowVariance<ORDER> pol{g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0};
+        RowVariance<ORDER> pol{g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0, 0.f};
         sweep.rows(c, P.r[c][k], P.r2[c][k], pol);
+        if (tsum) *tsum = pol.T;
         return pol.v;
     }
     const bool sig = P.use_sigma;
@@ -436,8 +447,9 @@ __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k,
     const float hl = P.hl[c][k];
     const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4], g5 = g[5];
     double v = 0.0;
+    float T = 0.f;
     sweep(c, P.r[c][k], P.r2[c][k],
-          [&](bool ok, double, float iv, double dx, double dy, double dxx, double dyy, float d2f) {
+          [&](bool ok, double y, auto iv, double dx, double dy, double dxx, double dyy, float d2f) {
               double t;
               if constexpr (EXACT) {
                   const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx),
@@ -452,7 +464,12 @@ __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k,
               if (ORDER >= 1) pg += dx * g1 + dy * g2;
               if (ORDER >= 2) pg += dxx * g3 + __dmul_rn(dx, dy) * g4 + dyy * g5;
               if (ok) v = fma(t, pg * pg, v);  // select: unused columns carry sentinels
+              if constexpr (!EXACT) {
+                  const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+                  if (ok) T = fmaf(W * (float)iv, fabsf((float)pg) * fabsf((float)y), T);
+              }
           });
+    if (tsum) *tsum = T;
     return sweep.reduce(v);
 }
 
@@ -534,6 +551,7 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     Acc<PN> acc;
     Fit fit;
     double L = 0.0, U = 0.0;
+    bool precise = true;
     for (int k = 0; k < P.n_scales; ++k) {
         accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
         const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
@@ -542,7 +560,8 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
             if (k == 0) return FIT_FAIL;
             break;  // an invalid scale ends the search at k-1
         }
-        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g));
+        float tk = 0.f;
+        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk));
         const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
         if (k == 0) {
             L = lo;
@@ -557,7 +576,9 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         R.gy = fit.c2;
         R.sidx = k;
         R.count = acc.count;
+        if constexpr (!EXACT) precise = fit_precise_sharp(fit.c0, tk, P.prec_floor);
     }
+    if (!precise) return FIT_AMBIG;  // selected estimate too close to fp32 rounding limits
     if (ORDER == 0) R.gx = R.gy = qnan();
     R.outcome = ORDER * 16;
     return FIT_OK;
@@ -757,6 +778,7 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
     const uint32_t txy = smem_addr(taps);
     const uint32_t tw = txy + (uint32_t)P.n_taps * (uint32_t)sizeof(TapXY);
     int count = 0;
+    float sabs = 0.f;
     for (int s = 0; s < P.n_sensors; ++s) {
         const int n = P.pat_cnt[s][c][py & 1];
         if (!n) continue;
@@ -773,6 +795,7 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
             // value are already zero exactly when the tap must not count
             const float2 e = lds_f2(vb + Q.y);
             const float w = __uint_as_float(Q.x) * e.y;
+            sabs = fmaf(w, fabsf(e.x), sabs);
             const double dxx = ORDER >= 2 ? __dmul_rn(X.x, X.x) : 0.0;
             const double dyy = ORDER >= 2 ? __dmul_rn(X.y, X.y) : 0.0;
             acc.add((double)w, (double)e.x, X.x, X.y, dxx, dyy, 0);
@@ -783,6 +806,7 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
         }
     }
     acc.count = count;
+    acc.sabs = sabs;
 }
 
 template <int ORDER, bool ICI, int MAXC, bool PAT>
@@ -825,6 +849,15 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor)) {
+                    // loose bound failed: the sharp one needs a sweep with g (not
+                    // for the tap path, where this is rare); else the exact path
+                    float tk = 0.f;
+                    if constexpr (!PAT && ORDER >= 1)
+                        fit_variance<ORDER, false>(P, c, 0, sweep, fit.g, &tk);
+                    if (PAT || ORDER == 0 || !fit_precise_sharp(fit.c0, tk, P.prec_floor))
+                        st = FIT_AMBIG;
+                }
                 if (st == FIT_OK) {
                     R.count = acc.count;
                     R.val = fit.c0;
@@ -857,7 +890,8 @@ template <int ORDER, bool ICI, int MAXC, bool PAT>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
-    lpa_fast_kernel(const __grid_constant__ DevParams P) {
+    lpa_fast_kernel(const __grid_constant__ DevParams P,
+                    const __grid_constant__ typename std::conditional<PAT, TapParam, NoTaps>::type T) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[2][MAXS][2];
     __shared__ int s_cov[2];
@@ -866,10 +900,11 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
     unsigned char *planes = smem + P.plane_base;
-    if (PAT) {
-        const uint32_t *src = (const uint32_t *)P.taps;
-        uint32_t *dst = (uint32_t *)(smem + P.off_taps);
-        for (int i = threadIdx.x; i < P.n_taps * (int)(sizeof(Tap) / 4); i += NT) dst[i] = src[i];
+    if constexpr (PAT) {
+        const uint4 *src = (const uint4 *)T.bytes;
+        uint4 *dst = (uint4 *)(smem + P.off_taps);
+        const int n16 = P.n_taps * (int)sizeof(Tap) / 16 + 1;  // 24 B per tap, 16-B chunks
+        for (int i = threadIdx.x; i < n16 && 16 * i < TAP_PARAM_BYTES; i += NT) dst[i] = src[i];
     }
     int t = blockIdx.x;
     if (threadIdx.x == 0) {
@@ -912,6 +947,17 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
                 stage_tile<!PAT>(P, pb, tn, s_org[b], &s_cov[b], &bar_full[b]);
         }
     }
+}
+
+// Exact radiometry LUT (scalar calibration): entry v = radiance_exact of a
+// raw value v below saturation, for the slow path's float64 sweeps.
+__global__ void radiance_lut_kernel(const __grid_constant__ DevParams P) {
+    const DevSensor &S = P.s[blockIdx.y];
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (S.planes || v >= S.sat) return;
+    double f, iv;
+    radiometry_exact(S, v, S.bias, S.nonuni, S.readvar, P.use_sigma, f, iv);
+    S.lut[v] = make_double2(f, iv);
 }
 
 // Per-frame radiometric pre-pass: every raw pixel converted once into the
@@ -1003,7 +1049,7 @@ __device__ __forceinline__ void accumulate_hinv(const Sweep &sweep, int c, doubl
                                                 Acc<NC<ORDER>::P> &acc) {
     acc.zero();
     const double h12x2 = 2.0 * h12;
-    sweep(c, r, r2, [&](bool, double v, float iv, double dx, double dy, double dxx, double dyy,
+    sweep(c, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
                         float) {
         // q = h11*dx*dx + 2.0*h12*dx*dy + h22*dy*dy (_kernels.py:164)
         const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(h11, dx), dx),
@@ -1380,7 +1426,8 @@ static int set_smem_attr(const void *fn, int bytes) {
 }
 
 template <int ORDER, bool ICI, int MAXC, bool PAT = false>
-static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream_t st) {
+static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
+                       cudaStream_t st) {
     const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148, per_sm = 1;
@@ -1390,7 +1437,10 @@ static int launch_fast(const DevParams &P, int tiles, int smem_bytes, cudaStream
         per_sm < 1)
         return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
-    lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P);
+    if constexpr (PAT)
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P, T);
+    else
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_fast_kernel launch");
 }
 
@@ -1426,16 +1476,17 @@ static bool encode_phase_map(const DevSensor &d, CUtensorMap *map) {
 }
 
 template <int ORDER>
-static int launch_all(const DevParams &P, int tiles, int smem_bytes, int maxc, cudaStream_t st) {
+static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem_bytes, int maxc,
+                      cudaStream_t st) {
     int rc;
     if (P.pat)
-        rc = launch_fast<ORDER, false, 4, true>(P, tiles, smem_bytes, st);
+        rc = launch_fast<ORDER, false, 4, true>(P, T, tiles, smem_bytes, st);
     else if (P.n_scales > 1)
-        rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, true, 8>(P, tiles, smem_bytes, st);
+        rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, true, 8>(P, T, tiles, smem_bytes, st);
     else
-        rc = maxc <= 4 ? launch_fast<ORDER, false, 4>(P, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, false, 8>(P, tiles, smem_bytes, st);
+        rc = maxc <= 4 ? launch_fast<ORDER, false, 4>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, false, 8>(P, T, tiles, smem_bytes, st);
     if (rc != HDR_OK) return rc;
     if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;
     int dev = 0, nsm = 148;
@@ -1516,42 +1567,11 @@ static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
             }
         }
     }
-    if (taps.size() * sizeof(Tap) > WS_TAPS) return false;
+    if (taps.size() * sizeof(Tap) > TAP_PARAM_BYTES) return false;
     P.n_taps = (int)taps.size();
     return true;
 }
 
-static uint64_t fnv1a(const void *p, size_t n) {
-    uint64_t h = 1469598103934665603ull;
-    for (size_t i = 0; i < n; ++i) h = (h ^ ((const unsigned char *)p)[i]) * 1099511628211ull;
-    return h;
-}
-
-// Upload the tap table into the workspace unless this workspace already holds it.
-static int upload_taps(const std::vector<Tap> &taps, void *dst, cudaStream_t st) {
-    static std::mutex mu;
-    static std::unordered_map<void *, uint64_t> last;
-    const size_t n = taps.size(), bytes = n * (sizeof(TapXY) + sizeof(TapW));
-    static std::vector<unsigned char> soa;
-    const uint64_t sig = fnv1a(taps.data(), n * sizeof(Tap)) ^ (uint64_t)bytes;
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = last.find(dst);
-    if (it != last.end() && it->second == sig) return HDR_OK;
-    soa.resize(bytes);
-    TapXY *xy = (TapXY *)soa.data();
-    TapW *w = (TapW *)(soa.data() + n * sizeof(TapXY));
-    for (size_t i = 0; i < n; ++i) {
-        xy[i].dx = taps[i].dx;
-        xy[i].dy = taps[i].dy;
-        w[i].W = taps[i].W;
-        w[i].off = taps[i].delta * (int)sizeof(float2);
-    }
-    // pageable source: the copy is staged before cudaMemcpyAsync returns
-    if (cudaMemcpyAsync(dst, soa.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return HDR_ERR_CUDA;
-    last[dst] = sig;
-    return HDR_OK;
-}
 
 }  // namespace hdrlpa
 
@@ -1577,8 +1597,10 @@ const char *hdr_lpa_status_string(int status) {
     }
 }
 
-// Workspace layout: [header][pre-computed taps][phase planes of every sensor]
-// [work items].  Phase planes: per sensor [4][phg][pwg] float2 with
+// Workspace layout: [header][phase planes of every sensor]
+// [exact radiometry LUT of every sensor][work items].  LUT: 65536 x
+// (f_hat, 1/den) float64 per sensor, indexed by the raw value (scalar
+// calibration only).  Phase planes: per sensor [4][phg][pwg] float2 with
 // pwg = ceil(w/2) rounded up to even (16-B rows), phg = ceil(h/2).
 static size_t phase_bytes(const HdrSensor &s) {
     const size_t pwg = (size_t)(((s.width + 1) / 2 + 1) & ~1), phg = (size_t)((s.height + 1) / 2);
@@ -1595,7 +1617,8 @@ int hdr_lpa_workspace_bytes(const HdrSensor *sensors, int n_sensors, int out_w, 
         if (sensors[s].width <= 0 || sensors[s].height <= 0) return HDR_ERR_ARG;
         planes += phase_bytes(sensors[s]);
     }
-    *bytes = WS_HEADER + WS_TAPS + planes + (size_t)out_w * out_h * 3 * sizeof(uint32_t);
+    *bytes = WS_HEADER + planes + (size_t)n_sensors * LUT_BYTES +
+             (size_t)out_w * out_h * 3 * sizeof(uint32_t);
     return HDR_OK;
 }
 
@@ -1638,6 +1661,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.max_radius = params->max_radius;
     P.cond = params->cond_threshold;
     P.gamma = params->ici_gamma;
+    P.prec_floor = 10.0;  // e/s: the parity tests' relative-error floor (oracle/compare.py)
     fastR = 0.0;
     for (int c = 0; c < 3; ++c)
         for (int k = 0; k < P.n_scales; ++k) {
@@ -1661,7 +1685,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.count = out->count;
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
-    char *wsp = (char *)workspace + WS_HEADER + WS_TAPS;
+    char *wsp = (char *)workspace + WS_HEADER;
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
         d.phase = (float2 *)wsp;
@@ -1669,12 +1693,23 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
         d.phg = (d.height + 1) / 2;
         wsp += phase_bytes(sensors[s]);
     }
+    for (int s = 0; s < n_sensors; ++s) {
+        P.s[s].lut = (double2 *)wsp;
+        wsp += LUT_BYTES;
+    }
     P.work_items = (uint32_t *)wsp;
 
     return HDR_OK;
 }
 
 static int launch_prepass(const DevParams &P, cudaStream_t st) {
+    int maxsat = 0;
+    for (int s = 0; s < P.n_sensors; ++s)
+        if (!P.s[s].planes) maxsat = max(maxsat, P.s[s].sat);
+    if (maxsat > 0) {
+        radiance_lut_kernel<<<dim3((maxsat + 255) / 256, P.n_sensors), 256, 0, st>>>(P);
+        if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("radiance_lut_kernel launch");
+    }
     int maxpw = 0, maxph = 0;
     for (int s = 0; s < P.n_sensors; ++s) {
         maxpw = max(maxpw, P.s[s].pwg);
@@ -1722,10 +1757,20 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         maxc = max(maxc, (int)floor(fastR * d.nrow0) + 2);
     }
     std::vector<Tap> taps;
+    static thread_local TapParam T;  // kernel-parameter image of the tap table
     P.pat = build_taps(P, taps) ? 1 : 0;
     if (P.pat) {
         P.off_taps = take((int)(taps.size() * sizeof(Tap)));
-        P.taps = (const void *)((char *)workspace + WS_HEADER);
+        // SoA layout (TapXY[n], TapW[n]) in the kernel parameter
+        const size_t n = taps.size();
+        TapXY *xy = (TapXY *)T.bytes;
+        TapW *w = (TapW *)(T.bytes + n * sizeof(TapXY));
+        for (size_t i = 0; i < n; ++i) {
+            xy[i].dx = taps[i].dx;
+            xy[i].dy = taps[i].dy;
+            w[i].W = taps[i].W;
+            w[i].off = taps[i].delta * (int)sizeof(float2);
+        }
     }
     P.plane_base = smem;
     smem = 0;
@@ -1752,14 +1797,12 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     const int tiles = P.tiles_x * P.tiles_y;
     if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
-    if (P.pat && upload_taps(taps, (char *)workspace + WS_HEADER, st) != HDR_OK)
-        return cuda_fail("tap upload");
     if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;  // per-frame radiometry
     int rc;
     switch (P.order) {
-        case 0: rc = launch_all<0>(P, tiles, smem_bytes, maxc, st); break;
-        case 1: rc = launch_all<1>(P, tiles, smem_bytes, maxc, st); break;
-        default: rc = launch_all<2>(P, tiles, smem_bytes, maxc, st); break;
+        case 0: rc = launch_all<0>(P, T, tiles, smem_bytes, maxc, st); break;
+        case 1: rc = launch_all<1>(P, T, tiles, smem_bytes, maxc, st); break;
+        default: rc = launch_all<2>(P, T, tiles, smem_bytes, maxc, st); break;
     }
     return rc;
 }

@@ -47,6 +47,7 @@ struct DevSensor {
     // fast-path staging geometry
     int rw, rh;               // staged region (even), phase planes are (rh/2) x (rw/2)
     int off_vi;               // byte offset (in a plane buffer) of the 4 staged phase planes
+    double2 *lut;             // exact (f_hat, 1/den) per raw value (scalar calibration)
     float2 *phase;            // global phase planes [4][phg][pwg] of (f_hat, 1/den) (workspace)
     int pwg, phg;             // their padded width (float2 elements) and height
     int off_tx0, off_tx3;     // f64 tables fl(T00*x), fl(T10*x) over the region's columns
@@ -71,6 +72,14 @@ struct TapW {
     float W;
     int off;  // delta in bytes (float2 elements x 8)
 };
+// The tap table travels as a __grid_constant__ kernel parameter (kernel
+// parameters may total 32764 B; DevParams takes ~5.6 KB): no device copy whose
+// lifetime could outlive the caller's workspace.
+constexpr int TAP_PARAM_BYTES = 26880;  // 1120 taps
+struct __align__(16) TapParam {
+    unsigned char bytes[TAP_PARAM_BYTES];
+};
+struct NoTaps {};
 
 struct DevParams {
     CUtensorMap tmap[MAXS];   // per-sensor 3-D maps over the phase planes (box = staged region)
@@ -96,7 +105,6 @@ struct DevParams {
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, pad2;
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
-    const void *taps;               // device copy (in the workspace), staged into shared memory
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
     int pat_base[MAXS][2];          // offset (ox, oy) of the tap window's origin: see build_taps
@@ -104,6 +112,7 @@ struct DevParams {
     uint32_t *work_items;
     // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)
     const double *st_theta, *st_sigma, *st_gamma;
+    double prec_floor;              // fit_precise: radiance below which only absolute precision counts
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -161,6 +170,47 @@ __device__ __forceinline__ float2 radiance_sample(const DevSensor &S, int x, int
     return radiance_from_raw(S, raw, x, y, use_sigma);
 }
 
+// float64 radiometry in the reference's operation order (the oracle's
+// pixel_sample; radiometry.py:264-336, radiometry.py:240 stores sigma^2,
+// _kernels.py:165-167 divides by sigma^2 or sqrt(sigma^2)).  Returns false
+// for "no sample"; iv = 1/den (one rounding more than the reference's W/den).
+// Used by the exact (slow) path, whose results must not inherit the fp32
+// rounding of the staged phase planes.
+__device__ __forceinline__ void radiometry_exact(const DevSensor &S, int raw, double b, double a,
+                                                 double vr, int use_sigma, double &f, double &iv) {
+    const double denom = __dmul_rn(__dmul_rn(__dmul_rn(S.g, S.t), S.n), a);
+    f = __ddiv_rn(__dsub_rn((double)raw, b), denom);
+    const double d2 = __dmul_rn(denom, denom);
+    const double shot = __dmul_rn(
+        __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(S.g, S.g), S.t), a), S.n), f > 0.0 ? f : 0.0);
+    const double var = __ddiv_rn(__dadd_rn(shot, vr), d2);
+    const double qv = __ddiv_rn(1.0 / 12.0, d2);
+    const double sg = __dsqrt_rn(var >= qv ? var : qv);
+    double den = __dmul_rn(sg, sg);
+    if (use_sigma) den = __dsqrt_rn(den);
+    iv = __drcp_rn(den);
+}
+// Scalar calibration: the per-frame LUT over raw values (radiance_lut_kernel).
+__device__ __forceinline__ bool radiance_exact(const DevSensor &S, int x, int y, int use_sigma,
+                                               double &f, double &iv) {
+    if (x < 0 || y < 0 || x >= S.width || y >= S.height) return false;
+    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+    if (raw >= S.sat) return false;
+    const size_t i = (size_t)y * S.width + x;
+    if (S.defective && __ldg(S.defective + i)) return false;
+    if (!S.planes) {
+        const double2 e = __ldg(S.lut + raw);
+        f = e.x;
+        iv = e.y;
+        return true;
+    }
+    const double b = S.bias_p ? __ldg(S.bias_p + i) : S.bias;
+    const double a = S.nonuni_p ? __ldg(S.nonuni_p + i) : S.nonuni;
+    const double vr = S.readvar_p ? __ldg(S.readvar_p + i) : S.readvar;
+    radiometry_exact(S, raw, b, a, vr, use_sigma, f, iv);
+    return true;
+}
+
 // Sensor-space bounding box of the support disk |X - q| <= r.  In real
 // arithmetic the ellipse T^{-1}(disk) lies in [c - h, c + h]; the rounding of
 // c and h (~1e-13 px) can only add candidates, which the exact float64
@@ -186,12 +236,14 @@ struct Acc {
     double A[NA];   // upper triangle, row-major packed
     double b[P];
     int count;
+    float sabs;     // fast paths: sum w |y| (fp32), for the precision bound (fit_precise)
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int i = 0; i < NA; ++i) A[i] = 0.0;
 #pragma unroll
         for (int i = 0; i < P; ++i) b[i] = 0.0;
         count = 0;
+        sabs = 0.f;
     }
     // A += w phi phi^T, b += w phi y with phi = [1, dx, dy, dx^2, dx dy, dy^2][:P]
     __device__ __forceinline__ void add(double wd, double yd, double dx, double dy, double dxx,
@@ -337,6 +389,28 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
         return FIT_AMBIG;
     }
+}
+
+// Precision escalation of the fast path.  Its weights and values carry fp32
+// rounding (relative <= FAST_EPS per sample); the resulting error of
+// c0 = g . sum w phi y is bounded by FAST_EPS * max|g . phi| * sum w |y|
+// with max|g . phi| <= |g0| + r (|g1| + |g2|) + r^2 (|g3| + |g4| + |g5|).
+// A fit whose bound exceeds FAST_TOL relative to max(|c0|, floor) -- dark
+// pixels next to much brighter samples, where order-2 kernels' negative
+// lobes amplify the rounding -- is re-done by the exact path.
+constexpr double FAST_EPS = 4e-7;
+constexpr double FAST_TOL = 2e-5;
+template <int P>
+__device__ __forceinline__ bool fit_precise(const Fit &fit, float sabs, double r, double floor) {
+    double G = fabs(fit.g[0]);
+    if (P >= 3) G += r * (fabs(fit.g[1]) + fabs(fit.g[2]));
+    if (P >= 6) G += r * r * (fabs(fit.g[3]) + fabs(fit.g[4]) + fabs(fit.g[5]));
+    return FAST_EPS * G * (double)sabs <= FAST_TOL * fmax(fabs(fit.c0), floor);
+}
+// Sharp form: with T = sum w |g.phi| |y|, first-order perturbation of the
+// weights (by the residuals y - phi.c) and values gives |dc0| <~ 2 FAST_EPS T.
+__device__ __forceinline__ bool fit_precise_sharp(double c0, float T, double floor) {
+    return 2.0 * FAST_EPS * (double)T <= FAST_TOL * fmax(fabs(c0), floor);
 }
 
 // ---------------------------------------------------------------------------
