@@ -550,7 +550,7 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     constexpr int PN = NC<ORDER>::P;
     Acc<PN> acc;
     Fit fit;
-    double L = 0.0, U = 0.0;
+    double L = 0.0, U = 0.0, eL = 0.0, eU = 0.0;  // running bounds and their error bounds
     bool precise = true;
     for (int k = 0; k < P.n_scales; ++k) {
         accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
@@ -563,12 +563,20 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         float tk = 0.f;
         const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk));
         const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
+        // fast path: error bound of lo/hi (fp32 rounding of c0: fit_precise_sharp;
+        // of sd: ICI_SD_EPS relative) -- an intersection test closer than the
+        // bounds is decided by the exact path, so scale indices stay exact
+        const double ek = EXACT ? 0.0 : 2.0 * FAST_EPS * (double)tk + P.gamma * sd * ICI_SD_EPS;
         if (k == 0) {
             L = lo;
             U = hi;
+            eL = eU = ek;
         } else {
+            if (lo >= L) eL = lo > L ? ek : fmax(eL, ek);
+            if (hi <= U) eU = hi < U ? ek : fmax(eU, ek);
             L = fmax(L, lo);
             U = fmin(U, hi);
+            if (!EXACT && fabs(L - U) <= eL + eU) return FIT_AMBIG;
             if (L > U) break;
         }
         R.val = fit.c0;

@@ -400,6 +400,9 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
 // lobes amplify the rounding -- is re-done by the exact path.
 constexpr double FAST_EPS = 4e-7;
 constexpr double FAST_TOL = 2e-5;
+// relative error allowance of the fast path's ICI standard deviations (fp32
+// weights through g = A^-1 e1; ~25x FAST_EPS)
+constexpr double ICI_SD_EPS = 1e-5;
 template <int P>
 __device__ __forceinline__ bool fit_precise(const Fit &fit, float sabs, double r, double floor) {
     double G = fabs(fit.g[0]);

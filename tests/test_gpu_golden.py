@@ -24,11 +24,11 @@ def test_gpu_matches_reference_golden(cuda, name):
     s = compare.summary(rgb, ref["rgb"])
     print(name, s)
     assert s["nan_map_equal"]
-    assert s["frac_over"] <= 1e-3 and s["max"] <= (1e-2 if params.order == 2 else 1e-3)
+    assert s["frac_over"] == 0 and s["max"] <= 1e-4
     assert int((out["outcome"].cpu().numpy() != ref["outcome"]).sum()) == 0
     if "rgb" in arrays:  # the reference's own float32 output
         s2 = compare.summary(rgb, arrays["rgb"])
-        assert s2["nan_map_equal"] and s2["frac_over"] <= 1e-3
+        assert s2["nan_map_equal"] and s2["frac_over"] == 0 and s2["max"] <= 1e-4
     g = out["grad"].cpu().numpy()
     sg = compare.summary(g[:, 0], ref["gx"], floor=1e3)
     assert sg["nan_map_equal"] and sg["p99"] < 1e-3
