@@ -586,10 +586,30 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         R.count = acc.count;
         if constexpr (!EXACT) precise = fit_precise_sharp(fit.c0, tk, P.prec_floor);
     }
-    if (!precise) return FIT_AMBIG;  // selected estimate too close to fp32 rounding limits
+    if (!precise) return FIT_PREC;  // selected estimate too close to fp32 rounding limits
     if (ORDER == 0) R.gx = R.gy = qnan();
     R.outcome = ORDER * 16;
     return FIT_OK;
+}
+
+// Float64 recomputation of a fit whose fast-path decisions (validity, ICI
+// scale) were sound but whose value failed fit_precise: exact weights and
+// values at scale k.  False if the exact solve disagrees (then the caller
+// runs the full exact evaluation).
+template <int ORDER, class Sweep>
+__device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep, PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    Acc<PN> acc;
+    accumulate<ORDER, true>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+    Fit fit;
+    if (solve_fast<PN>(acc, P.cond, fit) != FIT_OK) return false;
+    R.val = fit.c0;
+    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+    R.gy = ORDER >= 1 ? fit.c2 : qnan();
+    R.sidx = k;
+    R.outcome = ORDER * 16;
+    R.count = acc.count;
+    return true;
 }
 
 // One warp per work item: the lanes share every window's candidates.
@@ -600,11 +620,14 @@ __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ D
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = warp; i < n; i += nwarps) {
         const uint32_t item = P.work_items[i];
-        const int pix = (int)(item >> 2), c = (int)(item & 3);
+        const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
+        const int kk = (int)((item >> 2) & 15);
         const int ox = pix % P.out_w, oy = pix / P.out_w;
         const GlobalSweep<32> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         PixelResult R;
-        if (P.n_scales > 1) {
+        if (kk && precise_fit<ORDER>(P, c, kk - 1, sweep, R)) {
+            // the fast path's decisions stand; only the value was recomputed
+        } else if (P.n_scales > 1) {
             if (ici<ORDER, true>(P, c, sweep, R) != FIT_OK) ladder<ORDER>(P, c, sweep, R);
         } else {
             ladder<ORDER>(P, c, sweep, R);
@@ -864,7 +887,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                     if constexpr (!PAT && ORDER >= 1)
                         fit_variance<ORDER, false>(P, c, 0, sweep, fit.g, &tk);
                     if (PAT || ORDER == 0 || !fit_precise_sharp(fit.c0, tk, P.prec_floor))
-                        st = FIT_AMBIG;
+                        st = FIT_PREC;
                 }
                 if (st == FIT_OK) {
                     R.count = acc.count;
@@ -878,8 +901,12 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         if (st == FIT_OK) {
             write_result(P, pix, c, R);
         } else {
+            // work item: band-relative pixel | kk | channel, kk = 0: full exact
+            // evaluation, kk = k + 1: float64 recomputation of the fit at scale k
+            const uint32_t kk = st == FIT_PREC ? (uint32_t)R.sidx + 1u : 0u;
             const uint32_t slot = atomicAdd(P.work_count, 1u);
-            P.work_items[slot] = ((uint32_t)pix << 2) | (uint32_t)c;
+            P.work_items[slot] =
+                ((uint32_t)(pix - P.row_begin * P.out_w) << 6) | (kk << 2) | (uint32_t)c;
         }
     }
 }
@@ -1645,6 +1672,12 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     if (!(params->max_radius > 0) || !(params->cond_threshold > 0)) return HDR_ERR_ARG;
     if (row_end <= 0 || row_end > out_h) row_end = out_h;
     if (row_begin < 0 || row_begin >= row_end) return HDR_ERR_ARG;
+    if ((size_t)(row_end - row_begin) * out_w >= (1ull << 26)) {  // work-item packing
+        snprintf(g_last_error, sizeof(g_last_error),
+                 "row band of %zu pixels: split calls into bands of < 2^26 output pixels",
+                 (size_t)(row_end - row_begin) * out_w);
+        return HDR_ERR_ARG;
+    }
     if ((uintptr_t)workspace & 255) return HDR_ERR_ARG;
 
     memset(&P, 0, sizeof(P));

@@ -27,6 +27,7 @@ constexpr int MAXJ = HDR_LPA_MAX_SCALES;
 constexpr int FIT_OK = 0;
 constexpr int FIT_FAIL = 1;   // TOO_FEW / ILL_CONDITIONED (decided)
 constexpr int FIT_AMBIG = 2;  // condition number too close to the threshold to decide from bounds
+constexpr int FIT_PREC = 3;   // decisions sound, value needs the float64 recomputation (fit_precise)
 
 struct DevSensor {
     const uint16_t *raw;
