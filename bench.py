@@ -5,7 +5,9 @@ Metric: HDR frames/s (and output Mpixel/s) reconstructing synthetic 3-sensor
   cfg2 (default, configs[1]): aligned rig, order-1 LPA, fixed window
   cfg3 (configs[2]): sub-pixel misaligned rig, order-2 LPA, ICI (J=4)
   cfg4 (configs[3]): cfg3 reconstructed to the 2x upsampled 4800x3400 grid
-A step = one reconstruction of one frame (all three sensors -> RGB).
+  cfg5 (configs[4]): 4-sensor video, misaligned, order-2 ICI (--steps 300 = the
+                     300-frame clip; frame-parallel across ranks under torchrun)
+A step = one reconstruction of one frame (all sensors -> RGB).
 
 Our arm:  python bench.py [--gpus N --steps K --warmup W --workload cfg2]
 Reference arm:  python bench.py --impl reference ...  (the CPU restatement of
@@ -44,11 +46,15 @@ WORKLOADS = {
                  desc="3-sensor 4-Mpixel, sub-pixel affine misalignment, order-2 LPA, ICI J=4"),
     "cfg4": dict(rig="misaligned", order=2, J=4, out=(2 * W_IN, 2 * H_IN), size=(W_IN, H_IN),
                  desc="3-sensor 4-Mpixel to 2x upsampled 4800x3400 grid, order-2 LPA, ICI J=4"),
+    "cfg5": dict(rig="misaligned", order=2, J=4, out=(W_IN, H_IN), size=(W_IN, H_IN), sensors=4,
+                 desc="4-sensor 4-Mpixel HDR video (exposures 1, 2^-4, 2^-8, 2^-12), misaligned, "
+                      "adaptive order-2 LPA, ICI J=4; one step = one video frame"),
 }
 
 # algorithmic FLOP per inside-window sample per scale:
 # FP32 8 (offsets, window, weight) + FP64 3+(p-1)+p(p+1)+2p (basis + moments)
 FLOP64_PER_SAMPLE = {0: 0, 1: 20, 2: 62}
+NC = {0: 1, 1: 3, 2: 6}  # polynomial coefficients p
 FLOP32_PER_SAMPLE = {0: 12, 1: 8, 2: 8}
 
 
@@ -127,7 +133,7 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml"}
 
 
-REF_BAND_ROWS = {"cfg1": None, "cfg2": 200, "cfg3": 24, "cfg4": 24}
+REF_BAND_ROWS = {"cfg1": None, "cfg2": 200, "cfg3": 24, "cfg4": 24, "cfg5": 16}
 _SIM_CACHE = {}
 
 
@@ -141,10 +147,10 @@ def cpu_reference_frame_seconds(wl, threads, band_rows=None, seed=123):
     from paper_1308_4908_b200 import simulate as sim
 
     W, H = wl["size"]
-    key = (wl["rig"], W, H, seed)
+    key = (wl["rig"], W, H, seed, wl.get("sensors", 3))
     if key not in _SIM_CACHE:
         gt = sim.hdr_chart(W, H)
-        rig = sim.baseline_rig(wl["rig"], W, H, seed=seed)
+        rig = sim.baseline_rig(wl["rig"], W, H, seed=seed, n_sensors=wl.get("sensors", 3))
         _SIM_CACHE[key] = (rig, sim.simulate_rig(gt, rig))
     rig, frames = _SIM_CACHE[key]
     cals = rig.calibrations()
@@ -218,7 +224,7 @@ def run_ours(args, wl, world, rank, local):
     out_w, out_h = wl["out"]
     params = _params(wl)
     gt = sim.hdr_chart(W, H)
-    rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0)
+    rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0, n_sensors=wl.get("sensors", 3))
     cals = rigspec.calibrations()
     frame_sets = [sim.simulate_rig_torch(gt, rigspec, dev, seed=1000 * rank + i)
                   for i in range(N_DISTINCT)]
@@ -268,11 +274,15 @@ def run_ours(args, wl, world, rank, local):
     slow_items = rig.slow_items((out_w, out_h))
 
     # algorithmic work of one launch: inside-window samples of the accepted fits
-    cnt = rig.reconstruct((out_w, out_h), params, ref_size=(W, H), want_count=True,
-                          want_scale_idx=True)
-    n_inside = float(cnt["count"].to(torch.int64).sum().item())
+    # (the kernel's own work plane: inside-window samples over every moment
+    # sweep it evaluated -- all ICI scales; the variance sweeps of ICI add
+    # 2p+3 FP64 FLOP per inside sample per scale)
+    cnt = rig.reconstruct((out_w, out_h), params, ref_size=(W, H), want_work=True,
+                          flags=N.HDR_FLAG_FAST_ONLY)
+    n_inside = float(cnt["work"].to(torch.int64).sum().item())
     p = wl["order"]
-    flop64 = n_inside * FLOP64_PER_SAMPLE[p]
+    per64 = FLOP64_PER_SAMPLE[p] + (2 * NC[p] + 3 if wl["J"] > 1 else 0)
+    flop64 = n_inside * per64
     flop32 = n_inside * FLOP32_PER_SAMPLE[p]
     peak64 = ctypes_probe(N, stream)
     if p == 0:

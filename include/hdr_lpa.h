@@ -42,7 +42,7 @@ extern "C" {
 
 #define HDR_LPA_MAX_SENSORS 8
 #define HDR_LPA_MAX_SCALES 8
-#define HDR_LPA_ABI_VERSION 2
+#define HDR_LPA_ABI_VERSION 3
 
 /* status codes */
 #define HDR_OK 0
@@ -117,6 +117,9 @@ typedef struct HdrOutputs {
     float *value;               /* nullable: [3][out_h][out_w] unclamped fitted constant term */
     uint16_t *count;            /* nullable: [3][out_h][out_w] samples inside the accepted window
                                    (selected ICI scale; 0 where NaN) */
+    uint32_t *work;             /* nullable: [3][out_h][out_w] inside-window samples summed over
+                                   every moment sweep evaluated (all ICI scales / ladder steps):
+                                   the algorithmic work behind the pixel (ABI v3) */
 } HdrOutputs;
 
 /* Bytes of device workspace hdr_lpa_reconstruct needs for these sensors and

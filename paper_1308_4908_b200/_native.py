@@ -89,6 +89,7 @@ class HdrOutputs(ctypes.Structure):
         ("outcome", ctypes.c_void_p),
         ("value", ctypes.c_void_p),
         ("count", ctypes.c_void_p),
+        ("work", ctypes.c_void_p),
     ]
 
 
@@ -174,7 +175,7 @@ def lib():
             for name in EXPORTED:
                 if name not in ("hdr_lpa_status_string", "hdr_lpa_last_error"):
                     getattr(L, name).restype = ctypes.c_int
-            if L.hdr_lpa_abi_version() != 2:
+            if L.hdr_lpa_abi_version() != 3:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L
         return _lib

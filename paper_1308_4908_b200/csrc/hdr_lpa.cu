@@ -477,7 +477,8 @@ struct PixelResult {
     double val, gx, gy;
     int outcome;  // order*16 + radius step, or HDR_OUTCOME_NAN
     int sidx;
-    int count;    // samples in the accepted window
+    int count;     // samples in the accepted window
+    int work = 0;  // inside-window samples over every moment sweep evaluated
 };
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
@@ -497,6 +498,7 @@ __device__ __forceinline__ void write_result(const DevParams &P, int pix, int c,
     if (P.outcome) P.outcome[(size_t)c * plane + pix] = (uint8_t)R.outcome;
     if (P.value) P.value[(size_t)c * plane + pix] = (float)v;
     if (P.count) P.count[(size_t)c * plane + pix] = (uint16_t)min(R.count, 65535);
+    if (P.work) P.work[(size_t)c * plane + pix] = (uint32_t)R.work;
 }
 
 // ---------------------------------------------------------------------------
@@ -511,6 +513,7 @@ __device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, Pixe
     Acc<PN> acc;
     for (;;) {
         accumulate<ORDER, true>(P, c, 0, r, __dmul_rn(r, r), sweep, acc);
+        R.work += acc.count;
         Fit fit;
         if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
             R.count = acc.count;
@@ -554,6 +557,7 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     bool precise = true;
     for (int k = 0; k < P.n_scales; ++k) {
         accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+        R.work += acc.count;
         const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
         if (st == FIT_AMBIG) return FIT_AMBIG;
         if (st != FIT_OK) {
@@ -601,6 +605,7 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
     constexpr int PN = NC<ORDER>::P;
     Acc<PN> acc;
     accumulate<ORDER, true>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+    R.work += acc.count;
     Fit fit;
     if (solve_fast<PN>(acc, P.cond, fit) != FIT_OK) return false;
     R.val = fit.c0;
@@ -878,6 +883,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                     accumulate_taps<ORDER>(P, sm, taps, org, c, px, py, acc);
                 else
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
+                R.work = acc.count;
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
                 if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor)) {
@@ -1108,6 +1114,7 @@ __device__ bool steered_order(const DevParams &P, int c, const Sweep &sweep, con
         int step = 0;
         for (;;) {
             accumulate_hinv<ORDER>(sweep, c, h11, h12, h22, r, __dmul_rn(r, r), acc);
+            R.work += acc.count;
             Fit fit;
             if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
                 R.count = acc.count;
@@ -1724,6 +1731,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.outcome = out->outcome;
     P.value = out->value;
     P.count = out->count;
+    P.work = out->work;
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
     char *wsp = (char *)workspace + WS_HEADER;

@@ -102,6 +102,7 @@ struct DevParams {
     uint8_t *outcome;
     float *value;
     uint16_t *count;
+    uint32_t *work;
     int flags, pad1;
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, pad2;

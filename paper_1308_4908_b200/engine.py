@@ -189,7 +189,8 @@ class DeviceRig:
         return self._workspaces[key]
 
     def allocate_outputs(self, out_size, want_grad=False, want_scale_idx=False,
-                         want_outcome=False, raw_value=False, want_count=False):
+                         want_outcome=False, raw_value=False, want_count=False,
+                         want_work=False):
         out_w, out_h = out_size
         dev = self.device
         out = {"rgb": torch.empty((out_h, out_w, 3), dtype=torch.float32, device=dev)}
@@ -203,15 +204,18 @@ class DeviceRig:
             out["value"] = torch.empty((3, out_h, out_w), dtype=torch.float32, device=dev)
         if want_count:
             out["count"] = torch.empty((3, out_h, out_w), dtype=torch.int16, device=dev)
+        if want_work:
+            out["work"] = torch.zeros((3, out_h, out_w), dtype=torch.int32, device=dev)
         return out
 
     def reconstruct(self, out_size, params: ReconstructionParams, ref_size=None, rows=None,
                     want_grad=False, want_scale_idx=False, want_outcome=False, raw_value=False,
-                    want_count=False, out=None, stream=None, flags=0):
+                    want_count=False, want_work=False, out=None, stream=None, flags=0):
         """Launch the reconstruction on the current (or given) stream.
 
         Returns the dict of output tensors (``rgb`` (H, W, 3) float32 and the
-        optional ``grad``/``scale_idx``/``outcome``/``value`` planes).  With
+        optional ``grad``/``scale_idx``/``outcome``/``value``/``count``/``work``
+        planes; ``work`` = inside-window samples over every moment sweep).  With
         ``rows=(r0, r1)`` only that output row band is computed.
         """
         out_w, out_h = int(out_size[0]), int(out_size[1])
@@ -219,7 +223,7 @@ class DeviceRig:
             ref_size = (out_w, out_h)  # lpa.py:393 (ref_size or out_size)
         if out is None:
             out = self.allocate_outputs((out_w, out_h), want_grad, want_scale_idx,
-                                        want_outcome, raw_value, want_count)
+                                        want_outcome, raw_value, want_count, want_work)
         o = N.HdrOutputs()
         o.rgb = out["rgb"].data_ptr()
         o.grad = out["grad"].data_ptr() if "grad" in out else None
@@ -227,6 +231,7 @@ class DeviceRig:
         o.outcome = out["outcome"].data_ptr() if "outcome" in out else None
         o.value = out["value"].data_ptr() if "value" in out else None
         o.count = out["count"].data_ptr() if "count" in out else None
+        o.work = out["work"].data_ptr() if "work" in out else None
         ws = self.workspace(out_w, out_h)
         r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
