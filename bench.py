@@ -261,7 +261,9 @@ def run_ours(args, wl, world, rank, local):
     for i in range(args.warmup):
         step(i)
     with ClockSampler(local) as clocks:
+        n_launch0 = N.lib().hdr_lpa_launch_count()
         ms = timed(step, args.steps)
+        n_launches = int(N.lib().hdr_lpa_launch_count() - n_launch0)
     clk = clocks.summary()
     ms_step = ms / args.steps
     fps = world * args.steps / (ms / 1e3)
@@ -368,7 +370,7 @@ def run_ours(args, wl, world, rank, local):
             "cpu_baseline": cpu,
             "e2e": {"value": fps_e2e, "unit": "frames/s", "h2d_bytes_per_step": pipe.h2d_bytes,
                     "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": ms_e2e / args.steps},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": n_launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -229,6 +229,11 @@ const char *hdr_lpa_status_string(int status);
 const char *hdr_lpa_last_error(void);
 int hdr_lpa_abi_version(void);
 
+/* Number of kernel launches this library has issued since it was loaded
+ * (all entry points, all threads): lets a caller count the device work behind
+ * a timed region (bench.py's gpu_launches). */
+unsigned long long hdr_lpa_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

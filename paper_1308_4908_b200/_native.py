@@ -43,6 +43,7 @@ EXPORTED = (
     "hdr_lpa_status_string",
     "hdr_lpa_last_error",
     "hdr_lpa_abi_version",
+    "hdr_lpa_launch_count",
 )
 
 
@@ -173,8 +174,11 @@ def lib():
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]
             L.hdr_lpa_last_error.restype = ctypes.c_char_p
             for name in EXPORTED:
-                if name not in ("hdr_lpa_status_string", "hdr_lpa_last_error"):
+                if name not in ("hdr_lpa_status_string", "hdr_lpa_last_error",
+                                "hdr_lpa_launch_count"):
                     getattr(L, name).restype = ctypes.c_int
+            L.hdr_lpa_launch_count.restype = ctypes.c_ulonglong
+            L.hdr_lpa_launch_count.argtypes = []
             if L.hdr_lpa_abi_version() != 3:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <climits>
 #include <type_traits>
 #include <math.h>
@@ -54,30 +55,37 @@ struct NC {
 // ---------------------------------------------------------------------------
 
 // Slow path: straight from the raw frames in global memory, float64 radiometry.
-// LANES > 1: the candidates of every window are split over the lanes of a
-// warp (candidate j -> lane j % 32) and the sums are combined by a butterfly
-// reduction, after which every lane holds bitwise-identical totals.
+// LANES > 1: the candidates of every window are split over an aligned group
+// of LANES lanes of a warp (candidate j -> group lane j % LANES) and the sums
+// are combined by a butterfly reduction, after which every lane of the group
+// holds bitwise-identical totals.  Groups of one warp may diverge.
 template <int LANES>
 struct GlobalSweep {
     const DevParams &P;
     double qx, qy;
+    __device__ __forceinline__ static unsigned group_mask() {
+        if constexpr (LANES >= 32) return 0xffffffffu;
+        return ((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1));
+    }
     template <int PN>
     __device__ __forceinline__ void reduce(Acc<PN> &acc) const {
         if constexpr (LANES > 1) {
+            const unsigned mask = group_mask();
 #pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) {
+            for (int m = LANES / 2; m >= 1; m >>= 1) {
 #pragma unroll
-                for (int i = 0; i < Acc<PN>::NA; ++i) acc.A[i] += __shfl_xor_sync(0xffffffffu, acc.A[i], m);
+                for (int i = 0; i < Acc<PN>::NA; ++i) acc.A[i] += __shfl_xor_sync(mask, acc.A[i], m);
 #pragma unroll
-                for (int i = 0; i < PN; ++i) acc.b[i] += __shfl_xor_sync(0xffffffffu, acc.b[i], m);
-                acc.count += __shfl_xor_sync(0xffffffffu, acc.count, m);
+                for (int i = 0; i < PN; ++i) acc.b[i] += __shfl_xor_sync(mask, acc.b[i], m);
+                acc.count += __shfl_xor_sync(mask, acc.count, m);
             }
         }
     }
     __device__ __forceinline__ double reduce(double v) const {
         if constexpr (LANES > 1) {
+            const unsigned mask = group_mask();
 #pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+            for (int m = LANES / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(mask, v, m);
         }
         return v;
     }
@@ -97,7 +105,7 @@ struct GlobalSweep {
                 const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
                 const int nrow = yhi >= ys ? ((yhi - ys) >> 1) + 1 : 0;
                 const int ncol = xhi >= xs ? ((xhi - xs) >> 1) + 1 : 0;
-                const int lane = LANES > 1 ? (int)(threadIdx.x & 31) : 0;
+                const int lane = LANES > 1 ? (int)(threadIdx.x & (LANES - 1)) : 0;
                 for (int j = lane; j < nrow * ncol; j += LANES) {
                     const int y = ys + 2 * (j / ncol), x = xs + 2 * (j % ncol);
                     const double yd = (double)y;
@@ -617,18 +625,23 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
     return true;
 }
 
-// One warp per work item: the lanes share every window's candidates.
+// One group of SLOW_LANES lanes per work item: they share every window's
+// candidates.
+#ifndef SLOW_LANES
+#define SLOW_LANES 8
+#endif
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
+    constexpr int G = SLOW_LANES;  // lanes per work item
     const uint32_t n = *P.work_count;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t i = warp; i < n; i += nwarps) {
+    const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t ngrp = (gridDim.x * blockDim.x) / G;
+    for (uint32_t i = grp; i < n; i += ngrp) {
         const uint32_t item = P.work_items[i];
         const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
         const int kk = (int)((item >> 2) & 15);
         const int ox = pix % P.out_w, oy = pix / P.out_w;
-        const GlobalSweep<32> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         PixelResult R;
         if (kk && precise_fit<ORDER>(P, c, kk - 1, sweep, R)) {
             // the fast path's decisions stand; only the value was recomputed
@@ -637,7 +650,7 @@ __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ D
         } else {
             ladder<ORDER>(P, c, sweep, R);
         }
-        if ((threadIdx.x & 31) == 0) write_result(P, pix, c, R);
+        if ((threadIdx.x & (G - 1)) == 0) write_result(P, pix, c, R);
     }
 }
 
@@ -1004,14 +1017,47 @@ __global__ void radiance_lut_kernel(const __grid_constant__ DevParams P) {
 // Per-frame radiometric pre-pass: every raw pixel converted once into the
 // de-interleaved phase planes (radiometry.py:303-336 for the whole frame);
 // out-of-frame padding gets 1/den = 0 (no sample).  HBM-bound.
-__global__ void radiance_phase_kernel(const __grid_constant__ DevParams P) {
-    const int s = blockIdx.z >> 2, ph = blockIdx.z & 3;
-    const DevSensor &S = P.s[s];
-    const int j = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= S.pwg || j >= S.phg) return;
-    const int x = 2 * i + (ph & 1), y = 2 * j + (ph >> 1);
-    S.phase[((size_t)ph * S.phg + j) * S.pwg + i] = radiance_sample(S, x, y, P.use_sigma);
+// One thread per (sensor, phase row j, group of 4 phase columns): raw rows
+// 2j and 2j+1, columns 8g..8g+7 read as 16-B vectors (when the frame's pitch
+// and base allow), the four phase planes written as 2 x 16-B per plane.
+__global__ void __launch_bounds__(128) radiance_phase_kernel(const __grid_constant__ DevParams P) {
+    const DevSensor &S = P.s[blockIdx.z];
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= S.pwg || j >= S.phg) return;
+    const int x0 = 2 * i0;
+    const bool vec = S.vec_raw && x0 + 8 <= S.pitch;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int y = 2 * j + r;
+        uint16_t v[8];
+        if (y < S.height && vec) {
+            const uint4 q = __ldg((const uint4 *)(S.raw + (size_t)y * S.pitch + x0));
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[2 * k] = (uint16_t)(w[k] & 0xffffu);
+                v[2 * k + 1] = (uint16_t)(w[k] >> 16);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                v[k] = (y < S.height && x0 + k < S.width) ? __ldg(S.raw + (size_t)y * S.pitch + x0 + k)
+                                                          : (uint16_t)0;
+        }
+        float2 o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            o[k] = (y < S.height && x0 + k < S.width)
+                       ? radiance_from_raw(S, (int)v[k], x0 + k, y, P.use_sigma)
+                       : make_float2(0.f, 0.f);  // padding: no sample
+#pragma unroll
+        for (int px = 0; px < 2; ++px) {
+            float4 *dst = (float4 *)(S.phase + ((size_t)(2 * r + px) * S.phg + j) * S.pwg + i0);
+            dst[0] = make_float4(o[px].x, o[px].y, o[px + 2].x, o[px + 2].y);
+            dst[1] = make_float4(o[px + 4].x, o[px + 4].y, o[px + 6].x, o[px + 6].y);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1408,6 +1454,8 @@ static int fill_sensor(const HdrSensor &h, DevSensor &d) {
     d.width = h.width;
     d.height = h.height;
     d.pitch = h.pitch;
+    // 16-B vector loads of raw rows in the pre-pass
+    d.vec_raw = ((uintptr_t)h.raw % 16 == 0) && (h.pitch % 8 == 0);
     d.sat = h.saturation_level;
     for (int c = 0; c < 3; ++c) {
         d.phmask[c] = 0;
@@ -1455,6 +1503,9 @@ static int fill_sensor(const HdrSensor &h, DevSensor &d) {
 }
 
 static thread_local char g_last_error[256] = "";
+// kernel launches issued by this library since load (hdr_lpa_launch_count)
+static std::atomic<unsigned long long> g_launches{0};
+#define COUNT_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 
 static int cuda_fail(const char *where) {
     const cudaError_t e = cudaGetLastError();
@@ -1479,6 +1530,7 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
         per_sm < 1)
         return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
+    COUNT_LAUNCH();
     if constexpr (PAT)
         lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P, T);
     else
@@ -1534,6 +1586,7 @@ static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    COUNT_LAUNCH();
     lpa_slow_kernel<ORDER><<<nsm * 4, 128, 0, st>>>(P);
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_slow_kernel launch");
     return HDR_OK;
@@ -1625,6 +1678,8 @@ extern "C" {
 
 int hdr_lpa_abi_version(void) { return HDR_LPA_ABI_VERSION; }
 
+unsigned long long hdr_lpa_launch_count(void) { return g_launches.load(); }
+
 const char *hdr_lpa_last_error(void) { return g_last_error; }
 
 const char *hdr_lpa_status_string(int status) {
@@ -1643,9 +1698,10 @@ const char *hdr_lpa_status_string(int status) {
 // [exact radiometry LUT of every sensor][work items].  LUT: 65536 x
 // (f_hat, 1/den) float64 per sensor, indexed by the raw value (scalar
 // calibration only).  Phase planes: per sensor [4][phg][pwg] float2 with
-// pwg = ceil(w/2) rounded up to even (16-B rows), phg = ceil(h/2).
+// pwg = ceil(w/2) rounded up to a multiple of 4 (32-B rows: the pre-pass
+// writes 4 float2 per thread), phg = ceil(h/2).
 static size_t phase_bytes(const HdrSensor &s) {
-    const size_t pwg = (size_t)(((s.width + 1) / 2 + 1) & ~1), phg = (size_t)((s.height + 1) / 2);
+    const size_t pwg = (size_t)(((s.width + 1) / 2 + 3) & ~3), phg = (size_t)((s.height + 1) / 2);
     return 4 * pwg * phg * sizeof(float2);
 }
 
@@ -1738,7 +1794,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
         d.phase = (float2 *)wsp;
-        d.pwg = ((d.width + 1) / 2 + 1) & ~1;
+        d.pwg = ((d.width + 1) / 2 + 3) & ~3;
         d.phg = (d.height + 1) / 2;
         wsp += phase_bytes(sensors[s]);
     }
@@ -1756,6 +1812,7 @@ static int launch_prepass(const DevParams &P, cudaStream_t st) {
     for (int s = 0; s < P.n_sensors; ++s)
         if (!P.s[s].planes) maxsat = max(maxsat, P.s[s].sat);
     if (maxsat > 0) {
+        COUNT_LAUNCH();
         radiance_lut_kernel<<<dim3((maxsat + 255) / 256, P.n_sensors), 256, 0, st>>>(P);
         if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("radiance_lut_kernel launch");
     }
@@ -1764,8 +1821,9 @@ static int launch_prepass(const DevParams &P, cudaStream_t st) {
         maxpw = max(maxpw, P.s[s].pwg);
         maxph = max(maxph, P.s[s].phg);
     }
-    dim3 grid((maxpw + 127) / 128, maxph, 4 * P.n_sensors);
-    radiance_phase_kernel<<<grid, 128, 0, st>>>(P);
+    dim3 grid((maxpw / 4 + 31) / 32, (maxph + 3) / 4, P.n_sensors);
+    COUNT_LAUNCH();
+    radiance_phase_kernel<<<grid, dim3(32, 4), 0, st>>>(P);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("radiance_phase_kernel launch");
 }
 
@@ -1878,9 +1936,9 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = nsm * 8;
     switch (P.order) {
-        case 0: lpa_steered_kernel<0><<<grid, 128, 0, st>>>(P); break;
-        case 1: lpa_steered_kernel<1><<<grid, 128, 0, st>>>(P); break;
-        default: lpa_steered_kernel<2><<<grid, 128, 0, st>>>(P); break;
+        case 0: COUNT_LAUNCH(); lpa_steered_kernel<0><<<grid, 128, 0, st>>>(P); break;
+        case 1: COUNT_LAUNCH(); lpa_steered_kernel<1><<<grid, 128, 0, st>>>(P); break;
+        default: COUNT_LAUNCH(); lpa_steered_kernel<2><<<grid, 128, 0, st>>>(P); break;
     }
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_steered_kernel launch");
 }
@@ -1924,9 +1982,9 @@ int hdr_lpa_evaluate_samples(const HdrSampleIndex *index, const double *qx, cons
     const int grid = min((m + 127) / 128, 148 * 16);
     cudaStream_t st = (cudaStream_t)stream;
     switch (order) {
-        case 0: lpa_samples_kernel<0><<<grid, 128, 0, st>>>(ix, Q); break;
-        case 1: lpa_samples_kernel<1><<<grid, 128, 0, st>>>(ix, Q); break;
-        default: lpa_samples_kernel<2><<<grid, 128, 0, st>>>(ix, Q); break;
+        case 0: COUNT_LAUNCH(); lpa_samples_kernel<0><<<grid, 128, 0, st>>>(ix, Q); break;
+        case 1: COUNT_LAUNCH(); lpa_samples_kernel<1><<<grid, 128, 0, st>>>(ix, Q); break;
+        default: COUNT_LAUNCH(); lpa_samples_kernel<2><<<grid, 128, 0, st>>>(ix, Q); break;
     }
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_samples_kernel launch");
 }
@@ -1948,6 +2006,7 @@ int hdr_steering_field(const float *gx, const float *gy, int width, int height,
     K.sigma_max = sigma_max;
     K.inv_scale = 1.0 / gradient_scale;
     dim3 grid((width + 127) / 128, height);
+    COUNT_LAUNCH();
     steering_field_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(gx, gy, width, height, K, theta,
                                                                   sigma, gamma);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("steering_field_kernel launch");
@@ -1961,6 +2020,7 @@ int hdr_saturation_mask(const HdrSensor *sensor, uint32_t *out_bits, int words_p
     if (rc != HDR_OK) return rc;
     if (words_per_row < (d.width + 31) / 32) return HDR_ERR_SHAPE;
     dim3 grid((d.width + 255) / 256, d.height);
+    COUNT_LAUNCH();
     saturation_mask_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d, out_bits, words_per_row);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
 }
@@ -1973,6 +2033,7 @@ int hdr_radiance_planes(const HdrSensor *sensor, int weight_mode, float *value, 
     const int rc = fill_sensor(*sensor, d);
     if (rc != HDR_OK) return rc;
     dim3 grid((d.width + 255) / 256, d.height);
+    COUNT_LAUNCH();
     radiance_planes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
         d, weight_mode == HDR_WEIGHT_SIGMA, value, inv_den);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
@@ -1990,10 +2051,12 @@ int hdr_fp64_peak_probe(double *flops_per_s, void *stream) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    COUNT_LAUNCH();
     fp64_probe_kernel<<<blocks, 256, 0, st>>>(sink, iters / 8, 0.999999, 1e-7);  // warm-up
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(e0, st);
+        COUNT_LAUNCH();
         fp64_probe_kernel<<<blocks, 256, 0, st>>>(sink, iters, 0.999999, 1e-7);
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);

@@ -45,6 +45,7 @@ struct DevSensor {
     double inv_denom, inv_denom2, c_shot, qv;  // scalar-calibration constants
     float bias_f, readvar_f, inv_denom_f, inv_denom2_f, c_shot_f, qv_f;
     int planes;               // any calibration plane present
+    int vec_raw;              // raw base 16-B aligned and pitch % 8 == 0
     // fast-path staging geometry
     int rw, rh;               // staged region (even), phase planes are (rh/2) x (rw/2)
     int off_vi;               // byte offset (in a plane buffer) of the 4 staged phase planes
@@ -508,16 +509,23 @@ __device__ __forceinline__ int solve_exact(const Acc<P> &acc, double cond, Fit &
         fit.g[0] = 1.0 / acc.A[0];
         return FIT_OK;
     } else {
+        // Both of the reference's rejections (eigenvalue test, Cholesky pivot)
+        // give FIT_FAIL, so their order does not matter.  The float64
+        // condition bounds decide whenever they are 1e-5 clear of the
+        // threshold (their rounding error is <= cond * 1e-16, and so is the
+        // reference's eigenvalues'); only the rest pays for the eigenvalues.
+        double L[P * (P + 1) / 2], inv[P];
+        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;
+        double cu, cl;
+        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
+        if (cu <= cond * (1.0 - 1e-5)) return FIT_OK;
+        if (cl >= cond * (1.0 + 1e-5)) return FIT_FAIL;
         double lmin, lmax;
         if constexpr (P == 3)
             eig_range3(acc.A, lmin, lmax);
         else
             eig_range6(acc.A, lmin, lmax);
         if (lmin <= 0.0 || lmax > cond * lmin) return FIT_FAIL;
-        double L[P * (P + 1) / 2], inv[P];
-        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;
-        double cu, cl;
-        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
         return FIT_OK;
     }
 }

@@ -17,7 +17,8 @@ HEADER = ROOT / "include" / "hdr_lpa.h"
 
 def declared_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(hdr_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:unsigned\s+)?(?:long\s+)*\w+\s*\*?\s*(hdr_\w+)\s*\(",
+                                  text, re.M)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
