@@ -37,6 +37,12 @@ constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per ti
 
 // workspace layout: [header: work counter][pre-computed taps][work items]
 static const size_t WS_HEADER = 256;
+// Order-2 tile sweeps: skip samples outside the disk with branches (1) or
+// accumulate them with zero weight (0; the row-factored moments make a
+// sample cheap enough that divergent branches cost more than they save)
+#ifndef HDR_BRANCHY_O2
+#define HDR_BRANCHY_O2 1
+#endif
 static const size_t LUT_BYTES = 65536 * sizeof(double2);
 
 template <int ORDER>
@@ -74,7 +80,7 @@ struct GlobalSweep {
 #pragma unroll
             for (int m = LANES / 2; m >= 1; m >>= 1) {
 #pragma unroll
-                for (int i = 0; i < Acc<PN>::NA; ++i) acc.A[i] += __shfl_xor_sync(mask, acc.A[i], m);
+                for (int i = 0; i < Acc<PN>::NS; ++i) acc.A[i] += __shfl_xor_sync(mask, acc.A[i], m);
 #pragma unroll
                 for (int i = 0; i < PN; ++i) acc.b[i] += __shfl_xor_sync(mask, acc.b[i], m);
                 acc.count += __shfl_xor_sync(mask, acc.count, m);
@@ -192,7 +198,7 @@ struct TileSweep {
                             } else {
                                 // finite sentinel: never inside, and 0 * phi stays 0
                                 cdx[i] = 0.0;
-                                cdxx[i] = 1e300;
+                                cdxx[i] = 1e150;  // (1e150)^2 stays finite: 0 * dx^4 = 0
                             }
                         }
                         const int colbase = ph * plane + ((xs - ox) >> 1);
@@ -306,37 +312,60 @@ struct RowMoments {
         cnt = 0;
     }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double,
-                                           double, double, float d2f) {
+                                           double dxx, double, float d2f) {
         const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double w = (double)w32, y = ok ? v : 0.0;
         acc.sabs = fmaf(w32, fabsf((float)y), acc.sabs);
-        double p = w;
+        // w dx^n from independent products (dx^2 is the cached column square):
+        // dependency depth 2 instead of a 2*ORDER-long multiply chain
+        double p[5];
+        p[0] = w;
+        if (ORDER >= 1) {
+            p[1] = w * dx;
+            p[2] = w * dxx;
+        }
+        if (ORDER >= 2) {
+            p[3] = w * (dx * dxx);
+            p[4] = w * (dxx * dxx);
+        }
 #pragma unroll
         for (int n = 0; n <= 2 * ORDER; ++n) {
-            S[n] += p;
-            if (n <= ORDER) T[n] = fma(p, y, T[n]);
-            if (n < 2 * ORDER) p *= dx;
+            S[n] += p[n];
+            if (n <= ORDER) T[n] = fma(p[n], y, T[n]);
         }
         cnt += ok ? 1 : 0;
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) {
-        // basis exponents (i, j): order 1: (0,0) (1,0) (0,1); order 2 adds (2,0) (1,1) (0,2)
-        constexpr int I[6] = {0, 1, 0, 2, 1, 0}, J[6] = {0, 0, 1, 0, 1, 2};
         double dp[5];
         dp[0] = 1.0;
         dp[1] = dy;
         dp[2] = dyy;
         dp[3] = dyy * dy;
         dp[4] = dyy * dyy;
-        int k = 0;
 #pragma unroll
         for (int a = 0; a < PN; ++a) {
-            acc.b[a] = (J[a] == 0) ? acc.b[a] + T[I[a]] : fma(T[I[a]], dp[J[a]], acc.b[a]);
+            const int ia = basis_i(a), ja = basis_j(a);
+            acc.b[a] = (ja == 0) ? acc.b[a] + T[ia] : fma(T[ia], dp[ja], acc.b[a]);
+        }
+        if constexpr (Acc<PN>::MOM) {
+            // moments M_ij += S_i dy^j, i + j <= 2 ORDER
 #pragma unroll
-            for (int bb = a; bb < PN; ++bb) {
-                const int jj = J[a] + J[bb];
-                acc.A[k] = jj == 0 ? acc.A[k] + S[I[a] + I[bb]] : fma(S[I[a] + I[bb]], dp[jj], acc.A[k]);
-                ++k;
+            for (int d = 0; d <= 2 * ORDER; ++d)
+#pragma unroll
+                for (int j = 0; j <= d; ++j) {
+                    const int k = midx(d - j, j);
+                    acc.A[k] = j == 0 ? acc.A[k] + S[d - j] : fma(S[d - j], dp[j], acc.A[k]);
+                }
+        } else {
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < PN; ++a) {
+#pragma unroll
+                for (int bb = a; bb < PN; ++bb) {
+                    const int ii = basis_i(a) + basis_i(bb), jj = basis_j(a) + basis_j(bb);
+                    acc.A[k] = jj == 0 ? acc.A[k] + S[ii] : fma(S[ii], dp[jj], acc.A[k]);
+                    ++k;
+                }
             }
         }
         acc.count += cnt;
@@ -881,7 +910,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
                    yhi < org[s][1] + S.rh;
     }
-    const TileSweep<MAXC, (ORDER >= 2)> sweep{P, sm, org, qx, qy};
+    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2)> sweep{P, sm, org, qx, qy};
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;

@@ -234,15 +234,32 @@ __device__ __forceinline__ void window_bbox(const DevSensor &S, double qx, doubl
 // Moment accumulators (_kernels.py:155-182).  P = number of coefficients.
 // ---------------------------------------------------------------------------
 template <int P>
+__device__ __forceinline__ constexpr int uidx(int a, int c) {  // packed upper index, a <= c
+    return a * P - a * (a - 1) / 2 + (c - a);
+}
+
+// Basis exponents: phi_a = dx^I[a] dy^J[a] (lpa.py:104-118 order)
+__device__ __forceinline__ constexpr int basis_i(int a) { return a == 1 ? 1 : a == 3 ? 2 : a == 4 ? 1 : 0; }
+__device__ __forceinline__ constexpr int basis_j(int a) { return a == 2 ? 1 : a == 4 ? 1 : a == 5 ? 2 : 0; }
+// Index of the monomial dx^i dy^j (degree-major, then by j)
+__device__ __forceinline__ constexpr int midx(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
+
+// A (P(P+1)/2 packed upper entries) and b.  For P = 6 the normal matrix is
+// stored as its 15 distinct moments M_ij = sum w dx^i dy^j (i + j <= 4; A is a
+// Hankel-like arrangement of them): 15 accumulators instead of 21, and the
+// row-factored sweeps add S_i dy^j into them directly.  fill_A expands.
+template <int P>
 struct Acc {
     static constexpr int NA = P * (P + 1) / 2;
-    double A[NA];   // upper triangle, row-major packed
+    static constexpr bool MOM = (P == 6);
+    static constexpr int NS = MOM ? 15 : NA;  // stored entries
+    double A[NS];   // P <= 3: upper triangle, row-major packed; P = 6: moments M[midx(i, j)]
     double b[P];
     int count;
     float sabs;     // fast paths: sum w |y| (fp32), for the precision bound (fit_precise)
     __device__ __forceinline__ void zero() {
 #pragma unroll
-        for (int i = 0; i < NA; ++i) A[i] = 0.0;
+        for (int i = 0; i < NS; ++i) A[i] = 0.0;
 #pragma unroll
         for (int i = 0; i < P; ++i) b[i] = 0.0;
         count = 0;
@@ -251,36 +268,65 @@ struct Acc {
     // A += w phi phi^T, b += w phi y with phi = [1, dx, dy, dx^2, dx dy, dy^2][:P]
     __device__ __forceinline__ void add(double wd, double yd, double dx, double dy, double dxx,
                                         double dyy, int inc = 1) {
-        double phi[6];
-        phi[0] = 1.0;
-        if (P >= 3) {
-            phi[1] = dx;
-            phi[2] = dy;
-        }
-        if (P >= 6) {
-            phi[3] = dxx;
-            phi[4] = __dmul_rn(dx, dy);
-            phi[5] = dyy;
-        }
-        int k = 0;
+        if constexpr (MOM) {
+            double m[15];
+            m[1] = dx;
+            m[2] = dy;
+            m[3] = dxx;
+            m[4] = __dmul_rn(dx, dy);
+            m[5] = dyy;
+            m[6] = dxx * dx;
+            m[7] = dxx * dy;
+            m[8] = dx * dyy;
+            m[9] = dyy * dy;
+            m[10] = dxx * dxx;
+            m[11] = dxx * m[4];
+            m[12] = dxx * dyy;
+            m[13] = m[4] * dyy;
+            m[14] = dyy * dyy;
+            A[0] += wd;
 #pragma unroll
-        for (int a = 0; a < P; ++a) {
-            const double wa = (a == 0) ? wd : wd * phi[a];
-            b[a] = fma(wa, yd, b[a]);
+            for (int k = 1; k < 15; ++k) A[k] = fma(wd, m[k], A[k]);
+            const double wy = wd * yd;
+            b[0] += wy;
 #pragma unroll
-            for (int c = a; c < P; ++c) {
-                A[k] = (c == 0) ? A[k] + wa : fma(wa, phi[c], A[k]);
-                ++k;
+            for (int a = 1; a < 6; ++a) b[a] = fma(wy, m[midx(basis_i(a), basis_j(a))], b[a]);
+        } else {
+            double phi[3];
+            phi[0] = 1.0;
+            if (P >= 3) {
+                phi[1] = dx;
+                phi[2] = dy;
+            }
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                const double wa = (a == 0) ? wd : wd * phi[a];
+                b[a] = fma(wa, yd, b[a]);
+#pragma unroll
+                for (int c = a; c < P; ++c) {
+                    A[k] = (c == 0) ? A[k] + wa : fma(wa, phi[c], A[k]);
+                    ++k;
+                }
             }
         }
         count += inc;
     }
+    // packed upper triangle of A
+    __device__ __forceinline__ void fill_A(double *out) const {
+        if constexpr (MOM) {
+#pragma unroll
+            for (int a = 0; a < P; ++a)
+#pragma unroll
+                for (int c = a; c < P; ++c)
+                    out[uidx<P>(a, c)] = A[midx(basis_i(a) + basis_i(c), basis_j(a) + basis_j(c))];
+        } else {
+#pragma unroll
+            for (int i = 0; i < NA; ++i) out[i] = A[i];
+        }
+    }
 };
 
-template <int P>
-__device__ __forceinline__ constexpr int uidx(int a, int c) {  // packed upper index, a <= c
-    return a * P - a * (a - 1) / 2 + (c - a);
-}
 
 // Result of a solved window: coefficients and g = A^{-1} e1 (for the ICI variance)
 struct Fit {
@@ -383,10 +429,11 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         fit.g[0] = 1.0 / acc.A[0];
         return FIT_OK;
     } else {
-        double L[P * (P + 1) / 2], inv[P];
-        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;  // pivot <= 0: far beyond 1e8
+        double A[P * (P + 1) / 2], L[P * (P + 1) / 2], inv[P];
+        acc.fill_A(A);
+        if (!cholesky<P>(A, L, inv)) return FIT_FAIL;  // pivot <= 0: far beyond 1e8
         double cu, cl;
-        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
+        chol_finish<P>(A, acc.b, L, inv, fit, cu, cl);
         const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
         if (cu <= cond * (1.0 - margin)) return FIT_OK;
         if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
@@ -514,17 +561,18 @@ __device__ __forceinline__ int solve_exact(const Acc<P> &acc, double cond, Fit &
         // condition bounds decide whenever they are 1e-5 clear of the
         // threshold (their rounding error is <= cond * 1e-16, and so is the
         // reference's eigenvalues'); only the rest pays for the eigenvalues.
-        double L[P * (P + 1) / 2], inv[P];
-        if (!cholesky<P>(acc.A, L, inv)) return FIT_FAIL;
+        double A[P * (P + 1) / 2], L[P * (P + 1) / 2], inv[P];
+        acc.fill_A(A);
+        if (!cholesky<P>(A, L, inv)) return FIT_FAIL;
         double cu, cl;
-        chol_finish<P>(acc.A, acc.b, L, inv, fit, cu, cl);
+        chol_finish<P>(A, acc.b, L, inv, fit, cu, cl);
         if (cu <= cond * (1.0 - 1e-5)) return FIT_OK;
         if (cl >= cond * (1.0 + 1e-5)) return FIT_FAIL;
         double lmin, lmax;
         if constexpr (P == 3)
-            eig_range3(acc.A, lmin, lmax);
+            eig_range3(A, lmin, lmax);
         else
-            eig_range6(acc.A, lmin, lmax);
+            eig_range6(A, lmin, lmax);
         if (lmin <= 0.0 || lmax > cond * lmin) return FIT_FAIL;
         return FIT_OK;
     }
