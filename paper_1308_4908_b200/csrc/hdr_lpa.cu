@@ -70,8 +70,10 @@ struct GlobalSweep {
     const DevParams &P;
     double qx, qy;
     __device__ __forceinline__ static unsigned group_mask() {
-        if constexpr (LANES >= 32) return 0xffffffffu;
-        return ((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1));
+        if constexpr (LANES >= 32)
+            return 0xffffffffu;
+        else
+            return ((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1));
     }
     template <int PN>
     __device__ __forceinline__ void reduce(Acc<PN> &acc) const {

@@ -1,3 +1,7 @@
-set -x
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/b_torchrun.json 2>gpurun_out/b_torchrun.err; python scripts/bench_summary.py gpurun_out/b_torchrun.json; tail -3 gpurun_out/b_torchrun.err
+# A/B of experimental library builds (exp/lib_*.so) on one workload: bench lines only
+W=${1:-cfg3}
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+for lib in exp/lib_*.so; do
+  HDR_LPA_LIB=$lib timeout 300 python bench.py --steps 10 --warmup 3 --workload $W --no-cpu-baseline > gpurun_out/exp_$(basename $lib .so).json 2>/dev/null
+  echo "$lib: $(python scripts/bench_summary.py gpurun_out/exp_$(basename $lib .so).json | cut -c1-120)"
+done
