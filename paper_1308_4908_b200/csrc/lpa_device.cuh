@@ -428,6 +428,33 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         fit.c1 = fit.c2 = 0.0;
         fit.g[0] = 1.0 / acc.A[0];
         return FIT_OK;
+    } else if constexpr (P == 3) {
+        // 3x3: adjugate.  Positive definiteness by Sylvester (a > 0, ad - b^2 > 0,
+        // det > 0: where the reference's Cholesky would hit a pivot <= 0),
+        // A^-1 = adj(A)/det gives c, g = A^-1 e1 and the same two-sided
+        // condition bounds as the Cholesky path (tr A tr A^-1 and
+        // max A_ii max (A^-1)_ii); float64 rounding of the cofactors moves them
+        // by <= cond * 1e-16 relative, far inside the 1e-5 margin.
+        const double a = acc.A[0], b = acc.A[1], cc = acc.A[2];
+        const double d = acc.A[3], e = acc.A[4], f = acc.A[5];
+        const double C00 = fma(d, f, -e * e), C01 = fma(cc, e, -b * f), C02 = fma(b, e, -cc * d);
+        const double C11 = fma(a, f, -cc * cc), C12 = fma(b, cc, -a * e), C22 = fma(a, d, -b * b);
+        const double det = fma(a, C00, fma(b, C01, cc * C02));
+        if (!(a > 0.0) || !(C22 > 0.0) || !(det > 0.0)) return FIT_FAIL;
+        const double rd = 1.0 / det;
+        const double b0 = acc.b[0], b1 = acc.b[1], b2 = acc.b[2];
+        fit.c0 = fma(C00, b0, fma(C01, b1, C02 * b2)) * rd;
+        fit.c1 = fma(C01, b0, fma(C11, b1, C12 * b2)) * rd;
+        fit.c2 = fma(C02, b0, fma(C12, b1, C22 * b2)) * rd;
+        fit.g[0] = C00 * rd;
+        fit.g[1] = C01 * rd;
+        fit.g[2] = C02 * rd;
+        const double cu = (a + d + f) * ((C00 + C11 + C22) * rd);
+        const double cl = fmax(a, fmax(d, f)) * (fmax(C00, fmax(C11, C22)) * rd);
+        const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
+        if (cu <= cond * (1.0 - margin)) return FIT_OK;
+        if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
+        return FIT_AMBIG;
     } else {
         double A[P * (P + 1) / 2], L[P * (P + 1) / 2], inv[P];
         acc.fill_A(A);
