@@ -43,6 +43,12 @@ static const size_t WS_HEADER = 256;
 #ifndef HDR_BRANCHY_O2
 #define HDR_BRANCHY_O2 1
 #endif
+// plane buffers per CTA of the fast kernel's staging pipeline (measured: 3
+// buffers gain nothing on cfg2 and cost cfg3 5% through occupancy)
+#ifndef HDR_NBUF
+#define HDR_NBUF 2
+#endif
+constexpr int NBUF = HDR_NBUF;
 static const size_t LUT_BYTES = 65536 * sizeof(double2);
 
 template <int ORDER>
@@ -978,10 +984,10 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__ typename std::conditional<PAT, TapParam, NoTaps>::type T) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_org[2][MAXS][2];
-    __shared__ int s_cov[2];
-    __shared__ unsigned s_done[2];
-    __shared__ __align__(8) uint64_t bar_full[2];
+    __shared__ int s_org[NBUF][MAXS][2];
+    __shared__ int s_cov[NBUF];
+    __shared__ unsigned s_done[NBUF];
+    __shared__ __align__(8) uint64_t bar_full[NBUF];
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
     unsigned char *planes = smem + P.plane_base;
@@ -993,30 +999,33 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     }
     int t = blockIdx.x;
     if (threadIdx.x == 0) {
-        mbar_init(&bar_full[0], 1);
-        mbar_init(&bar_full[1], 1);
-        s_done[0] = s_done[1] = 0;
+#pragma unroll
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&bar_full[b], 1);
+            s_done[b] = 0;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();  // barriers initialised, taps staged
-    // prologue: warp 0 stages this CTA's first two tiles
+    // prologue: warp 0 stages this CTA's first NBUF tiles
     if (threadIdx.x < 32) {
-        if (t < ntiles) stage_tile<!PAT>(P, planes, t, s_org[0], &s_cov[0], &bar_full[0]);
-        if (t + (int)gridDim.x < ntiles)
-            stage_tile<!PAT>(P, planes + P.buf_stride, t + gridDim.x, s_org[1], &s_cov[1],
-                             &bar_full[1]);
+#pragma unroll
+        for (int b = 0; b < NBUF; ++b)
+            if (t + b * (int)gridDim.x < ntiles)
+                stage_tile<!PAT>(P, planes + b * P.buf_stride, t + b * gridDim.x, s_org[b],
+                                 &s_cov[b], &bar_full[b]);
     }
     // No CTA-wide barrier in the loop: a warp waits only for its tile's data.
-    // The LAST warp to finish tile t (buffer b) refills b with tile t + 2G, so
-    // warps that finish early run ahead into tile t + G instead of idling at a
-    // __syncthreads while the slowest warp of the tile completes.
+    // The LAST warp to finish tile t (buffer b) refills b with tile t + NBUF*G,
+    // so warps that finish early run up to NBUF-1 tiles ahead instead of idling
+    // at a __syncthreads while the slowest warp of the tile completes.
     constexpr int NWARPS = NT / 32;
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
-        const int b = i & 1;
+        const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
-        mbar_wait(&bar_full[b], (uint32_t)((i >> 1) & 1));
+        mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
         tile_compute<ORDER, ICI, MAXC, PAT>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
-        const int tn = t + 2 * (int)gridDim.x;
+        const int tn = t + NBUF * (int)gridDim.x;
         if (tn < ntiles) {  // CTA-uniform
             __syncwarp();
             unsigned last = 0;
@@ -1921,7 +1930,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         d.off_ty4 = take(d.rh * 8);
     }
     P.buf_stride = smem;
-    const int smem_bytes = P.plane_base + 2 * P.buf_stride;
+    const int smem_bytes = P.plane_base + NBUF * P.buf_stride;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
     for (int s = 0; s < n_sensors; ++s)
         if (!encode_phase_map(P.s[s], &P.tmap[s])) {
