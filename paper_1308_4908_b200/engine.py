@@ -274,6 +274,28 @@ class DeviceRig:
         N.check(rc, "hdr_lpa_reconstruct_steered")
         return out
 
+    def capture(self, out_size, params: ReconstructionParams, ref_size=None, out=None,
+                **want) -> "CapturedReconstruction":
+        """Record one reconstruction (pre-pass, fast and slow kernels) as a CUDA
+        graph over this rig's current frame buffers: ``replay()`` re-runs it
+        with one launch.  Refill the frames in place (``copy_`` into
+        ``rig.raws``) between replays; ``set_frames`` invalidates the graph.
+        The outputs ``out`` (allocated if None) are the graph's."""
+        if out is None:
+            out = self.allocate_outputs(tuple(out_size), **want)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        # one eager run first: workspace allocation, kernel attributes
+        self.reconstruct(out_size, params, ref_size=ref_size, out=out, stream=side)
+        side.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = N.lib().hdr_lpa_launch_count()
+        with torch.cuda.graph(graph, stream=side):
+            self.reconstruct(out_size, params, ref_size=ref_size, out=out,
+                             stream=torch.cuda.current_stream(self.device))
+        n_kernels = int(N.lib().hdr_lpa_launch_count() - n0)
+        return CapturedReconstruction(graph, out, n_kernels, list(self.raws))
+
     def slow_items(self, out_size) -> int:
         """Work items the last reconstruct on this output size sent to the slow path."""
         ws = self.workspace(int(out_size[0]), int(out_size[1]))
@@ -334,3 +356,19 @@ class DeviceRig:
                          1.0 / np.sqrt(iv[idx].astype(np.float64)),
                          np.full(len(idx), k, np.int32)))
         return tuple(np.concatenate([c[i] for c in cols]) for i in range(5))
+
+
+class CapturedReconstruction:
+    """A reconstruction recorded as a CUDA graph (:meth:`DeviceRig.capture`).
+    Replays on the caller's current stream."""
+
+    def __init__(self, graph, out, n_kernels, raws):
+        self.graph = graph
+        self.out = out
+        self.n_kernels = n_kernels  # kernel launches of the library inside the graph
+        self.raws = raws            # the frame buffers the graph reads
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+

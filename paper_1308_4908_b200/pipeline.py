@@ -4,7 +4,8 @@ The paper's implementation overlaps transfers with computation on two
 streams.  Here three CUDA streams carry, per frame,
 H2D of the raw sensor frames -> reconstruction -> D2H of the RGB result,
 with double-buffered device slots so frame i+1's upload and frame i-1's
-download overlap frame i's kernels.  Ordering is expressed with CUDA events
+download overlap frame i's kernels.  Each slot's reconstruction is recorded
+once as a CUDA graph and replayed per frame.  Ordering is expressed with CUDA events
 only; the host never blocks inside :meth:`FramePipeline.submit`.
 """
 
@@ -18,7 +19,8 @@ from .lpa import ReconstructionParams
 
 class FramePipeline:
     def __init__(self, configs, cals, sensor_shapes, out_size, params: ReconstructionParams,
-                 ref_size=None, device=None, slots: int = 2, d2h_streams: int = 1):
+                 ref_size=None, device=None, slots: int = 2, d2h_streams: int = 1,
+                 graphs: bool = True):
         self.device = torch.device(device if device is not None else
                                    torch.device("cuda", torch.cuda.current_device()))
         self.out_size = (int(out_size[0]), int(out_size[1]))
@@ -33,6 +35,10 @@ class FramePipeline:
         for r in self.rigs[1:]:
             r._workspaces[self.out_size] = ws
         self.outs = [self.rigs[0].allocate_outputs(self.out_size) for _ in range(slots)]
+        # per slot, the reconstruction recorded once as a CUDA graph (its frame
+        # buffers are the slot's fixed upload targets): one launch per frame
+        self.captured = [rig.capture(self.out_size, params, ref_size=ref_size, out=o)
+                         for rig, o in zip(self.rigs, self.outs)] if graphs else None
         self.s_in = torch.cuda.Stream(self.device)
         self.s_comp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
@@ -68,8 +74,11 @@ class FramePipeline:
             self.s_comp.wait_event(self.ev_in[k])
             if self.n >= self.slots:
                 self.s_comp.wait_event(self.ev_out[k])  # output slot downloaded
-            self.rigs[k].reconstruct(self.out_size, self.params, ref_size=self.ref_size,
-                                     out=self.outs[k], stream=self.s_comp)
+            if self.captured:
+                self.captured[k].replay()
+            else:
+                self.rigs[k].reconstruct(self.out_size, self.params, ref_size=self.ref_size,
+                                         out=self.outs[k], stream=self.s_comp)
             self.ev_comp[k].record(self.s_comp)
             self.ev_free[k] = self.ev_comp[k]
         streams = [self.s_out] + self.s_out_extra
