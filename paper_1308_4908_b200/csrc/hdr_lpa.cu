@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <type_traits>
@@ -43,6 +44,7 @@ static const size_t WS_HEADER = 256;
 #ifndef HDR_BRANCHY_O2
 #define HDR_BRANCHY_O2 1
 #endif
+static_assert(sizeof(DevParams) + TAP_PARAM_BYTES <= 32764, "kernel parameter space");
 // plane buffers per CTA of the fast kernel's staging pipeline (measured: 3
 // buffers gain nothing on cfg2 and cost cfg3 5% through occupancy)
 #ifndef HDR_NBUF
@@ -104,7 +106,8 @@ struct GlobalSweep {
         return v;
     }
     template <class Body>
-    __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
+    __device__ __forceinline__ void operator()(int c, int /*k*/, double r, double r2,
+                                               Body body) const {
         for (int s = 0; s < P.n_sensors; ++s) {
             const DevSensor &S = P.s[s];
             const int pm = S.phmask[c];
@@ -156,31 +159,67 @@ struct PerSample {
     }
 };
 
-template <int MAXC, bool BRANCHY>
+template <int MAXC, bool BRANCHY, bool RT = false>
 struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
     const int (*org)[2];
     double qx, qy;
+    int px, py;                 // the output pixel (RT: parity class, phase-plane base)
+    const unsigned char *rt;    // RT: row-tap table in shared memory (rows, then taps)
     template <int PN>
     __device__ __forceinline__ void reduce(Acc<PN> &) const {}
     __device__ __forceinline__ double reduce(double v) const { return v; }
     // Per-sample traversal (same interface as GlobalSweep).
     template <class Body>
-    __device__ __forceinline__ void operator()(int c, double r, double r2, Body body) const {
+    __device__ __forceinline__ void operator()(int c, int k, double r, double r2, Body body) const {
         PerSample<Body> pol{body};
-        rows(c, r, r2, pol);
+        rows(c, k, r, r2, pol);
+    }
+
+    // RT: the pre-computed rows of a translation-only sensor at scale k (all
+    // taps inside r_k by construction; masked samples contribute weight 0).
+    template <class Pol>
+    __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol) const {
+        const DevSensor &S = P.s[s];
+        const int cls = ((py & 1) << 1) | (px & 1);
+        const int r0 = P.pat_off[s][c][cls], nr = P.rt_nrow[s][c][cls];
+        const TapRow *rows = (const TapRow *)rt;
+        const RowTap *taps = (const RowTap *)(rt + (size_t)P.n_taps * sizeof(TapRow));
+        const int pw = S.rw >> 1;
+        const unsigned char *vb = sm + S.off_vi +
+                                  8 * (((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+        for (int ri = r0; ri < r0 + nr; ++ri) {
+            const TapRow &R = rows[ri];
+            const int lo = R.lo[k], hi = R.hi[k];
+            if (lo >= hi) continue;
+            const double dy = R.dy, dyy = dy * dy;
+            pol.begin_row(dy, dyy);
+            for (int t = R.first + lo; t < R.first + hi; ++t) {
+                const RowTap T = taps[t];
+                const float2 e = *(const float2 *)(vb + T.off);
+                pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f);
+            }
+            pol.end_row(dy, dyy);
+        }
     }
 
     // Traversal with row hooks: for separable sensors every sample of a row
     // shares dy, so a policy can accumulate per-row sums (begin_row / sample /
     // end_row); rotated sensors go through pol.general() per sample.
     template <class Pol>
-    __device__ __forceinline__ void rows(int c, double r, double r2, Pol &pol) const {
+    __device__ __forceinline__ void rows(int c, int k, double r, double r2, Pol &pol) const {
         for (int s = 0; s < P.n_sensors; ++s) {
             const DevSensor &S = P.s[s];
             const int pm = S.phmask[c];
             if (!pm) continue;
+            if constexpr (RT) {
+                // RT mode: every separable sensor is translation-only and tapped
+                if (S.separable) {
+                    tap_rows(s, c, k, pol);
+                    continue;
+                }
+            }
             const int ox = org[s][0], oy = org[s][1];
             const float2 *vi = (const float2 *)(sm + S.off_vi);
             const double *tx0 = (const double *)(sm + S.off_tx0);
@@ -188,7 +227,7 @@ struct TileSweep {
             const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
             int xlo, xhi, ylo, yhi;
             window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
-            if (S.separable) {
+            if (!RT && S.separable) {
                 for (int ph = 0; ph < 4; ++ph) {
                     if (!((pm >> ph) & 1)) continue;
                     const int py = ph >> 1, px = ph & 1;
@@ -440,8 +479,8 @@ template <class Sweep>
 struct HasRows {
     static constexpr bool value = false;
 };
-template <int MAXC, bool BRANCHY>
-struct HasRows<TileSweep<MAXC, BRANCHY>> {
+template <int MAXC, bool BRANCHY, bool RT>
+struct HasRows<TileSweep<MAXC, BRANCHY, RT>> {
     static constexpr bool value = true;
 };
 
@@ -451,13 +490,13 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
     if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
         acc.zero();
         RowMoments<ORDER> pol{acc, P.hl[c][k]};
-        sweep.rows(c, r, r2, pol);
+        sweep.rows(c, k, r, r2, pol);
         return;
     }
     acc.zero();
     if constexpr (EXACT) {
         const double hi = P.hinv[c][k];
-        sweep(c, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
+        sweep(c, k, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
                             float) {
             const double q =
                 __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
@@ -466,7 +505,7 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
         sweep.reduce(acc);
     } else {
         const float hl = P.hl[c][k];
-        sweep(c, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
+        sweep(c, k, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
                             double dyy, float d2f) {
             const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;  // w = W / den
             const double y = ok ? v : 0.0;
@@ -483,7 +522,7 @@ __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k,
                                                const double *g, float *tsum = nullptr) {
     if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
         RowVariance<ORDER> pol{g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0, 0.f};
-        sweep.rows(c, P.r[c][k], P.r2[c][k], pol);
+        sweep.rows(c, k, P.r[c][k], P.r2[c][k], pol);
         if (tsum) *tsum = pol.T;
         return pol.v;
     }
@@ -493,7 +532,7 @@ __device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k,
     const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4], g5 = g[5];
     double v = 0.0;
     float T = 0.f;
-    sweep(c, P.r[c][k], P.r2[c][k],
+    sweep(c, k, P.r[c][k], P.r2[c][k],
           [&](bool ok, double y, auto iv, double dx, double dy, double dxx, double dyy, float d2f) {
               double t;
               if constexpr (EXACT) {
@@ -895,7 +934,7 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
     acc.sabs = sabs;
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT>
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int t,
                                              const int (*org)[2], bool tile_covered) {
@@ -918,7 +957,8 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
                    yhi < org[s][1] + S.rh;
     }
-    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2)> sweep{P, sm, org, qx, qy};
+    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org, qx, qy,
+                                                                   px, py, taps};
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
@@ -977,12 +1017,13 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #ifndef HDR_PAT_MINBLOCKS
 #define HDR_PAT_MINBLOCKS 3
 #endif
-template <int ORDER, bool ICI, int MAXC, bool PAT>
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
     lpa_fast_kernel(const __grid_constant__ DevParams P,
-                    const __grid_constant__ typename std::conditional<PAT, TapParam, NoTaps>::type T) {
+                    const __grid_constant__
+                    typename std::conditional<PAT || RT, TapParam, NoTaps>::type T) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];
@@ -991,11 +1032,11 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
     unsigned char *planes = smem + P.plane_base;
-    if constexpr (PAT) {
+    if constexpr (PAT || RT) {  // the kernel-parameter table into shared memory
         const uint4 *src = (const uint4 *)T.bytes;
         uint4 *dst = (uint4 *)(smem + P.off_taps);
-        const int n16 = P.n_taps * (int)sizeof(Tap) / 16 + 1;  // 24 B per tap, 16-B chunks
-        for (int i = threadIdx.x; i < n16 && 16 * i < TAP_PARAM_BYTES; i += NT) dst[i] = src[i];
+        const int n16 = (P.tab_bytes + 15) / 16;
+        for (int i = threadIdx.x; i < n16; i += NT) dst[i] = src[i];
     }
     int t = blockIdx.x;
     if (threadIdx.x == 0) {
@@ -1024,7 +1065,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
-        tile_compute<ORDER, ICI, MAXC, PAT>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
+        tile_compute<ORDER, ICI, MAXC, PAT, RT>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
         const int tn = t + NBUF * (int)gridDim.x;
         if (tn < ntiles) {  // CTA-uniform
             __syncwarp();
@@ -1176,7 +1217,7 @@ __device__ __forceinline__ void accumulate_hinv(const Sweep &sweep, int c, doubl
                                                 Acc<NC<ORDER>::P> &acc) {
     acc.zero();
     const double h12x2 = 2.0 * h12;
-    sweep(c, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
+    sweep(c, -1, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
                         float) {
         // q = h11*dx*dx + 2.0*h12*dx*dy + h22*dy*dy (_kernels.py:164)
         const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(h11, dx), dx),
@@ -1558,10 +1599,10 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT = false>
+template <int ORDER, bool ICI, int MAXC, bool PAT = false, bool RT = false>
 static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
-    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT>;
+    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -1571,10 +1612,10 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
         return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
     COUNT_LAUNCH();
-    if constexpr (PAT)
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P, T);
+    if constexpr (PAT || RT)
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT><<<grid, NT, smem_bytes, st>>>(P, T);
     else
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_fast_kernel launch");
 }
 
@@ -1615,6 +1656,12 @@ static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem
     int rc;
     if (P.pat)
         rc = launch_fast<ORDER, false, 4, true>(P, T, tiles, smem_bytes, st);
+    else if (P.rt && P.n_scales > 1)
+        rc = maxc <= 6 ? launch_fast<ORDER, true, 6, false, true>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, true, 8, false, true>(P, T, tiles, smem_bytes, st);
+    else if (P.rt)
+        rc = maxc <= 4 ? launch_fast<ORDER, false, 4, false, true>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, false, 8, false, true>(P, T, tiles, smem_bytes, st);
     else if (P.n_scales > 1)
         rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, T, tiles, smem_bytes, st)
                        : launch_fast<ORDER, true, 8>(P, T, tiles, smem_bytes, st);
@@ -1641,6 +1688,101 @@ static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem
 // the reference's arithmetic at a representative pixel; a tap closer than
 // 1e-9 r^2 to the support boundary (where that rounding could flip the
 // membership test) disables the mode.
+// Row-tap mode: the same construction for the translation-only sensors of a
+// rig on the reference grid when PAT does not apply (ICI scales, order 2 or a
+// rotated sensor elsewhere in the rig).  Per (sensor, channel, class) the
+// sensor rows of the largest window, each with the exact dy and its taps in
+// column order; d2 is convex along a row, so each scale's members are one run
+// [lo[k], hi[k]).  Any tap within 1e-9 r_k^2 of any scale's support boundary
+// disables the mode (the per-pixel rounding could flip membership there).
+static bool build_rowtaps(DevParams &P, TapParam &T) {
+    if (P.sx != 1.0 || P.sy != 1.0) return false;
+    bool any = false;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const DevSensor &S = P.s[s];
+        if (!S.separable) continue;
+        if (!(S.T[0] == 1.0 && S.T[4] == 1.0)) return false;  // separable but scaled
+        if (fabs(S.T[2]) > 64 || fabs(S.T[5]) > 64 || S.width > 4096 || S.height > 4096)
+            return false;
+        any = true;
+    }
+    if (!any) return false;
+    std::vector<TapRow> rows;
+    std::vector<RowTap> taps;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const DevSensor &S = P.s[s];
+        if (!S.separable) continue;
+        int tile[4];
+        for (int ph = 0; ph < 4; ++ph)
+            for (int c = 0; c < 3; ++c)
+                if ((S.phmask[c] >> ph) & 1) tile[ph] = c;
+        const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
+        for (int c = 0; c < 3; ++c) {
+            double rmax2 = 0.0, rmax = 0.0;
+            for (int k = 0; k < P.n_scales; ++k) {
+                rmax2 = fmax(rmax2, P.r2[c][k]);
+                rmax = fmax(rmax, P.r[c][k]);
+            }
+            const int R = (int)ceil(rmax + fabs(S.T[2]) + fabs(S.T[5])) + 1;
+            for (int cl = 0; cl < 4; ++cl) {
+                const int j = 64 + (cl & 1), i = 64 + (cl >> 1);  // representative pixel
+                const double qx = (double)j, qy = (double)i;      // qcoord(j, 1.0) == j
+                P.pat_off[s][c][cl] = (int)rows.size();
+                for (int m = -R; m <= R; ++m) {
+                    const int y = i + m;
+                    TapRow row;
+                    memset(&row, 0, sizeof(row));
+                    row.first = (int)taps.size();
+                    std::vector<double> d2s;
+                    for (int k2 = -R; k2 <= R; ++k2) {
+                        const int x = j + k2;
+                        if (tile[((y & 1) << 1) | (x & 1)] != c) continue;
+                        const double X = (1.0 * (double)x + 0.0 * (double)y) + S.T[2];
+                        const double Y = (0.0 * (double)x + 1.0 * (double)y) + S.T[5];
+                        const double dx = X - qx, dy = Y - qy;
+                        const double d2 = dx * dx + dy * dy;
+                        for (int k = 0; k < P.n_scales; ++k)
+                            if (fabs(d2 - P.r2[c][k]) <= 1e-9 * P.r2[c][k]) return false;
+                        if (d2 > rmax2) continue;
+                        RowTap t;
+                        t.dx = dx;
+                        t.d2f = (float)d2;
+                        const int ph = ((y & 1) << 1) | (x & 1);
+                        t.off = (int)sizeof(float2) *
+                                (ph * plane + ((y >> 1) - (i >> 1)) * pw + ((x >> 1) - (j >> 1)));
+                        taps.push_back(t);
+                        d2s.push_back(d2);
+                        row.dy = dy;
+                    }
+                    const int n = (int)d2s.size();
+                    if (!n) continue;
+                    if (n > 255) return false;
+                    for (int k = 0; k < P.n_scales; ++k) {
+                        int lo = n, hi = 0;
+                        for (int u = 0; u < n; ++u)
+                            if (d2s[u] <= P.r2[c][k]) {
+                                lo = std::min(lo, u);
+                                hi = u + 1;
+                            }
+                        if (lo >= hi) lo = hi = 0;
+                        row.lo[k] = (unsigned char)lo;
+                        row.hi[k] = (unsigned char)hi;
+                    }
+                    rows.push_back(row);
+                }
+                P.rt_nrow[s][c][cl] = (int)rows.size() - P.pat_off[s][c][cl];
+            }
+        }
+    }
+    const size_t bytes = rows.size() * sizeof(TapRow) + taps.size() * sizeof(RowTap);
+    if (bytes > (size_t)TAP_PARAM_BYTES) return false;
+    memcpy(T.bytes, rows.data(), rows.size() * sizeof(TapRow));
+    memcpy(T.bytes + rows.size() * sizeof(TapRow), taps.data(), taps.size() * sizeof(RowTap));
+    P.n_taps = (int)rows.size();  // RT: the taps follow n_taps rows
+    P.tab_bytes = (int)bytes;
+    return true;
+}
+
 static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
     taps.clear();
     if (P.n_scales != 1 || P.sx != 1.0 || P.sy != 1.0) return false;
@@ -1918,6 +2060,10 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
             w[i].W = taps[i].W;
             w[i].off = taps[i].delta * (int)sizeof(float2);
         }
+        P.tab_bytes = (int)(n * sizeof(Tap));
+    } else {
+        P.rt = build_rowtaps(P, T) ? 1 : 0;
+        if (P.rt) P.off_taps = take(P.tab_bytes);
     }
     P.plane_base = smem;
     smem = 0;

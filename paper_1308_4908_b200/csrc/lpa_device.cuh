@@ -77,11 +77,26 @@ struct TapW {
 // The tap table travels as a __grid_constant__ kernel parameter (kernel
 // parameters may total 32764 B; DevParams takes ~5.6 KB): no device copy whose
 // lifetime could outlive the caller's workspace.
-constexpr int TAP_PARAM_BYTES = 26880;  // 1120 taps
+constexpr int TAP_PARAM_BYTES = 26752;  // 1114 PAT taps
 struct __align__(16) TapParam {
     unsigned char bytes[TAP_PARAM_BYTES];
 };
 struct NoTaps {};
+// Row taps (RT mode): per (translation-only sensor, channel, parity class) the
+// sensor rows of the largest ICI window, each with its exact dy and its taps
+// (exact dx, |d|^2, sample offset) in column order; per scale k the taps
+// [lo[k], hi[k]) of a row are the ones inside r_k (a contiguous run).
+struct __align__(16) RowTap {
+    double dx;
+    float d2f;
+    int off;  // byte offset of the sample from the pixel's own phase-plane position
+};
+struct __align__(16) TapRow {
+    double dy;
+    int first;  // index of the row's first RowTap
+    int pad;
+    unsigned char lo[8], hi[8];
+};
 
 struct DevParams {
     CUtensorMap tmap[MAXS];   // per-sensor 3-D maps over the phase planes (box = staged region)
@@ -106,11 +121,12 @@ struct DevParams {
     uint32_t *work;
     int flags, pad1;
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
-    int pat, n_taps, off_taps, pad2;
+    int pat, n_taps, off_taps, tab_bytes;  // tab_bytes: kernel-parameter table size (PAT or RT)
+    int rt;                         // row-tap mode (ICI / order 2 with translation-only sensors)
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
-    int pat_base[MAXS][2];          // offset (ox, oy) of the tap window's origin: see build_taps
+    int rt_nrow[MAXS][3][4];        // RT: tap rows of (sensor, channel, class); first row in pat_off
     uint32_t *work_count;
     uint32_t *work_items;
     // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)
