@@ -214,6 +214,16 @@ int hdr_saturation_mask(const HdrSensor *sensor, uint32_t *out_bits, int words_p
 int hdr_radiance_planes(const HdrSensor *sensor, int weight_mode, float *value, float *inv_den,
                         void *stream);
 
+/*
+ * The reference's sample columns of one sensor as float64 planes, bit-exact
+ * (radiometry.py:271-336 in its operation order): value[i] = f_hat and
+ * sigma[i] = sqrt(max(var, (1/12)/(g t a n)^2)); sigma == 0 marks a pixel that
+ * yields no sample.  Positions and channels follow from the pixel index
+ * (apply_transform, channel_map); RawFrameSet.materialize() compacts these on
+ * the device into RadianceSamples.
+ */
+int hdr_sample_planes(const HdrSensor *sensor, double *value, double *sigma, void *stream);
+
 /* Number of (pixel, channel) items the last call on this workspace routed
  * through the exact slow path (device value; reads it synchronously). */
 int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream);

@@ -38,6 +38,7 @@ EXPORTED = (
     "hdr_lpa_evaluate_samples",
     "hdr_saturation_mask",
     "hdr_radiance_planes",
+    "hdr_sample_planes",
     "hdr_lpa_slow_items",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
@@ -167,6 +168,8 @@ def lib():
                                               ctypes.c_int, ctypes.c_void_p]
             L.hdr_radiance_planes.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_int,
                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            L.hdr_sample_planes.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p]
             L.hdr_lpa_slow_items.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
                                              ctypes.c_void_p]
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]

@@ -1503,6 +1503,26 @@ __global__ void radiance_planes_kernel(const DevSensor S, int use_sigma, float *
     inv_den[(size_t)y * S.width + x] = e.y;
 }
 
+// The reference's sample columns as float64 planes (radiometry.py:303-336):
+// value = f_hat, sigma = sqrt(max(var, quantisation floor)); sigma = 0 marks
+// "no sample" (saturated / defective).
+__global__ void sample_planes_kernel(const DevSensor S, double *value, double *sigma) {
+    const int y = blockIdx.y;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= S.width) return;
+    const size_t i = (size_t)y * S.width + x;
+    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+    double f = 0.0, sg = 0.0;
+    if (raw < S.sat && !(S.defective && __ldg(S.defective + i))) {
+        const double b = S.bias_p ? __ldg(S.bias_p + i) : S.bias;
+        const double a = S.nonuni_p ? __ldg(S.nonuni_p + i) : S.nonuni;
+        const double vr = S.readvar_p ? __ldg(S.readvar_p + i) : S.readvar;
+        radiometry_sigma(S, raw, b, a, vr, f, sg);
+    }
+    value[i] = f;
+    sigma[i] = sg;
+}
+
 // DFMA throughput probe: 8 independent chains per thread, full occupancy.
 __global__ void __launch_bounds__(256) fp64_probe_kernel(double *sink, int iters, double a,
                                                          double b) {
@@ -2222,6 +2242,17 @@ int hdr_radiance_planes(const HdrSensor *sensor, int weight_mode, float *value, 
     COUNT_LAUNCH();
     radiance_planes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
         d, weight_mode == HDR_WEIGHT_SIGMA, value, inv_den);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+}
+
+int hdr_sample_planes(const HdrSensor *sensor, double *value, double *sigma, void *stream) {
+    if (!sensor || !value || !sigma) return HDR_ERR_ARG;
+    DevSensor d;
+    const int rc = fill_sensor(*sensor, d);
+    if (rc != HDR_OK) return rc;
+    dim3 grid((d.width + 255) / 256, d.height);
+    COUNT_LAUNCH();
+    sample_planes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d, value, sigma);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
 }
 

@@ -195,8 +195,9 @@ __device__ __forceinline__ float2 radiance_sample(const DevSensor &S, int x, int
 // for "no sample"; iv = 1/den (one rounding more than the reference's W/den).
 // Used by the exact (slow) path, whose results must not inherit the fp32
 // rounding of the staged phase planes.
-__device__ __forceinline__ void radiometry_exact(const DevSensor &S, int raw, double b, double a,
-                                                 double vr, int use_sigma, double &f, double &iv) {
+// f_hat and the reference's sigma = sqrt(max(var, quantisation floor))
+__device__ __forceinline__ void radiometry_sigma(const DevSensor &S, int raw, double b, double a,
+                                                 double vr, double &f, double &sg) {
     const double denom = __dmul_rn(__dmul_rn(__dmul_rn(S.g, S.t), S.n), a);
     f = __ddiv_rn(__dsub_rn((double)raw, b), denom);
     const double d2 = __dmul_rn(denom, denom);
@@ -204,8 +205,13 @@ __device__ __forceinline__ void radiometry_exact(const DevSensor &S, int raw, do
         __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(S.g, S.g), S.t), a), S.n), f > 0.0 ? f : 0.0);
     const double var = __ddiv_rn(__dadd_rn(shot, vr), d2);
     const double qv = __ddiv_rn(1.0 / 12.0, d2);
-    const double sg = __dsqrt_rn(var >= qv ? var : qv);
-    double den = __dmul_rn(sg, sg);
+    sg = __dsqrt_rn(var >= qv ? var : qv);
+}
+__device__ __forceinline__ void radiometry_exact(const DevSensor &S, int raw, double b, double a,
+                                                 double vr, int use_sigma, double &f, double &iv) {
+    double sg;
+    radiometry_sigma(S, raw, b, a, vr, f, sg);
+    double den = __dmul_rn(sg, sg);  // SampleIndex stores sigma**2 (radiometry.py:240)
     if (use_sigma) den = __dsqrt_rn(den);
     iv = __drcp_rn(den);
 }

@@ -336,26 +336,40 @@ class DeviceRig:
             res.append((v, iv))
         return res
 
+    def sample_planes(self):
+        """Per sensor (value, sigma) float64 (h, w) device tensors: the
+        reference's sample columns per pixel, bit-exact; sigma 0 = no sample."""
+        st = torch.cuda.current_stream(self.device)
+        res = []
+        for k, raw in enumerate(self.raws):
+            v = torch.empty(tuple(raw.shape), dtype=torch.float64, device=self.device)
+            s = torch.empty_like(v)
+            N.check(N.lib().hdr_sample_planes(ctypes.byref(self._sensors[k]), v.data_ptr(),
+                                              s.data_ptr(), st.cuda_stream), "hdr_sample_planes")
+            res.append((v, s))
+        return res
+
     def materialize_samples(self):
-        """Sample columns in the reference's order (sensor-major, raster):
-        positions (n, 2) f64, channels u8, values f64, sigmas f64, sensor ids."""
+        """Sample columns in the reference's order (sensor-major, raster;
+        radiometry.py:303-349), compacted on the device: positions (n, 2) f64,
+        channels u8, values f64, sigmas f64, sensor ids i32 as device tensors.
+        Values and sigmas are bit-identical to the reference's; positions use
+        apply_transform's operation order (T00*x + T01*y + T02)."""
         cols = []
-        for k, (v, iv) in enumerate(self.radiance_planes("variance")):
+        for k, (v, s) in enumerate(self.sample_planes()):
             cfg = self.configs[k]
-            v = v.cpu().numpy().ravel()
-            iv = iv.cpu().numpy().ravel()
-            h, w = int(self.raws[k].shape[0]), int(self.raws[k].shape[1])
-            idx = np.flatnonzero(iv > 0)
-            ys, xs = np.divmod(idx, w)
+            w = int(self.raws[k].shape[1])
+            idx = torch.nonzero(s.reshape(-1) > 0).squeeze(1)  # ascending = raster order
+            ys, xs = idx // w, idx % w
             T = np.asarray(cfg.transform, dtype=np.float64)
-            X = T[0, 0] * xs + T[0, 1] * ys + T[0, 2]
-            Y = T[1, 0] * xs + T[1, 1] * ys + T[1, 2]
-            tile = np.asarray(cfg.pattern.flat_tile(), np.uint8)
+            xd, yd = xs.to(torch.float64), ys.to(torch.float64)
+            X = float(T[0, 0]) * xd + float(T[0, 1]) * yd + float(T[0, 2])
+            Y = float(T[1, 0]) * xd + float(T[1, 1]) * yd + float(T[1, 2])
+            tile = torch.as_tensor(np.asarray(cfg.pattern.flat_tile(), np.uint8), device=self.device)
             ch = tile[(ys % 2) * 2 + xs % 2]
-            cols.append((np.column_stack([X, Y]), ch, v[idx].astype(np.float64),
-                         1.0 / np.sqrt(iv[idx].astype(np.float64)),
-                         np.full(len(idx), k, np.int32)))
-        return tuple(np.concatenate([c[i] for c in cols]) for i in range(5))
+            cols.append((torch.stack([X, Y], 1), ch, v.reshape(-1)[idx], s.reshape(-1)[idx],
+                         torch.full((len(idx),), k, dtype=torch.int32, device=self.device)))
+        return tuple(torch.cat([c[i] for c in cols]) for i in range(5))
 
 
 class CapturedReconstruction:

@@ -134,16 +134,17 @@ def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=
     ``samples`` is the RawFrameSet of :func:`frames_to_samples` (fused raw
     path) or scattered :class:`~.samples.RadianceSamples` (CSR index path)."""
     if _is_scattered(samples):
-        from .samples import reconstruct_channel_samples
+        import torch
 
-        out_w, out_h = out_size
-        planes = np.empty((out_h, out_w, 3), dtype=np.float32)
-        grads = {}
+        from .samples import reconstruct_channel_device
+
+        planes, grads = [], {}
         for ch in ColorChannel:
-            val, gx, gy = reconstruct_channel_samples(samples, out_size, params, ch, ref_size)
-            planes[:, :, int(ch)] = np.maximum(val, 0.0).astype(np.float32)
-            grads[ch] = (gx, gy)
-        img = HDRImage(planes)
+            val, gx, gy = reconstruct_channel_device(samples, out_size, params, ch, ref_size)
+            planes.append(torch.clamp_min(val, 0.0).to(torch.float32))  # keeps NaN (lpa.py:428)
+            if return_gradients:
+                grads[ch] = (gx.cpu().numpy(), gy.cpu().numpy())
+        img = HDRImage(torch.stack(planes, 2).cpu().numpy())
         return (img, grads) if return_gradients else img
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=return_gradients)

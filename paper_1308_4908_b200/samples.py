@@ -25,6 +25,10 @@ from .lpa import SUPPORT_SIGMAS, grid_coordinates
 from .validation import check_positions
 
 
+def _as_numpy(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a
+
+
 def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
@@ -38,24 +42,75 @@ class RadianceSample:
     sensor_id: int
 
 
+_COLUMNS = ("positions", "channels", "values", "sigmas", "sensor_ids")
+_DTYPES = {"positions": np.float64, "channels": np.uint8, "values": np.float64,
+           "sigmas": np.float64, "sensor_ids": np.int32}
+
+
 class RadianceSamples:
-    """Column-oriented samples (reference radiometry.py:150-205)."""
+    """Column-oriented samples (reference radiometry.py:150-205).
+
+    Columns may be host numpy arrays or device torch tensors (as produced by
+    ``RawFrameSet.materialize()``): device columns stay on the GPU for the
+    index build and the evaluation, and the numpy attributes are filled on
+    first access."""
 
     def __init__(self, positions, channels, values, sigmas, sensor_ids):
-        self.positions = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 2)
-        n = len(self.positions)
-        self.channels = np.ascontiguousarray(channels, dtype=np.uint8).reshape(n)
-        self.values = np.ascontiguousarray(values, dtype=np.float64).reshape(n)
-        self.sigmas = np.ascontiguousarray(sigmas, dtype=np.float64).reshape(n)
-        self.sensor_ids = np.ascontiguousarray(sensor_ids, dtype=np.int32).reshape(n)
-        if (self.sigmas <= 0).any():
-            raise ValueError("sample sigmas must be positive")
-        if not np.isfinite(self.positions).all():
-            raise ValueError("sample positions must be finite")
+        cols = dict(zip(_COLUMNS, (positions, channels, values, sigmas, sensor_ids)))
+        self._dev = None
+        if all(isinstance(v, torch.Tensor) and v.is_cuda for v in cols.values()):
+            tdt = {"positions": torch.float64, "channels": torch.uint8, "values": torch.float64,
+                   "sigmas": torch.float64, "sensor_ids": torch.int32}
+            dev = {k: v.to(tdt[k]).contiguous() for k, v in cols.items()}
+            n = dev["values"].numel()
+            dev["positions"] = dev["positions"].reshape(n, 2)
+            if bool((dev["sigmas"] <= 0).any()):
+                raise ValueError("sample sigmas must be positive")
+            if not bool(torch.isfinite(dev["positions"]).all()):
+                raise ValueError("sample positions must be finite")
+            self._dev, self._host, self._n = dev, {}, n
+        else:
+            host = {}
+            host["positions"] = np.ascontiguousarray(
+                _as_numpy(positions), dtype=np.float64).reshape(-1, 2)
+            n = len(host["positions"])
+            for k in _COLUMNS[1:]:
+                host[k] = np.ascontiguousarray(_as_numpy(cols[k]), dtype=_DTYPES[k]).reshape(n)
+            if (host["sigmas"] <= 0).any():
+                raise ValueError("sample sigmas must be positive")
+            if not np.isfinite(host["positions"]).all():
+                raise ValueError("sample positions must be finite")
+            self._host, self._n = host, n
         self._indexes = {}
+        self._uploads = {}
+
+    def _column(self, name):
+        if name not in self._host:
+            self._host[name] = self._dev[name].cpu().numpy()
+        return self._host[name]
+
+    positions = property(lambda self: self._column("positions"))
+    channels = property(lambda self: self._column("channels"))
+    values = property(lambda self: self._column("values"))
+    sigmas = property(lambda self: self._column("sigmas"))
+    sensor_ids = property(lambda self: self._column("sensor_ids"))
+
+    @property
+    def on_device(self) -> bool:
+        return self._dev is not None
+
+    def device_column(self, name, device):
+        """Column ``name`` as a device tensor (uploaded once if host-backed)."""
+        device = torch.device(device)
+        if self._dev is not None and self._dev[name].device == device:
+            return self._dev[name]
+        key = (name, str(device))
+        if key not in self._uploads:
+            self._uploads[key] = torch.from_numpy(self._column(name)).to(device)
+        return self._uploads[key]
 
     def __len__(self) -> int:
-        return len(self.values)
+        return self._n
 
     def __getitem__(self, k: int) -> RadianceSample:
         return RadianceSample((float(self.positions[k, 0]), float(self.positions[k, 1])),
@@ -72,8 +127,7 @@ class RadianceSamples:
         parts = [p for p in parts if len(p)]
         if not parts:
             return cls.empty()
-        return cls(*(np.concatenate([getattr(p, a) for p in parts]) for a in
-                     ("positions", "channels", "values", "sigmas", "sensor_ids")))
+        return cls(*(np.concatenate([getattr(p, a) for p in parts]) for a in _COLUMNS))
 
     def index(self, channel) -> "SampleIndex":
         key = int(channel)
@@ -89,10 +143,12 @@ class SampleIndex:
 
     def __init__(self, samples: RadianceSamples, channel: ColorChannel, device=None):
         dev = torch.device(device) if device is not None else _device()
-        sel = np.flatnonzero(samples.channels == int(channel))
-        self.n = int(len(sel))
-        x = torch.from_numpy(samples.positions[sel, 0].copy()).to(dev)
-        y = torch.from_numpy(samples.positions[sel, 1].copy()).to(dev)
+        ch = samples.device_column("channels", dev)
+        sel = torch.nonzero(ch == int(channel)).squeeze(1)  # ascending: the reference's order
+        self.n = int(sel.numel())
+        pos = samples.device_column("positions", dev)
+        x = pos[sel, 0].contiguous()
+        y = pos[sel, 1].contiguous()
         if self.n:
             self.x0 = int(math.floor(float(x.min())))
             self.y0 = int(math.floor(float(y.min())))
@@ -106,8 +162,8 @@ class SampleIndex:
         counts = torch.bincount(cell, minlength=self.nx * self.ny)
         self.cell_start = torch.zeros(self.nx * self.ny + 1, dtype=torch.int64, device=dev)
         self.cell_start[1:] = torch.cumsum(counts, 0)
-        v = torch.from_numpy(samples.values[sel].copy()).to(dev)
-        s = torch.from_numpy(samples.sigmas[sel].copy()).to(dev)
+        v = samples.device_column("values", dev)[sel]
+        s = samples.device_column("sigmas", dev)[sel]
         self.packed = torch.stack([x[order], y[order], v[order], (s * s)[order]], 1).contiguous()
         self.device = dev
 
@@ -121,19 +177,26 @@ class SampleIndex:
 
 def evaluate_index(index: SampleIndex, qx, qy, order: int, scale: float, max_radius: float,
                    cond_threshold: float, weight_mode: str = "variance", steering=None):
-    """_evaluate_index (lpa.py:322-376): (value, gx, gy) float64 numpy arrays."""
-    qx = np.ascontiguousarray(qx, dtype=np.float64).ravel()
-    qy = np.ascontiguousarray(qy, dtype=np.float64).ravel()
-    m = len(qx)
-    if len(index) == 0:
-        nan = np.full(m, np.nan)
-        return nan, nan.copy(), nan.copy()
+    """_evaluate_index (lpa.py:322-376): (value, gx, gy) float64 -- numpy arrays
+    for numpy queries, device tensors (no host round trip) for device queries."""
+    on_dev = isinstance(qx, torch.Tensor)
     dev = index.device
-    tqx, tqy = torch.from_numpy(qx).to(dev), torch.from_numpy(qy).to(dev)
+    if on_dev:
+        tqx = qx.to(dev, torch.float64).contiguous().reshape(-1)
+        tqy = qy.to(dev, torch.float64).contiguous().reshape(-1)
+    else:
+        tqx = torch.from_numpy(np.ascontiguousarray(qx, dtype=np.float64).ravel()).to(dev)
+        tqy = torch.from_numpy(np.ascontiguousarray(qy, dtype=np.float64).ravel()).to(dev)
+    m = tqx.numel()
+    if len(index) == 0:
+        nan = torch.full((m,), float("nan"), dtype=torch.float64, device=dev)
+        out = (nan, nan.clone(), nan.clone())
+        return out if on_dev else tuple(o.cpu().numpy() for o in out)
     out = [torch.empty(m, dtype=torch.float64, device=dev) for _ in range(3)]
     an = [None] * 4
     if steering is not None:
-        an = [torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).ravel()).to(dev)
+        an = [a.to(dev, torch.float64).contiguous().reshape(-1) if isinstance(a, torch.Tensor)
+              else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).ravel()).to(dev)
               for a in steering]
     ix = index.c_struct()
     st = torch.cuda.current_stream(dev)
@@ -144,7 +207,7 @@ def evaluate_index(index: SampleIndex, qx, qy, order: int, scale: float, max_rad
         float(cond_threshold), N.HDR_WEIGHT_SIGMA if weight_mode == "sigma" else
         N.HDR_WEIGHT_VARIANCE, out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(),
         st.cuda_stream), "hdr_lpa_evaluate_samples")
-    return tuple(o.cpu().numpy() for o in out)
+    return tuple(out) if on_dev else tuple(o.cpu().numpy() for o in out)
 
 
 def smoothing_to_kernel_inputs(smoothing, n_queries: int):
@@ -166,16 +229,32 @@ def smoothing_to_kernel_inputs(smoothing, n_queries: int):
     return d / det, -b / det, a / det, radius
 
 
+def _grid_queries(out_size, ref_size, device):
+    """lpa.py:393-396 meshgrid of the output pixel centres, built on the device."""
+    xs, ys = grid_coordinates(out_size, ref_size or out_size)
+    tx = torch.from_numpy(np.ascontiguousarray(xs)).to(device)
+    ty = torch.from_numpy(np.ascontiguousarray(ys)).to(device)
+    qy, qx = torch.meshgrid(ty, tx, indexing="ij")
+    return qx.reshape(-1), qy.reshape(-1)
+
+
+def reconstruct_channel_device(samples: RadianceSamples, out_size, params, channel,
+                               ref_size=None, steering=None):
+    """(value, gx, gy) (out_h, out_w) float64 device tensors of one channel."""
+    out_w, out_h = out_size
+    index = samples.index(channel)
+    qx, qy = _grid_queries(out_size, ref_size, index.device)
+    val, gx, gy = evaluate_index(index, qx, qy, params.order, params.channel_scale(channel),
+                                 params.resolved_max_radius(), params.cond_threshold,
+                                 params.weight_mode, steering)
+    return val.reshape(out_h, out_w), gx.reshape(out_h, out_w), gy.reshape(out_h, out_w)
+
+
 def reconstruct_channel_samples(samples: RadianceSamples, out_size, params, channel,
                                 ref_size=None, steering=None):
-    """reconstruct_channel on scattered samples (lpa.py:379-408)."""
-    out_w, out_h = out_size
-    xs, ys = grid_coordinates(out_size, ref_size or out_size)
-    qx, qy = np.meshgrid(xs, ys)
-    val, gx, gy = evaluate_index(samples.index(channel), qx, qy, params.order,
-                                 params.channel_scale(channel), params.resolved_max_radius(),
-                                 params.cond_threshold, params.weight_mode, steering)
-    return val.reshape(out_h, out_w), gx.reshape(out_h, out_w), gy.reshape(out_h, out_w)
+    """reconstruct_channel on scattered samples (lpa.py:379-408): numpy planes."""
+    return tuple(t.cpu().numpy() for t in reconstruct_channel_device(
+        samples, out_size, params, channel, ref_size, steering))
 
 
 class LocalPolynomialRegressor(BaseEstimator, RegressorMixin):

@@ -145,3 +145,18 @@ def test_gpu_scattered_path_reproduces_reference_pin9_sha(cuda):
     s = hl.RadianceSamples(*oracle.frames_to_samples(frames, cfgs, cals))
     img = hl.reconstruct_frame(s, out_size, params)
     assert hashlib.sha256(img.data.tobytes()).hexdigest() == manifest()["pin9_sha256_reference_test"]
+
+
+def test_device_materialized_samples_reproduce_reference_pin9_sha(cuda):
+    """End to end on the GPU: raw frames -> hdr_sample_planes (float64
+    radiometry) -> device compaction -> GPU SampleIndex -> CSR kernel gives
+    the reference's pinned golden SHA-256 bit for bit."""
+    import hashlib
+
+    from golden_cases import manifest
+
+    frames, cfgs, cals, out_size, params, ref_size, case, arrays = load("pin9_rotation_256x192_o1")
+    s = hl.frames_to_samples(frames, cfgs, cals).materialize()
+    assert s.on_device
+    img = hl.reconstruct_frame(s, out_size, params)
+    assert hashlib.sha256(img.data.tobytes()).hexdigest() == manifest()["pin9_sha256_reference_test"]
