@@ -49,6 +49,14 @@ WORKLOADS = {
     "cfg5": dict(rig="misaligned", order=2, J=4, out=(W_IN, H_IN), size=(W_IN, H_IN), sensors=4,
                  desc="4-sensor 4-Mpixel HDR video (exposures 1, 2^-4, 2^-8, 2^-12), misaligned, "
                       "adaptive order-2 LPA, ICI J=4; one step = one video frame"),
+    # SURVEY.md s8(f) rows, measured on the cfg2 frames
+    "calpa": dict(kind="calpa", rig="aligned", order=1, J=1, out=(W_IN, H_IN), size=(W_IN, H_IN),
+                  desc="CALPA (steering.py:214-248) on cfg2 frames: isotropic order-1 G pass, "
+                       "steering field, steered RGB pass"),
+    "samples": dict(kind="samples", rig="aligned", order=1, J=1, out=(W_IN, H_IN),
+                    size=(W_IN, H_IN),
+                    desc="scattered-sample mode on cfg2 frames: frames_to_samples + SampleIndex "
+                         "+ lpa_evaluate (CSR kernel), order 1"),
 }
 
 # algorithmic FLOP per inside-window sample per scale:
@@ -133,7 +141,8 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml"}
 
 
-REF_BAND_ROWS = {"cfg1": None, "cfg2": 200, "cfg3": 24, "cfg4": 24, "cfg5": 16}
+REF_BAND_ROWS = {"cfg1": None, "cfg2": 200, "cfg3": 24, "cfg4": 24, "cfg5": 16, "calpa": None,
+                 "samples": 200}
 _SIM_CACHE = {}
 
 
@@ -176,6 +185,161 @@ def cpu_reference_frame_seconds(wl, threads, band_rows=None, seed=123):
     return dt, frac, desc
 
 
+def _calpa_params():
+    import paper_1308_4908_b200 as hl
+
+    return hl.AdaptiveParams(base=hl.ReconstructionParams(order=1, scale=0.7))
+
+
+def cpu_calpa_frame_seconds(wl, threads, seed=123):
+    """The oracle's CALPA (restating steering.py:214-248 over lpa_evaluate's
+    two-phase mode) on one full frame."""
+    from oracle import oracle
+    from paper_1308_4908_b200 import simulate as sim
+
+    W, H = wl["size"]
+    key = (wl["rig"], W, H, seed, 3)
+    if key not in _SIM_CACHE:
+        rig = sim.baseline_rig(wl["rig"], W, H, seed=seed)
+        _SIM_CACHE[key] = (rig, sim.simulate_rig(sim.hdr_chart(W, H), rig))
+    rig, frames = _SIM_CACHE[key]
+    t0 = time.perf_counter()
+    oracle.calpa(frames, rig.sensors, rig.calibrations(), wl["out"], _calpa_params(),
+                 threads=threads)
+    dt = time.perf_counter() - t0
+    return dt, 1.0, f"full frame of {wl['desc']}, {threads} threads"
+
+
+def run_next(args, wl, world, rank, local):
+    """SURVEY.md s8(f) workloads (calpa, samples): device time per frame
+    (CUDA events), the dominant kernel's FP64 roofline, end to end through the
+    public API (host frames in, host image out) and the CPU oracle beside it."""
+    import torch
+
+    import paper_1308_4908_b200 as hl
+    from paper_1308_4908_b200 import _native as N
+    from paper_1308_4908_b200 import simulate as sim
+    from paper_1308_4908_b200.engine import DeviceRig
+    from paper_1308_4908_b200.samples import RadianceSamples, reconstruct_channel_device
+    from paper_1308_4908_b200.steering import (auto_gradient_scale, compute_steering_field,
+                                               gradient_field)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W, H = wl["size"]
+    out_size = wl["out"]
+    rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0)
+    cals = rigspec.calibrations()
+    frame_sets = [sim.simulate_rig_torch(sim.hdr_chart(W, H), rigspec, dev, seed=1000 * rank + i)
+                  for i in range(N_DISTINCT)]
+    rigs = [DeviceRig.from_device(fs, rigspec.sensors, cals) for fs in frame_sets]
+    params = _params(wl)
+    ap = _calpa_params()
+    stream = torch.cuda.current_stream(dev)
+    kind = wl["kind"]
+    kern = {}  # events around the dominant kernel's launches
+
+    def step(i):
+        rig = rigs[i % N_DISTINCT]
+        if kind == "calpa":
+            val, gx, gy = gradient_field(rig, out_size, ap.base, hl.ColorChannel.G)
+            fld = compute_steering_field((gx, gy), ap, auto_gradient_scale(val))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = rig.reconstruct_steered(out_size, ap.base, (fld.theta, fld.sigma, fld.gamma),
+                                          want_work=True)
+            e1.record(stream)
+            kern.setdefault("ev", []).append((e0, e1))
+            kern["work"] = out["work"]
+        else:
+            s = RadianceSamples(*rig.materialize_samples())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for ch in hl.ColorChannel:
+                s.index(ch)
+            e0.record(stream)
+            for ch in hl.ColorChannel:
+                reconstruct_channel_device(s, out_size, params, ch)
+            e1.record(stream)
+            kern.setdefault("ev", []).append((e0, e1))
+
+    for i in range(args.warmup):
+        step(i)
+    kern.clear()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        n0 = N.lib().hdr_lpa_launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        n_launches = int(N.lib().hdr_lpa_launch_count() - n0)
+    ms = e0.elapsed_time(e1)
+    ms_kernel = float(np.mean([a.elapsed_time(b) for a, b in kern["ev"]]))
+    fps = args.steps / (ms / 1e3)
+    # algorithmic work of the dominant kernel
+    if kind == "calpa":
+        n_inside = float(kern["work"].to(torch.int64).sum().item())
+        kname = "lpa_steered_kernel"
+    else:  # same windows and samples as the raw-frame path: its work plane counts them
+        n_inside = float(rigs[0].reconstruct(out_size, params, want_work=True)["work"]
+                         .to(torch.int64).sum().item())
+        kname = "lpa_samples_kernel"
+    flop64 = n_inside * FLOP64_PER_SAMPLE[1]
+    peak64 = ctypes_probe(N, stream)
+    achieved = flop64 / (ms_kernel * 1e-3)
+    # end to end through the public API: pinned host frames -> device -> host image
+    host_sets = [[t.cpu().pin_memory() for t in fs] for fs in frame_sets]
+    raw_dev = [torch.empty_like(t) for t in frame_sets[0]]
+    erig = DeviceRig.from_device(raw_dev, rigspec.sensors, cals)
+    nrep = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(nrep):
+        for d, h in zip(raw_dev, host_sets[i % N_DISTINCT]):
+            d.copy_(h, non_blocking=True)
+        if kind == "calpa":
+            img = hl.calpa_reconstruct(erig, out_size, ap)
+        else:
+            img = hl.reconstruct_frame(RadianceSamples(*erig.materialize_samples()), out_size,
+                                       params)
+    e2e_s = (time.perf_counter() - t0) / nrep
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+
+        thr = oracle.max_threads()
+        if kind == "calpa":
+            dt, frac, desc = cpu_calpa_frame_seconds(wl, thr)
+        else:
+            dt, frac, desc = cpu_reference_frame_seconds(wl, thr, band_rows=REF_BAND_ROWS["samples"])
+        cpu = {"value": frac / dt, "unit": "frames/s", "cores": thr, "kind": "port",
+               "sample": desc}
+    if rank == 0:
+        line = {
+            "metric": "HDR frames/s", "value": fps, "unit": "frames/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "in": [W, H],
+                       "out": list(out_size), "sensors": 3,
+                       "l2": f"inputs larger than L2: {N_DISTINCT} distinct frames cycled"},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak64 / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak64, "traffic": None,
+                         "kernel": kname, "kernel_ms": ms_kernel,
+                         "inside_samples_per_launch": n_inside, "flop64_per_launch": flop64},
+            "cpu_baseline": cpu,
+            "e2e": {"value": 1.0 / e2e_s, "unit": "frames/s",
+                    "h2d_bytes_per_step": sum(t.numel() * 2 for t in frame_sets[0]),
+                    "d2h_bytes_per_step": out_size[0] * out_size[1] * 12,
+                    "note": "host wall clock around the synchronous public API call"},
+            "gpu_launches": n_launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def run_reference(args, wl, world, rank):
     if rank != 0:
         return
@@ -185,7 +349,11 @@ def run_reference(args, wl, world, rank):
     band = REF_BAND_ROWS[args.workload]
     times = []
     for i in range(args.warmup + args.steps):
-        dt, frac, desc = cpu_reference_frame_seconds(wl, threads, band_rows=band, seed=100 + i % 2)
+        if wl.get("kind") == "calpa":
+            dt, frac, desc = cpu_calpa_frame_seconds(wl, threads, seed=100 + i % 2)
+        else:
+            dt, frac, desc = cpu_reference_frame_seconds(wl, threads, band_rows=band,
+                                                         seed=100 + i % 2)
         if i >= args.warmup:
             times.append(dt / frac)
     sec = float(np.mean(times))
@@ -425,6 +593,8 @@ def main():
     world, rank, local = _dist_init()
     if args.impl == "reference":
         run_reference(args, wl, world, rank)
+    elif wl.get("kind") in ("calpa", "samples"):
+        run_next(args, wl, world, rank, local)
     else:
         run_ours(args, wl, world, rank, local)
 

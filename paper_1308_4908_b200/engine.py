@@ -245,7 +245,7 @@ class DeviceRig:
 
     def reconstruct_steered(self, out_size, params: ReconstructionParams, field, ref_size=None,
                             rows=None, out=None, want_outcome=False, raw_value=False,
-                            stream=None):
+                            want_work=False, stream=None):
         """CALPA second pass with a steering field (theta, sigma, gamma float64
         device tensors over the output grid): hdr_lpa_reconstruct_steered."""
         out_w, out_h = int(out_size[0]), int(out_size[1])
@@ -253,7 +253,7 @@ class DeviceRig:
             ref_size = (out_w, out_h)
         if out is None:
             out = self.allocate_outputs((out_w, out_h), want_outcome=want_outcome,
-                                        raw_value=raw_value)
+                                        raw_value=raw_value, want_work=want_work)
         th, sg, gm = (t.contiguous() for t in field)
         for t in (th, sg, gm):
             if t.dtype != torch.float64 or tuple(t.shape) != (out_h, out_w) or t.device != self.device:
@@ -263,6 +263,7 @@ class DeviceRig:
         o.rgb = out["rgb"].data_ptr()
         o.outcome = out["outcome"].data_ptr() if "outcome" in out else None
         o.value = out["value"].data_ptr() if "value" in out else None
+        o.work = out["work"].data_ptr() if "work" in out else None
         ws = self.workspace(out_w, out_h)
         r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
