@@ -934,7 +934,77 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
     acc.sabs = sabs;
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT>
+// ---------------------------------------------------------------------------
+// CALPA steered pass, fast path (lpa_evaluate two_phase, _kernels.py:257-300):
+// the phase-0 step-0 fit (anisotropic window of the steering field at
+// r = min(r0, max_radius)) from the staged planes with fp32 weights; any
+// other outcome, and fits failing fit_precise, go to lpa_steered_slow_kernel.
+// ---------------------------------------------------------------------------
+// Per-pixel kernel inputs (SteeringField.kernel_inputs, steering.py:80-107),
+// float64 in the reference's operation order; an = (h11, h12, h22, r0).
+__device__ __forceinline__ void steer_inputs(const DevParams &P, int pix, int c, double *an) {
+    const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
+    const double ct = cos(th), st = sin(th);
+    const double h = P.h[c][0];  // channel scale
+    const double c11 = g * (s * ct * ct + st * st / s);
+    const double c12 = g * (ct * st) * (1.0 / s - s);
+    const double c22 = g * (s * st * st + ct * ct / s);
+    an[0] = c11 / h;
+    an[1] = c12 / h;
+    an[2] = c22 / h;
+    an[3] = 3.0 * sqrt(h * s / g);
+}
+
+// Row-factored moments with the anisotropic window
+// W = exp(-(h11 dx^2 + 2 h12 dx dy + h22 dy^2)) (_kernels.py:164-168): along a
+// row dy is constant, so q = h11 dx^2 + (2 h12 dy) dx + h22 dy^2.
+template <int ORDER>
+struct RowAniso {
+    static constexpr int PN = NC<ORDER>::P;
+    RowMoments<ORDER> m;
+    float h11, h12x2, h22;  // pre-scaled by log2(e)
+    float a, b;             // per row: h22 dy^2, 2 h12 dy
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        m.begin_row(dy, dyy);
+        a = h22 * (float)dyy;
+        b = h12x2 * (float)dy;
+    }
+    __device__ __forceinline__ void end_row(double dy, double dyy) { m.end_row(dy, dyy); }
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
+                                           double dxx, double dyy, float) {
+        const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
+        // RowMoments' weight is ex2(-hl * d2f) * iv: feed it q2 with hl = 1
+        m.sample(ok, v, iv, dx, dy, dxx, dyy, q2);
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float) {
+        const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+        m.general(ok, v, iv, dx, dy, dxx, dyy, q2);
+    }
+};
+
+template <int ORDER, class Sweep>
+__device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, const double *an,
+                                                 double r, double r2, Acc<NC<ORDER>::P> &acc) {
+    constexpr float L2E = 1.4426950408889634f;
+    acc.zero();
+    const float h11 = (float)an[0] * L2E, h12x2 = 2.f * (float)an[1] * L2E, h22 = (float)an[2] * L2E;
+    if constexpr (ORDER >= 1) {
+        RowAniso<ORDER> pol{RowMoments<ORDER>{acc, 1.0f}, h11, h12x2, h22, 0.f, 0.f};
+        sweep.rows(c, -1, r, r2, pol);
+    } else {
+        sweep(c, -1, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
+                                double dyy, float) {
+            const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+            const float w = ok ? ex2_approx(-q2) * iv : 0.f;
+            const double y = ok ? v : 0.0;
+            acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+            acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+        });
+    }
+}
+
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT, bool STEER>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int t,
                                              const int (*org)[2], bool tile_covered) {
@@ -965,7 +1035,24 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         R.sidx = 0;
         int st = FIT_AMBIG;
         if (covered) {
-            if constexpr (ICI) {
+            if constexpr (STEER) {
+                double an[4];
+                steer_inputs(P, pix, c, an);
+                const double r = fmin(an[3], P.max_radius);
+                Acc<PN> acc;
+                accumulate_aniso<ORDER>(sweep, c, an, r, __dmul_rn(r, r), acc);
+                R.work = acc.count;
+                Fit fit;
+                st = solve_fast<PN>(acc, P.cond, fit);
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, r, P.prec_floor)) st = FIT_AMBIG;
+                if (st == FIT_OK) {
+                    R.count = acc.count;
+                    R.val = fit.c0;
+                    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                    R.gy = ORDER >= 1 ? fit.c2 : qnan();
+                    R.outcome = ORDER * 16;  // phase 0 (anisotropic), radius step 0
+                }
+            } else if constexpr (ICI) {
                 st = ici<ORDER, false>(P, c, sweep, R);
             } else {
                 Acc<PN> acc;
@@ -1017,7 +1104,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #ifndef HDR_PAT_MINBLOCKS
 #define HDR_PAT_MINBLOCKS 3
 #endif
-template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false>
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false, bool STEER = false>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
@@ -1065,7 +1152,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
-        tile_compute<ORDER, ICI, MAXC, PAT, RT>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
         const int tn = t + NBUF * (int)gridDim.x;
         if (tn < ntiles) {  // CTA-uniform
             __syncwarp();
@@ -1291,6 +1378,35 @@ __global__ void __launch_bounds__(128) lpa_steered_kernel(const __grid_constant_
             R.count = 0;
         }
         if ((threadIdx.x & 31) == 0) write_result(P, pix, c, R);
+    }
+}
+
+// The steered pass's exact evaluation of the fast path's work items (all
+// outcomes other than a sound phase-0 step-0 fit), one 8-lane group per item.
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_steered_slow_kernel(const __grid_constant__ DevParams P) {
+    constexpr int G = SLOW_LANES;
+    const uint32_t n = *P.work_count;
+    const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t ngrp = (gridDim.x * blockDim.x) / G;
+    for (uint32_t i = grp; i < n; i += ngrp) {
+        const uint32_t item = P.work_items[i];
+        const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
+        const int ox = pix % P.out_w, oy = pix / P.out_w;
+        const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        double an[4];
+        steer_inputs(P, pix, c, an);
+        PixelResult R;
+        R.sidx = 0;
+        bool ok = steered_order<ORDER>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 1) ok = steered_order<(ORDER >= 1 ? ORDER - 1 : 0)>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 2) ok = steered_order<0>(P, c, sweep, an, R);
+        if (!ok) {
+            R.val = R.gx = R.gy = qnan();
+            R.outcome = HDR_OUTCOME_NAN;
+            R.count = 0;
+        }
+        if ((threadIdx.x & (G - 1)) == 0) write_result(P, pix, c, R);
     }
 }
 
@@ -1619,10 +1735,10 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT = false, bool RT = false>
+template <int ORDER, bool ICI, int MAXC, bool PAT = false, bool RT = false, bool STEER = false>
 static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
-    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT>;
+    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -1633,9 +1749,9 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
     COUNT_LAUNCH();
     if constexpr (PAT || RT)
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT><<<grid, NT, smem_bytes, st>>>(P, T);
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, T);
     else
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_fast_kernel launch");
 }
 
@@ -2029,22 +2145,16 @@ static int launch_prepass(const DevParams &P, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("radiance_phase_kernel launch");
 }
 
-int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
-                        int out_w, int out_h, double ref_w, double ref_h, int row_begin,
-                        int row_end, const HdrOutputs *out, void *workspace,
-                        size_t workspace_bytes, void *stream) {
-    DevParams P;
-    double fastR = 0.0;
-    {
-        const int rc = setup_params(sensors, n_sensors, params, out_w, out_h, ref_w, ref_h,
-                                    row_begin, row_end, out, workspace, workspace_bytes, P, fastR);
-        if (rc != HDR_OK) return rc;
-    }
+// Staged-region geometry, shared-memory layout, tap tables (when allowed) and
+// TMA descriptors of the fast kernels, for windows up to radius fastR.
+static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_taps, TapParam &T,
+                         int &smem_bytes, int &maxc) {
     // Staged region per sensor: tile extent in sensor space + 2 x window
     // half-width (+ rounding/alignment slack).  Shared memory: pre-computed
     // taps, then two plane buffers, each holding per sensor the four staged
     // (f_hat, 1/den) phase planes and the f64 coordinate tables.
-    int smem = 0, maxc = 1;
+    int smem = 0;
+    maxc = 1;
     auto take = [&](int bytes) {
         const int off = smem;
         smem += (bytes + 64 + 127) & ~127;  // 128-B aligned (TMA destinations) + read slack
@@ -2066,8 +2176,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         maxc = max(maxc, (int)floor(fastR * d.nrow0) + 2);
     }
     std::vector<Tap> taps;
-    static thread_local TapParam T;  // kernel-parameter image of the tap table
-    P.pat = build_taps(P, taps) ? 1 : 0;
+    P.pat = allow_taps && build_taps(P, taps) ? 1 : 0;
     if (P.pat) {
         P.off_taps = take((int)(taps.size() * sizeof(Tap)));
         // SoA layout (TapXY[n], TapW[n]) in the kernel parameter
@@ -2081,7 +2190,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
             w[i].off = taps[i].delta * (int)sizeof(float2);
         }
         P.tab_bytes = (int)(n * sizeof(Tap));
-    } else {
+    } else if (allow_taps) {
         P.rt = build_rowtaps(P, T) ? 1 : 0;
         if (P.rt) P.off_taps = take(P.tab_bytes);
     }
@@ -2096,7 +2205,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         d.off_ty4 = take(d.rh * 8);
     }
     P.buf_stride = smem;
-    const int smem_bytes = P.plane_base + NBUF * P.buf_stride;
+    smem_bytes = P.plane_base + NBUF * P.buf_stride;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
     for (int s = 0; s < n_sensors; ++s)
         if (!encode_phase_map(P.s[s], &P.tmap[s])) {
@@ -2104,6 +2213,26 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
             return HDR_ERR_CUDA;
         }
 
+    return HDR_OK;
+}
+
+int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams *params,
+                        int out_w, int out_h, double ref_w, double ref_h, int row_begin,
+                        int row_end, const HdrOutputs *out, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+    DevParams P;
+    double fastR = 0.0;
+    {
+        const int rc = setup_params(sensors, n_sensors, params, out_w, out_h, ref_w, ref_h,
+                                    row_begin, row_end, out, workspace, workspace_bytes, P, fastR);
+        if (rc != HDR_OK) return rc;
+    }
+    static thread_local TapParam T;  // kernel-parameter image of the tap table
+    int smem_bytes = 0, maxc = 1;
+    {
+        const int rc = setup_staging(P, n_sensors, fastR, true, T, smem_bytes, maxc);
+        if (rc != HDR_OK) return rc;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     P.tiles_y = (row_end - row_begin + TH - 1) / TH;
     P.tiles_x = (out_w + TW - 1) / TW;
@@ -2136,10 +2265,40 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     P.st_sigma = steering->sigma;
     P.st_gamma = steering->gamma;
     cudaStream_t st = (cudaStream_t)stream;
+    // fast path: tiles staged for the largest steered radius (max_radius)
+    static thread_local TapParam T;
+    int smem_bytes = 0, maxc = 1;
+    P.fast_R = P.max_radius;
+    const bool staged =
+        setup_staging(P, n_sensors, P.max_radius, false, T, smem_bytes, maxc) == HDR_OK;
+    if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess)
+        return cuda_fail("cudaMemsetAsync");
     if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (staged) {
+        P.tiles_y = (P.row_end - P.row_begin + TH - 1) / TH;
+        P.tiles_x = (out_w + TW - 1) / TW;
+        const int tiles = P.tiles_x * P.tiles_y;
+        int rc2;
+        switch (P.order) {
+            case 0: rc2 = launch_fast<0, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
+            case 1: rc2 = launch_fast<1, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
+            default: rc2 = launch_fast<2, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
+        }
+        if (rc2 != HDR_OK) return rc2;
+        if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;
+        const int grid = nsm * 4;
+        switch (P.order) {
+            case 0: COUNT_LAUNCH(); lpa_steered_slow_kernel<0><<<grid, 128, 0, st>>>(P); break;
+            case 1: COUNT_LAUNCH(); lpa_steered_slow_kernel<1><<<grid, 128, 0, st>>>(P); break;
+            default: COUNT_LAUNCH(); lpa_steered_slow_kernel<2><<<grid, 128, 0, st>>>(P); break;
+        }
+        return cudaPeekAtLastError() == cudaSuccess ? HDR_OK
+                                                    : cuda_fail("lpa_steered_slow_kernel launch");
+    }
+    // windows too large to stage: every pixel-channel through the exact kernel
     const int grid = nsm * 8;
     switch (P.order) {
         case 0: COUNT_LAUNCH(); lpa_steered_kernel<0><<<grid, 128, 0, st>>>(P); break;
