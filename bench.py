@@ -288,6 +288,10 @@ def run_next(args, wl, world, rank, local):
         kname = "lpa_samples_kernel"
     flop64 = n_inside * FLOP64_PER_SAMPLE[1]
     peak64 = ctypes_probe(N, stream)
+    traffic = None
+    tpath = ROOT / "profiles" / "r01_traffic.json"
+    if tpath.exists():
+        traffic = (json.loads(tpath.read_text()).get(args.workload) or {}).get("traffic_bytes")
     achieved = flop64 / (ms_kernel * 1e-3)
     # end to end through the public API: pinned host frames -> device -> host image
     host_sets = [[t.cpu().pin_memory() for t in fs] for fs in frame_sets]
@@ -326,7 +330,7 @@ def run_next(args, wl, world, rank, local):
                        "out": list(out_size), "sensors": 3,
                        "l2": f"inputs larger than L2: {N_DISTINCT} distinct frames cycled"},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak64 / 1e12,
-                         "unit": "TFLOP/s", "frac": achieved / peak64, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak64, "traffic": traffic,
                          "kernel": kname, "kernel_ms": ms_kernel,
                          "inside_samples_per_launch": n_inside, "flop64_per_launch": flop64},
             "cpu_baseline": cpu,
