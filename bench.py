@@ -477,6 +477,7 @@ def run_ours(args, wl, world, rank, local):
     flop64 = n_inside * per64
     flop32 = n_inside * FLOP32_PER_SAMPLE[p]
     peak64 = ctypes_probe(N, stream)
+    fp32_peak = 148 * 128 * 2 * (clk["sm_max_mhz"] or 1965.0) * 1e6
     if p == 0:
         achieved = flop32 / (ms_fast * 1e-3)
         bound, peak, peak_src = "fp32", 148 * 128 * 2 * (clk["sm_max_mhz"] or 1965.0) * 1e6, \
@@ -557,6 +558,11 @@ def run_ours(args, wl, world, rank, local):
                          "peak_source": peak_src, "kernel": "lpa_fast_kernel",
                          "kernel_ms": ms_fast, "inside_samples_per_launch": n_inside,
                          "flop64_per_launch": flop64, "flop32_per_launch": flop32,
+                         "fp32": {"achieved_tflops": flop32 / (ms_fast * 1e-3) / 1e12,
+                                  "peak_tflops": fp32_peak / 1e12,
+                                  "frac": flop32 / (ms_fast * 1e-3) / fp32_peak,
+                                  "peak_source": "nominal 148 SM x 128 FFMA lanes x 2 x "
+                                                 "max SM clock"},
                          "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": peaks["hbm_gbs"],
                                  "frac": hbm_achieved / peaks["hbm_gbs"],
                                  "algorithmic_bytes": planes_bytes + out_bytes,
