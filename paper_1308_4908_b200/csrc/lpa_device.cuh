@@ -463,6 +463,16 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         const double C11 = fma(a, f, -cc * cc), C12 = fma(b, cc, -a * e), C22 = fma(a, d, -b * b);
         const double det = fma(a, C00, fma(b, C01, cc * C02));
         if (!(a > 0.0) || !(C22 > 0.0) || !(det > 0.0)) return FIT_FAIL;
+        // The cofactors are differences of products: near-singular windows
+        // (e.g. coincident samples of identical sensors at a frame corner) leave
+        // them at rounding-noise level, where their ratios are meaningless.  A
+        // window with cond <= 1e8 keeps every principal minor >= 1e-8 of the
+        // product of its diagonal (interlacing) and det >= ~1e-8 of its terms,
+        // so anything below 1e-10 is decided by the exact path.
+        constexpr double kRel = 1e-10;
+        if (!(C00 > kRel * d * f) || !(C11 > kRel * a * f) || !(C22 > kRel * a * d) ||
+            !(det > kRel * (fabs(a * C00) + fabs(b * C01) + fabs(cc * C02))))
+            return FIT_AMBIG;
         const double rd = 1.0 / det;
         const double b0 = acc.b[0], b1 = acc.b[1], b2 = acc.b[2];
         fit.c0 = fma(C00, b0, fma(C01, b1, C02 * b2)) * rd;
@@ -473,6 +483,7 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         fit.g[2] = C02 * rd;
         const double cu = (a + d + f) * ((C00 + C11 + C22) * rd);
         const double cl = fmax(a, fmax(d, f)) * (fmax(C00, fmax(C11, C22)) * rd);
+        if (!(cu >= 9.0 * (1.0 - 1e-6))) return FIT_AMBIG;  // tr A tr A^-1 >= p^2 always
         const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
         if (cu <= cond * (1.0 - margin)) return FIT_OK;
         if (cl >= cond * (1.0 + margin)) return FIT_FAIL;

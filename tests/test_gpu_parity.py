@@ -248,3 +248,16 @@ def test_cuda_graph_replay_matches_eager(cuda):
         ref = DeviceRig.from_device(src, cfgs, cals).reconstruct((96, 64), p)["rgb"]
         torch.cuda.synchronize()
         assert torch.equal(torch.nan_to_num(got, nan=-1.0), torch.nan_to_num(ref, nan=-1.0))
+
+
+def test_aligned_coincident_samples_at_corner(cuda):
+    """Identical (aligned) sensors put the B samples of pixel (0, 0) at one
+    position: a rank-1 window the reference rejects (radius step 1).  The fast
+    path must not accept it from rounding-noise cofactors."""
+    gt = sim.hdr_chart(96, 64)
+    rig = sim.baseline_rig("aligned", 96, 64, seed=7)
+    frames = sim.simulate_rig(gt, rig)
+    p = hl.ReconstructionParams(order=1, scale=0.7)
+    got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), (96, 64), p)
+    assert ref["outcome"][2, 0, 0] == 17  # order 1, radius step 1
+    _check(got, ref)
