@@ -52,6 +52,7 @@ static_assert(sizeof(DevParams) + TAP_PARAM_BYTES <= 32764, "kernel parameter sp
 #endif
 constexpr int NBUF = HDR_NBUF;
 static const size_t LUT_BYTES = 65536 * sizeof(double2);
+static const size_t RT_TABLE_BYTES = 64 * 1024;  // row-tap table (workspace, then shared memory)
 
 template <int ORDER>
 struct NC {
@@ -182,13 +183,18 @@ struct TileSweep {
     template <class Pol>
     __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol) const {
         const DevSensor &S = P.s[s];
-        const int cls = ((py & 1) << 1) | (px & 1);
-        const int r0 = P.pat_off[s][c][cls], nr = P.rt_nrow[s][c][cls];
-        const TapRow *rows = (const TapRow *)rt;
-        const RowTap *taps = (const RowTap *)(rt + (size_t)P.n_taps * sizeof(TapRow));
+        const int pm = P.rt_period - 1;
+        const int cls = (py & pm) * P.rt_period + (px & pm);
+        const RtHeader &hd = *(const RtHeader *)rt;
+        const int r0 = hd.row0[s][c][cls], nr = hd.nrow[s][c][cls];
+        const TapRow *rows = (const TapRow *)(rt + sizeof(RtHeader));
+        const RowTap *taps =
+            (const RowTap *)(rt + sizeof(RtHeader) + (size_t)hd.n_rows * sizeof(TapRow));
         const int pw = S.rw >> 1;
+        // the pixel's anchor: its own sensor pixel (sx = 1) or cell (sx = 1/2)
+        const int ax = px >> P.rt_shift, ay = py >> P.rt_shift;
         const unsigned char *vb = sm + S.off_vi +
-                                  8 * (((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+                                  8 * (((ay - org[s][1]) >> 1) * pw + ((ax - org[s][0]) >> 1));
         for (int ri = r0; ri < r0 + nr; ++ri) {
             const TapRow &R = rows[ri];
             const int lo = R.lo[k], hi = R.hi[k];
@@ -1110,7 +1116,7 @@ template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false, bool STEER =
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
-                    typename std::conditional<PAT || RT, TapParam, NoTaps>::type T) {
+                    typename std::conditional<PAT, TapParam, NoTaps>::type T) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];
@@ -1119,11 +1125,16 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
     unsigned char *planes = smem + P.plane_base;
-    if constexpr (PAT || RT) {  // the kernel-parameter table into shared memory
+    if constexpr (PAT) {  // the kernel-parameter tap table into shared memory
         const uint4 *src = (const uint4 *)T.bytes;
         uint4 *dst = (uint4 *)(smem + P.off_taps);
         const int n16 = (P.tab_bytes + 15) / 16;
         for (int i = threadIdx.x; i < n16; i += NT) dst[i] = src[i];
+    } else if constexpr (RT) {  // the row-tap table from the workspace
+        const uint4 *src = (const uint4 *)P.rt_global;
+        uint4 *dst = (uint4 *)(smem + P.off_taps);
+        const int n16 = (P.tab_bytes + 15) / 16;
+        for (int i = threadIdx.x; i < n16; i += NT) dst[i] = __ldg(src + i);
     }
     int t = blockIdx.x;
     if (threadIdx.x == 0) {
@@ -1748,7 +1759,7 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
         return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
     COUNT_LAUNCH();
-    if constexpr (PAT || RT)
+    if constexpr (PAT)
         lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, T);
     else
         lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
@@ -1831,8 +1842,15 @@ static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem
 // column order; d2 is convex along a row, so each scale's members are one run
 // [lo[k], hi[k]).  Any tap within 1e-9 r_k^2 of any scale's support boundary
 // disables the mode (the per-pixel rounding could flip membership there).
-static bool build_rowtaps(DevParams &P, TapParam &T) {
-    if (P.sx != 1.0 || P.sy != 1.0) return false;
+static bool build_rowtaps(DevParams &P, std::vector<unsigned char> &table) {
+    int shift;
+    if (P.sx == 1.0 && P.sy == 1.0)
+        shift = 0;
+    else if (P.sx == 0.5 && P.sy == 0.5)
+        shift = 1;  // 2x output grid: classes repeat every 4 output pixels
+    else
+        return false;
+    const int period = 2 << shift;
     bool any = false;
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
@@ -1843,6 +1861,8 @@ static bool build_rowtaps(DevParams &P, TapParam &T) {
         any = true;
     }
     if (!any) return false;
+    RtHeader hd;
+    memset(&hd, 0, sizeof(hd));
     std::vector<TapRow> rows;
     std::vector<RowTap> taps;
     for (int s = 0; s < P.n_sensors; ++s) {
@@ -1859,19 +1879,22 @@ static bool build_rowtaps(DevParams &P, TapParam &T) {
                 rmax2 = fmax(rmax2, P.r2[c][k]);
                 rmax = fmax(rmax, P.r[c][k]);
             }
-            const int R = (int)ceil(rmax + fabs(S.T[2]) + fabs(S.T[5])) + 1;
-            for (int cl = 0; cl < 4; ++cl) {
-                const int j = 64 + (cl & 1), i = 64 + (cl >> 1);  // representative pixel
-                const double qx = (double)j, qy = (double)i;      // qcoord(j, 1.0) == j
-                P.pat_off[s][c][cl] = (int)rows.size();
+            const int R = (int)ceil(rmax + fabs(S.T[2]) + fabs(S.T[5])) + 2;
+            for (int cl = 0; cl < period * period; ++cl) {
+                // representative output pixel of the class and its anchor
+                const int j = 128 + cl % period, i = 128 + cl / period;
+                const double qx = ((double)j + 0.5) * P.sx + -0.5;  // qcoord (lpa.py:222-223)
+                const double qy = ((double)i + 0.5) * P.sy + -0.5;
+                const int ax = j >> shift, ay = i >> shift;
+                hd.row0[s][c][cl] = (int)rows.size();
                 for (int m = -R; m <= R; ++m) {
-                    const int y = i + m;
+                    const int y = ay + m;
                     TapRow row;
                     memset(&row, 0, sizeof(row));
                     row.first = (int)taps.size();
                     std::vector<double> d2s;
                     for (int k2 = -R; k2 <= R; ++k2) {
-                        const int x = j + k2;
+                        const int x = ax + k2;
                         if (tile[((y & 1) << 1) | (x & 1)] != c) continue;
                         const double X = (1.0 * (double)x + 0.0 * (double)y) + S.T[2];
                         const double Y = (0.0 * (double)x + 1.0 * (double)y) + S.T[5];
@@ -1885,7 +1908,7 @@ static bool build_rowtaps(DevParams &P, TapParam &T) {
                         t.d2f = (float)d2;
                         const int ph = ((y & 1) << 1) | (x & 1);
                         t.off = (int)sizeof(float2) *
-                                (ph * plane + ((y >> 1) - (i >> 1)) * pw + ((x >> 1) - (j >> 1)));
+                                (ph * plane + ((y >> 1) - (ay >> 1)) * pw + ((x >> 1) - (ax >> 1)));
                         taps.push_back(t);
                         d2s.push_back(d2);
                         row.dy = dy;
@@ -1906,17 +1929,49 @@ static bool build_rowtaps(DevParams &P, TapParam &T) {
                     }
                     rows.push_back(row);
                 }
-                P.rt_nrow[s][c][cl] = (int)rows.size() - P.pat_off[s][c][cl];
+                hd.nrow[s][c][cl] = (int)rows.size() - hd.row0[s][c][cl];
             }
         }
     }
-    const size_t bytes = rows.size() * sizeof(TapRow) + taps.size() * sizeof(RowTap);
-    if (bytes > (size_t)TAP_PARAM_BYTES) return false;
-    memcpy(T.bytes, rows.data(), rows.size() * sizeof(TapRow));
-    memcpy(T.bytes + rows.size() * sizeof(TapRow), taps.data(), taps.size() * sizeof(RowTap));
-    P.n_taps = (int)rows.size();  // RT: the taps follow n_taps rows
+    hd.n_rows = (int)rows.size();
+    const size_t bytes =
+        sizeof(RtHeader) + rows.size() * sizeof(TapRow) + taps.size() * sizeof(RowTap);
+    if (bytes > RT_TABLE_BYTES) return false;
+    table.resize(bytes);
+    memcpy(table.data(), &hd, sizeof(hd));
+    memcpy(table.data() + sizeof(hd), rows.data(), rows.size() * sizeof(TapRow));
+    memcpy(table.data() + sizeof(hd) + rows.size() * sizeof(TapRow), taps.data(),
+           taps.size() * sizeof(RowTap));
+    P.rt_period = period;
+    P.rt_shift = shift;
     P.tab_bytes = (int)bytes;
     return true;
+}
+
+// Device copy of a host table without a host->device memcpy (graph-capturable,
+// no host buffer lifetime): the bytes travel in kernel parameters, one chunk
+// per launch.
+struct __align__(16) TableChunk {
+    unsigned char bytes[24576];
+};
+__global__ void table_copy_kernel(const __grid_constant__ TableChunk ch, unsigned char *dst,
+                                  int n) {
+    for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n / 16; i += blockDim.x * gridDim.x)
+        ((uint4 *)dst)[i] = ((const uint4 *)ch.bytes)[i];
+}
+static int upload_table(const std::vector<unsigned char> &table, unsigned char *dst,
+                        cudaStream_t st) {
+    static thread_local TableChunk ch;
+    const size_t n = (table.size() + 15) & ~(size_t)15;
+    for (size_t off = 0; off < n; off += sizeof(ch.bytes)) {
+        const size_t len = std::min(sizeof(ch.bytes), n - off);
+        memset(ch.bytes, 0, sizeof(ch.bytes));
+        memcpy(ch.bytes, table.data() + off, std::min(len, table.size() - off));
+        COUNT_LAUNCH();
+        table_copy_kernel<<<4, 256, 0, st>>>(ch, dst + off, (int)len);
+        if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("table_copy_kernel launch");
+    }
+    return HDR_OK;
 }
 
 static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
@@ -2033,7 +2088,7 @@ int hdr_lpa_workspace_bytes(const HdrSensor *sensors, int n_sensors, int out_w, 
         if (sensors[s].width <= 0 || sensors[s].height <= 0) return HDR_ERR_ARG;
         planes += phase_bytes(sensors[s]);
     }
-    *bytes = WS_HEADER + planes + (size_t)n_sensors * LUT_BYTES +
+    *bytes = WS_HEADER + RT_TABLE_BYTES + planes + (size_t)n_sensors * LUT_BYTES +
              (size_t)out_w * out_h * 3 * sizeof(uint32_t);
     return HDR_OK;
 }
@@ -2108,7 +2163,8 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.work = out->work;
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
-    char *wsp = (char *)workspace + WS_HEADER;
+    P.rt_global = (const unsigned char *)workspace + WS_HEADER;
+    char *wsp = (char *)workspace + WS_HEADER + RT_TABLE_BYTES;
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
         d.phase = (float2 *)wsp;
@@ -2148,7 +2204,7 @@ static int launch_prepass(const DevParams &P, cudaStream_t st) {
 // Staged-region geometry, shared-memory layout, tap tables (when allowed) and
 // TMA descriptors of the fast kernels, for windows up to radius fastR.
 static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_taps, TapParam &T,
-                         int &smem_bytes, int &maxc) {
+                         std::vector<unsigned char> &rt_table, int &smem_bytes, int &maxc) {
     // Staged region per sensor: tile extent in sensor space + 2 x window
     // half-width (+ rounding/alignment slack).  Shared memory: pre-computed
     // taps, then two plane buffers, each holding per sensor the four staged
@@ -2191,7 +2247,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
         }
         P.tab_bytes = (int)(n * sizeof(Tap));
     } else if (allow_taps) {
-        P.rt = build_rowtaps(P, T) ? 1 : 0;
+        P.rt = build_rowtaps(P, rt_table) ? 1 : 0;
         if (P.rt) P.off_taps = take(P.tab_bytes);
     }
     P.plane_base = smem;
@@ -2228,9 +2284,10 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         if (rc != HDR_OK) return rc;
     }
     static thread_local TapParam T;  // kernel-parameter image of the tap table
+    std::vector<unsigned char> rt_table;
     int smem_bytes = 0, maxc = 1;
     {
-        const int rc = setup_staging(P, n_sensors, fastR, true, T, smem_bytes, maxc);
+        const int rc = setup_staging(P, n_sensors, fastR, true, T, rt_table, smem_bytes, maxc);
         if (rc != HDR_OK) return rc;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -2239,6 +2296,8 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     const int tiles = P.tiles_x * P.tiles_y;
     if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
+    if (P.rt && upload_table(rt_table, (unsigned char *)P.rt_global, st) != HDR_OK)
+        return HDR_ERR_CUDA;
     if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;  // per-frame radiometry
     int rc;
     switch (P.order) {
@@ -2267,10 +2326,11 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     cudaStream_t st = (cudaStream_t)stream;
     // fast path: tiles staged for the largest steered radius (max_radius)
     static thread_local TapParam T;
+    std::vector<unsigned char> rt_table;
     int smem_bytes = 0, maxc = 1;
     P.fast_R = P.max_radius;
     const bool staged =
-        setup_staging(P, n_sensors, P.max_radius, false, T, smem_bytes, maxc) == HDR_OK;
+        setup_staging(P, n_sensors, P.max_radius, false, T, rt_table, smem_bytes, maxc) == HDR_OK;
     if (cudaMemsetAsync(workspace, 0, sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;

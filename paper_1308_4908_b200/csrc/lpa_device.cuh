@@ -91,6 +91,13 @@ struct __align__(16) RowTap {
     float d2f;
     int off;  // byte offset of the sample from the pixel's own phase-plane position
 };
+// RT table layout: RtHeader, then TapRow[n_rows], then RowTap[n_taps].
+constexpr int RT_CLASSES = 16;  // (out x mod period) + period * (out y mod period), period <= 4
+struct RtHeader {
+    int row0[MAXS][3][RT_CLASSES];
+    int nrow[MAXS][3][RT_CLASSES];
+    int n_rows, pad[3];
+};
 struct __align__(16) TapRow {
     double dy;
     int first;  // index of the row's first RowTap
@@ -123,10 +130,11 @@ struct DevParams {
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, tab_bytes;  // tab_bytes: kernel-parameter table size (PAT or RT)
     int rt;                         // row-tap mode (ICI / order 2 with translation-only sensors)
+    int rt_period, rt_shift;        // RT: class period (2 / 4) and anchor shift (0 / 1) for sx 1 / 0.5
+    const unsigned char *rt_global; // RT: the table in the workspace (copied to shared memory)
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
-    int rt_nrow[MAXS][3][4];        // RT: tap rows of (sensor, channel, class); first row in pat_off
     uint32_t *work_count;
     uint32_t *work_items;
     // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)

@@ -71,10 +71,10 @@ def test_workspace_size():
     assert N.lib().hdr_lpa_workspace_bytes(s, 3, 2400, 1700, ctypes.byref(n)) == 0
     phase = 4 * 1200 * 850 * 8  # four (f_hat, 1/den) float2 phase planes per sensor
     lut = 65536 * 16  # exact (f_hat, 1/den) float64 per raw value
-    assert n.value == 256 + 3 * (phase + lut) + 2400 * 1700 * 3 * 4
+    assert n.value == 256 + 64 * 1024 + 3 * (phase + lut) + 2400 * 1700 * 3 * 4
     s[0].width = 2399  # odd width: phase planes padded to an even float2 count
     assert N.lib().hdr_lpa_workspace_bytes(s, 1, 2400, 1700, ctypes.byref(n)) == 0
-    assert n.value == 256 + 4 * 1200 * 850 * 8 + lut + 2400 * 1700 * 3 * 4
+    assert n.value == 256 + 64 * 1024 + 4 * 1200 * 850 * 8 + lut + 2400 * 1700 * 3 * 4
     assert N.lib().hdr_lpa_workspace_bytes(s, 3, 0, 10, ctypes.byref(n)) == N.HDR_ERR_ARG
 
 
