@@ -20,7 +20,7 @@ from .validation import ShapeMismatchError
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libhdrlpa.so"
-SOURCES = [PKG / "csrc" / "hdr_lpa.cu", PKG / "csrc" / "lpa_device.cuh", ROOT / "include" / "hdr_lpa.h"]
+SOURCES = sorted((PKG / "csrc").glob("*.cu*")) + [ROOT / "include" / "hdr_lpa.h"]
 
 MAX_SENSORS = 8
 MAX_SCALES = 8

@@ -1,0 +1,190 @@
+// calpa.cuh -- CALPA: steering field kernel and the exact steered pass.
+#pragma once
+
+#include "exact.cuh"
+
+namespace hdrlpa {
+
+// ---------------------------------------------------------------------------
+// CALPA: steering field and steered (anisotropic, two-phase) pass
+// (reference steering.py:72-248, _kernels.py:262-275, :303-392)
+// ---------------------------------------------------------------------------
+struct SteerConsts {
+    int half;
+    double wstd, lam1, lam2, alpha, sigma_max, inv_scale;
+};
+
+// steering_field_kernel (_kernels.py:310-392), float64, one thread per pixel.
+__global__ void steering_field_kernel(const float *gx, const float *gy, int w, int h,
+                                      SteerConsts K, double *theta, double *sigma,
+                                      double *gamma) {
+    const int xx = blockIdx.x * blockDim.x + threadIdx.x, yy = blockIdx.y;
+    if (xx >= w) return;
+    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+    int n = 0;
+    const double den = 2.0 * K.wstd * K.wstd;
+    for (int dy = -K.half; dy <= K.half; ++dy) {
+        const int iy = yy + dy;
+        if (iy < 0 || iy >= h) continue;
+        for (int dx = -K.half; dx <= K.half; ++dx) {
+            const int ix = xx + dx;
+            if (ix < 0 || ix >= w) continue;
+            const double g1 = (double)gx[(size_t)iy * w + ix] * K.inv_scale;
+            const double g2 = (double)gy[(size_t)iy * w + ix] * K.inv_scale;
+            if (!(isfinite(g1) && isfinite(g2))) continue;
+            const double wgt = exp(-(double)(dx * dx + dy * dy) / den);
+            s11 += wgt * g1 * g1;
+            s12 += wgt * g1 * g2;
+            s22 += wgt * g2 * g2;
+            ++n;
+        }
+    }
+    const size_t o = (size_t)yy * w + xx;
+    if (n == 0) {
+        theta[o] = 0.0;
+        sigma[o] = 1.0;
+        gamma[o] = 1.0;
+        return;
+    }
+    const double m = 0.5 * (s11 + s22), dd = hypot(0.5 * (s11 - s22), s12);
+    const double lmax = m + dd, lmin = fmax(m - dd, 0.0);
+    const double s1 = sqrt(lmax), s2 = sqrt(lmin);
+    double v1, v2;
+    if (fabs(s12) > 1e-300) {
+        v1 = s12;
+        v2 = lmin - s11;
+        if (v1 == 0.0 && v2 == 0.0) v1 = 1.0;
+    } else if (s11 <= s22) {
+        v1 = 1.0;
+        v2 = 0.0;
+    } else {
+        v1 = 0.0;
+        v2 = 1.0;
+    }
+    double th = atan2(v1, v2);
+    if (th <= -0.5 * M_PI)
+        th += M_PI;
+    else if (th > 0.5 * M_PI)
+        th -= M_PI;
+    const double dn = s2 + K.lam1;
+    double sg = dn == 0.0 ? ((s1 + K.lam1 == 0.0) ? 1.0 : K.sigma_max) : (s1 + K.lam1) / dn;
+    if (sg > K.sigma_max) sg = K.sigma_max;
+    theta[o] = th;
+    sigma[o] = sg;
+    gamma[o] = pow((s1 * s2 + K.lam2) / n, K.alpha);
+}
+
+// Exact accumulation with an arbitrary SPD window Hinv (two-phase CALPA).
+template <int ORDER, class Sweep>
+__device__ __forceinline__ void accumulate_hinv(const Sweep &sweep, int c, double h11, double h12,
+                                                double h22, double r, double r2,
+                                                Acc<NC<ORDER>::P> &acc) {
+    acc.zero();
+    const double h12x2 = 2.0 * h12;
+    sweep(c, -1, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
+                        float) {
+        // q = h11*dx*dx + 2.0*h12*dx*dy + h22*dy*dy (_kernels.py:164)
+        const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(h11, dx), dx),
+                                             __dmul_rn(__dmul_rn(h12x2, dx), dy)),
+                                   __dmul_rn(__dmul_rn(h22, dy), dy));
+        acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
+    });
+    sweep.reduce(acc);
+}
+
+template <int ORDER, class Sweep>
+__device__ bool steered_order(const DevParams &P, int c, const Sweep &sweep, const double *an,
+                              PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    Acc<PN> acc;
+    for (int phase = 0; phase < 2; ++phase) {
+        const double h11 = phase ? P.hinv[c][0] : an[0];
+        const double h12 = phase ? 0.0 : an[1];
+        const double h22 = phase ? P.hinv[c][0] : an[2];
+        double r = phase ? P.r[c][0] : fmin(an[3], P.max_radius);
+        int step = 0;
+        for (;;) {
+            accumulate_hinv<ORDER>(sweep, c, h11, h12, h22, r, __dmul_rn(r, r), acc);
+            R.work += acc.count;
+            Fit fit;
+            if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
+                R.count = acc.count;
+                R.val = fit.c0;
+                R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                R.gy = ORDER >= 1 ? fit.c2 : qnan();
+                R.outcome = ORDER * 16 + phase * 8 + (step < 7 ? step : 7);
+                return true;
+            }
+            if (r >= P.max_radius * (1.0 - 1e-12)) break;
+            r = fmin(r * 1.5, P.max_radius);
+            ++step;
+        }
+    }
+    return false;
+}
+
+// Steered pass (lpa_evaluate two_phase, _kernels.py:257-300): per pixel and
+// channel, Hinv = C/h and r0 = 3 sqrt(h sigma/gamma) from the steering field
+// (SteeringField.kernel_inputs, steering.py:94-107).
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_steered_kernel(const __grid_constant__ DevParams P) {
+    const int n = P.out_w * (P.row_end - P.row_begin) * 3;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int it = warp; it < n; it += nwarps) {  // one warp per pixel-channel
+        const int c = it % 3, pl = it / 3;
+        const int ox = pl % P.out_w, oy = P.row_begin + pl / P.out_w;
+        const int pix = oy * P.out_w + ox;
+        const GlobalSweep<32> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
+        const double ct = cos(th), st = sin(th);
+        const double h = P.h[c][0];  // channel scale
+        // covariance_entries (steering.py:80-87), same operation order
+        const double c11 = g * (s * ct * ct + st * st / s);
+        const double c12 = g * (ct * st) * (1.0 / s - s);
+        const double c22 = g * (s * st * st + ct * ct / s);
+        const double an[4] = {c11 / h, c12 / h, c22 / h, 3.0 * sqrt(h * s / g)};
+        PixelResult R;
+        R.sidx = 0;
+        bool ok = steered_order<ORDER>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 1) ok = steered_order<(ORDER >= 1 ? ORDER - 1 : 0)>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 2) ok = steered_order<0>(P, c, sweep, an, R);
+        if (!ok) {
+            R.val = R.gx = R.gy = qnan();
+            R.outcome = HDR_OUTCOME_NAN;
+            R.count = 0;
+        }
+        if ((threadIdx.x & 31) == 0) write_result(P, pix, c, R);
+    }
+}
+
+// The steered pass's exact evaluation of the fast path's work items (all
+// outcomes other than a sound phase-0 step-0 fit), one 8-lane group per item.
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_steered_slow_kernel(const __grid_constant__ DevParams P) {
+    constexpr int G = SLOW_LANES;
+    const uint32_t n = *P.work_count;
+    const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t ngrp = (gridDim.x * blockDim.x) / G;
+    for (uint32_t i = grp; i < n; i += ngrp) {
+        const uint32_t item = P.work_items[i];
+        const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
+        const int ox = pix % P.out_w, oy = pix / P.out_w;
+        const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        double an[4];
+        steer_inputs(P, pix, c, an);
+        PixelResult R;
+        R.sidx = 0;
+        bool ok = steered_order<ORDER>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 1) ok = steered_order<(ORDER >= 1 ? ORDER - 1 : 0)>(P, c, sweep, an, R);
+        if (!ok && ORDER >= 2) ok = steered_order<0>(P, c, sweep, an, R);
+        if (!ok) {
+            R.val = R.gx = R.gy = qnan();
+            R.outcome = HDR_OUTCOME_NAN;
+            R.count = 0;
+        }
+        if ((threadIdx.x & (G - 1)) == 0) write_result(P, pix, c, R);
+    }
+}
+
+}  // namespace hdrlpa

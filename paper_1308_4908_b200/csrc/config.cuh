@@ -1,0 +1,38 @@
+// config.cuh -- tiling, workspace and tuning constants of the sm_100a kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hdr_lpa.h"
+#include "lpa_device.cuh"
+
+namespace hdrlpa {
+
+constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per tile pixel
+
+// workspace layout: [header: work counter][pre-computed taps][work items]
+static const size_t WS_HEADER = 256;
+// Order-2 tile sweeps: skip samples outside the disk with branches (1) or
+// accumulate them with zero weight (0; the row-factored moments make a
+// sample cheap enough that divergent branches cost more than they save)
+#ifndef HDR_BRANCHY_O2
+#define HDR_BRANCHY_O2 1
+#endif
+static_assert(sizeof(DevParams) + TAP_PARAM_BYTES <= 32764, "kernel parameter space");
+// plane buffers per CTA of the fast kernel's staging pipeline (measured: 3
+// buffers gain nothing on cfg2 and cost cfg3 5% through occupancy)
+#ifndef HDR_NBUF
+#define HDR_NBUF 2
+#endif
+constexpr int NBUF = HDR_NBUF;
+static const size_t LUT_BYTES = 65536 * sizeof(double2);
+static const size_t RT_TABLE_BYTES = 64 * 1024;  // row-tap table (workspace, then shared memory)
+
+template <int ORDER>
+struct NC {
+    static constexpr int P = (ORDER + 1) * (ORDER + 2) / 2;
+};
+
+}  // namespace hdrlpa

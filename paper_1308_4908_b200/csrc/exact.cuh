@@ -1,0 +1,154 @@
+// exact.cuh -- the exact (slow) path: lpa_evaluate's ladder, the ICI rule,
+// float64 recomputation, and lpa_slow_kernel over the fast path's work list.
+#pragma once
+
+#include "sweeps.cuh"
+
+namespace hdrlpa {
+
+// ---------------------------------------------------------------------------
+// Exact evaluation (slow path): lpa_evaluate's ladder (_kernels.py:257-300)
+// and the ICI rule.
+// ---------------------------------------------------------------------------
+template <int ORDER, class Sweep>
+__device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    double r = P.r[c][0];  // already min(r0, max_radius)
+    int step = 0;
+    Acc<PN> acc;
+    for (;;) {
+        accumulate<ORDER, true>(P, c, 0, r, __dmul_rn(r, r), sweep, acc);
+        R.work += acc.count;
+        Fit fit;
+        if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
+            R.count = acc.count;
+            R.val = fit.c0;
+            R.gx = ORDER >= 1 ? fit.c1 : qnan();
+            R.gy = ORDER >= 1 ? fit.c2 : qnan();
+            R.outcome = ORDER * 16 + (step < 15 ? step : 15);
+            return true;
+        }
+        if (r >= P.max_radius * (1.0 - 1e-12)) return false;
+        r = fmin(r * 1.5, P.max_radius);
+        ++step;
+    }
+}
+
+template <int ORDER, class Sweep>
+__device__ void ladder(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+    R.sidx = 0;
+    if (ladder_order<ORDER>(P, c, sweep, R)) return;
+    if constexpr (ORDER >= 1) {
+        if (ladder_order<ORDER - 1>(P, c, sweep, R)) return;
+    }
+    if constexpr (ORDER >= 2) {
+        if (ladder_order<0>(P, c, sweep, R)) return;
+    }
+    R.val = R.gx = R.gy = qnan();
+    R.outcome = HDR_OUTCOME_NAN;
+    R.count = 0;
+}
+
+// ICI with a pluggable decision: fast (condition
+// bounds; may return AMBIG) or exact.  Returns FIT_OK with R filled, FIT_FAIL
+// if scale 0 fails (the caller runs the ladder), FIT_AMBIG if a decision
+// needs the exact path.
+template <int ORDER, bool EXACT, class Sweep>
+__device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    Acc<PN> acc;
+    Fit fit;
+    double L = 0.0, U = 0.0, eL = 0.0, eU = 0.0;  // running bounds and their error bounds
+    bool precise = true;
+    for (int k = 0; k < P.n_scales; ++k) {
+        accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+        R.work += acc.count;
+        const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
+        if (st == FIT_AMBIG) return FIT_AMBIG;
+        if (st != FIT_OK) {
+            if (k == 0) return FIT_FAIL;
+            break;  // an invalid scale ends the search at k-1
+        }
+        float tk = 0.f;
+        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk));
+        const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
+        // fast path: error bound of lo/hi (fp32 rounding of c0: fit_precise_sharp;
+        // of sd: ICI_SD_EPS relative) -- an intersection test closer than the
+        // bounds is decided by the exact path, so scale indices stay exact
+        const double ek = EXACT ? 0.0 : 2.0 * FAST_EPS * (double)tk + P.gamma * sd * ICI_SD_EPS;
+        if (k == 0) {
+            L = lo;
+            U = hi;
+            eL = eU = ek;
+        } else {
+            if (lo >= L) eL = lo > L ? ek : fmax(eL, ek);
+            if (hi <= U) eU = hi < U ? ek : fmax(eU, ek);
+            L = fmax(L, lo);
+            U = fmin(U, hi);
+            if (!EXACT && fabs(L - U) <= eL + eU) return FIT_AMBIG;
+            if (L > U) break;
+        }
+        R.val = fit.c0;
+        R.gx = fit.c1;
+        R.gy = fit.c2;
+        R.sidx = k;
+        R.count = acc.count;
+        if constexpr (!EXACT) precise = fit_precise_sharp(fit.c0, tk, P.prec_floor);
+    }
+    if (!precise) return FIT_PREC;  // selected estimate too close to fp32 rounding limits
+    if (ORDER == 0) R.gx = R.gy = qnan();
+    R.outcome = ORDER * 16;
+    return FIT_OK;
+}
+
+// Float64 recomputation of a fit whose fast-path decisions (validity, ICI
+// scale) were sound but whose value failed fit_precise: exact weights and
+// values at scale k.  False if the exact solve disagrees (then the caller
+// runs the full exact evaluation).
+template <int ORDER, class Sweep>
+__device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep, PixelResult &R) {
+    constexpr int PN = NC<ORDER>::P;
+    Acc<PN> acc;
+    accumulate<ORDER, true>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+    R.work += acc.count;
+    Fit fit;
+    if (solve_fast<PN>(acc, P.cond, fit) != FIT_OK) return false;
+    R.val = fit.c0;
+    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+    R.gy = ORDER >= 1 ? fit.c2 : qnan();
+    R.sidx = k;
+    R.outcome = ORDER * 16;
+    R.count = acc.count;
+    return true;
+}
+
+// One group of SLOW_LANES lanes per work item: they share every window's
+// candidates.
+#ifndef SLOW_LANES
+#define SLOW_LANES 8
+#endif
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
+    constexpr int G = SLOW_LANES;  // lanes per work item
+    const uint32_t n = *P.work_count;
+    const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t ngrp = (gridDim.x * blockDim.x) / G;
+    for (uint32_t i = grp; i < n; i += ngrp) {
+        const uint32_t item = P.work_items[i];
+        const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
+        const int kk = (int)((item >> 2) & 15);
+        const int ox = pix % P.out_w, oy = pix / P.out_w;
+        const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        PixelResult R;
+        if (kk && precise_fit<ORDER>(P, c, kk - 1, sweep, R)) {
+            // the fast path's decisions stand; only the value was recomputed
+        } else if (P.n_scales > 1) {
+            if (ici<ORDER, true>(P, c, sweep, R) != FIT_OK) ladder<ORDER>(P, c, sweep, R);
+        } else {
+            ladder<ORDER>(P, c, sweep, R);
+        }
+        if ((threadIdx.x & (G - 1)) == 0) write_result(P, pix, c, R);
+    }
+}
+
+}  // namespace hdrlpa

@@ -1,0 +1,314 @@
+// fast_kernel.cuh -- lpa_fast_kernel: the persistent tile kernel (tap, row-
+// tap, sweep, ICI and CALPA-steered variants) and its per-pixel compute.
+#pragma once
+
+#include "exact.cuh"
+#include "staging.cuh"
+
+namespace hdrlpa {
+
+// Fixed-scale accumulation from the pre-computed taps: the window of every
+// output pixel of a parity class visits the same sensor offsets with the same
+// weights, so there is no membership test, no exp and no loop control beyond
+// the tap list (the samples and weights are the reference's: DESIGN.md s3).
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
+template <int ORDER>
+__device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
+                                                const unsigned char *taps, const int (*org)[2],
+                                                int c, int px, int py, Acc<NC<ORDER>::P> &acc) {
+    acc.zero();
+    const int cls = ((py & 1) << 1) | (px & 1);
+    // shared-window addresses: one LDS.128 (dx, dy), one LDS.64 (W, byte
+    // offset) and one LDS.64 (f_hat, 1/den) per tap
+    const uint32_t txy = smem_addr(taps);
+    const uint32_t tw = txy + (uint32_t)P.n_taps * (uint32_t)sizeof(TapXY);
+    int count = 0;
+    float sabs = 0.f;
+    for (int s = 0; s < P.n_sensors; ++s) {
+        const int n = P.pat_cnt[s][c][py & 1];
+        if (!n) continue;
+        const DevSensor &S = P.s[s];
+        const int o = P.pat_off[s][c][cls];
+        const int pw = S.rw >> 1;
+        // the pixel's own position in its phase plane (origins are even)
+        const uint32_t vb = smem_addr(sm + S.off_vi) +
+                            8u * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+        for (int t = o; t < o + n; ++t) {
+            const double2 X = lds_d2(txy + 16u * (uint32_t)t);
+            const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
+            // masked samples carry (0, 0) and padding taps W = 0, so w and the
+            // value are already zero exactly when the tap must not count
+            const float2 e = lds_f2(vb + Q.y);
+            const float w = __uint_as_float(Q.x) * e.y;
+            sabs = fmaf(w, fabsf(e.x), sabs);
+            const double dxx = ORDER >= 2 ? __dmul_rn(X.x, X.x) : 0.0;
+            const double dyy = ORDER >= 2 ? __dmul_rn(X.y, X.y) : 0.0;
+            acc.add((double)w, (double)e.x, X.x, X.y, dxx, dyy, 0);
+            // predicated increment (setp + @p add): one instruction less than a select
+            asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, 0f00000000;\n @p add.s32 %0, %0, 1;\n}"
+                : "+r"(count)
+                : "f"(w));
+        }
+    }
+    acc.count = count;
+    acc.sabs = sabs;
+}
+
+// ---------------------------------------------------------------------------
+// CALPA steered pass, fast path (lpa_evaluate two_phase, _kernels.py:257-300):
+// the phase-0 step-0 fit (anisotropic window of the steering field at
+// r = min(r0, max_radius)) from the staged planes with fp32 weights; any
+// other outcome, and fits failing fit_precise, go to lpa_steered_slow_kernel.
+// ---------------------------------------------------------------------------
+// Per-pixel kernel inputs (SteeringField.kernel_inputs, steering.py:80-107),
+// float64 in the reference's operation order; an = (h11, h12, h22, r0).
+__device__ __forceinline__ void steer_inputs(const DevParams &P, int pix, int c, double *an) {
+    const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
+    const double ct = cos(th), st = sin(th);
+    const double h = P.h[c][0];  // channel scale
+    const double c11 = g * (s * ct * ct + st * st / s);
+    const double c12 = g * (ct * st) * (1.0 / s - s);
+    const double c22 = g * (s * st * st + ct * ct / s);
+    an[0] = c11 / h;
+    an[1] = c12 / h;
+    an[2] = c22 / h;
+    an[3] = 3.0 * sqrt(h * s / g);
+}
+
+// Row-factored moments with the anisotropic window
+// W = exp(-(h11 dx^2 + 2 h12 dx dy + h22 dy^2)) (_kernels.py:164-168): along a
+// row dy is constant, so q = h11 dx^2 + (2 h12 dy) dx + h22 dy^2.
+template <int ORDER>
+struct RowAniso {
+    static constexpr int PN = NC<ORDER>::P;
+    RowMoments<ORDER> m;
+    float h11, h12x2, h22;  // pre-scaled by log2(e)
+    float a, b;             // per row: h22 dy^2, 2 h12 dy
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        m.begin_row(dy, dyy);
+        a = h22 * (float)dyy;
+        b = h12x2 * (float)dy;
+    }
+    __device__ __forceinline__ void end_row(double dy, double dyy) { m.end_row(dy, dyy); }
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
+                                           double dxx, double dyy, float) {
+        const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
+        // RowMoments' weight is ex2(-hl * d2f) * iv: feed it q2 with hl = 1
+        m.sample(ok, v, iv, dx, dy, dxx, dyy, q2);
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float) {
+        const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+        m.general(ok, v, iv, dx, dy, dxx, dyy, q2);
+    }
+};
+
+template <int ORDER, class Sweep>
+__device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, const double *an,
+                                                 double r, double r2, Acc<NC<ORDER>::P> &acc) {
+    constexpr float L2E = 1.4426950408889634f;
+    acc.zero();
+    const float h11 = (float)an[0] * L2E, h12x2 = 2.f * (float)an[1] * L2E, h22 = (float)an[2] * L2E;
+    if constexpr (ORDER >= 1) {
+        RowAniso<ORDER> pol{RowMoments<ORDER>{acc, 1.0f}, h11, h12x2, h22, 0.f, 0.f};
+        sweep.rows(c, -1, r, r2, pol);
+    } else {
+        sweep(c, -1, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
+                                double dyy, float) {
+            const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+            const float w = ok ? ex2_approx(-q2) * iv : 0.f;
+            const double y = ok ? v : 0.0;
+            acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+            acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+        });
+    }
+}
+
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT, bool STEER>
+__device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
+                                             const unsigned char *taps, int t,
+                                             const int (*org)[2], bool tile_covered) {
+    constexpr int PN = NC<ORDER>::P;
+    int tx0, ty0, tx1, ty1;
+    tile_bounds(P, t, tx0, ty0, tx1, ty1);
+    const int px = tx0 + (int)(threadIdx.x % TW);
+    const int py = ty0 + (int)(threadIdx.x / TW);
+    if (px > tx1 || py > ty1) return;
+    const int pix = py * P.out_w + px;
+    const double qx = qcoord(px, P.sx), qy = qcoord(py, P.sy);
+
+    // every window of this pixel must lie inside the staged region (checked
+    // per pixel only when the tile as a whole is not covered)
+    bool covered = true;
+    for (int s = 0; !tile_covered && s < P.n_sensors; ++s) {
+        const DevSensor &S = P.s[s];
+        int xlo, xhi, ylo, yhi;
+        window_bbox(S, qx, qy, P.fast_R, xlo, xhi, ylo, yhi);
+        covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
+                   yhi < org[s][1] + S.rh;
+    }
+    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org, qx, qy,
+                                                                   px, py, taps};
+
+    for (int c = 0; c < 3; ++c) {
+        PixelResult R;
+        R.sidx = 0;
+        int st = FIT_AMBIG;
+        if (covered) {
+            if constexpr (STEER) {
+                double an[4];
+                steer_inputs(P, pix, c, an);
+                const double r = fmin(an[3], P.max_radius);
+                Acc<PN> acc;
+                accumulate_aniso<ORDER>(sweep, c, an, r, __dmul_rn(r, r), acc);
+                R.work = acc.count;
+                Fit fit;
+                st = solve_fast<PN>(acc, P.cond, fit);
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, r, P.prec_floor)) st = FIT_AMBIG;
+                if (st == FIT_OK) {
+                    R.count = acc.count;
+                    R.val = fit.c0;
+                    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                    R.gy = ORDER >= 1 ? fit.c2 : qnan();
+                    R.outcome = ORDER * 16;  // phase 0 (anisotropic), radius step 0
+                }
+            } else if constexpr (ICI) {
+                st = ici<ORDER, false>(P, c, sweep, R);
+            } else {
+                Acc<PN> acc;
+                if constexpr (PAT)
+                    accumulate_taps<ORDER>(P, sm, taps, org, c, px, py, acc);
+                else
+                    accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
+                R.work = acc.count;
+                Fit fit;
+                st = solve_fast<PN>(acc, P.cond, fit);
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor)) {
+                    // loose bound failed: the sharp one needs a sweep with g (not
+                    // for the tap path, where this is rare); else the exact path
+                    float tk = 0.f;
+                    if constexpr (!PAT && ORDER >= 1)
+                        fit_variance<ORDER, false>(P, c, 0, sweep, fit.g, &tk);
+                    if (PAT || ORDER == 0 || !fit_precise_sharp(fit.c0, tk, P.prec_floor))
+                        st = FIT_PREC;
+                }
+                if (st == FIT_OK) {
+                    R.count = acc.count;
+                    R.val = fit.c0;
+                    R.gx = ORDER >= 1 ? fit.c1 : qnan();
+                    R.gy = ORDER >= 1 ? fit.c2 : qnan();
+                    R.outcome = ORDER * 16;
+                }
+            }
+        }
+        if (st == FIT_OK) {
+            write_result(P, pix, c, R);
+        } else {
+            // work item: band-relative pixel | kk | channel, kk = 0: full exact
+            // evaluation, kk = k + 1: float64 recomputation of the fit at scale k
+            const uint32_t kk = st == FIT_PREC ? (uint32_t)R.sidx + 1u : 0u;
+            const uint32_t slot = atomicAdd(P.work_count, 1u);
+            P.work_items[slot] =
+                ((uint32_t)(pix - P.row_begin * P.out_w) << 6) | (kk << 2) | (uint32_t)c;
+        }
+    }
+}
+
+// Persistent kernel.  The raw frames were converted once per frame into
+// (f_hat, 1/den) phase planes by radiance_phase_kernel; each tile's staged
+// regions are TMA-loaded from them, double-buffered: while tile t is fitted
+// from buffer b, the copies for tile t+1 land in buffer b^1.
+#ifndef HDR_O2_MINBLOCKS
+#define HDR_O2_MINBLOCKS 2
+#endif
+#ifndef HDR_PAT_MINBLOCKS
+#define HDR_PAT_MINBLOCKS 3
+#endif
+template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false, bool STEER = false>
+// Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
+// by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
+__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
+    lpa_fast_kernel(const __grid_constant__ DevParams P,
+                    const __grid_constant__
+                    typename std::conditional<PAT, TapParam, NoTaps>::type T) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int s_org[NBUF][MAXS][2];
+    __shared__ int s_cov[NBUF];
+    __shared__ unsigned s_done[NBUF];
+    __shared__ __align__(8) uint64_t bar_full[NBUF];
+    const int ntiles = P.tiles_x * P.tiles_y;
+    const unsigned char *taps = smem + P.off_taps;
+    unsigned char *planes = smem + P.plane_base;
+    if constexpr (PAT) {  // the kernel-parameter tap table into shared memory
+        const uint4 *src = (const uint4 *)T.bytes;
+        uint4 *dst = (uint4 *)(smem + P.off_taps);
+        const int n16 = (P.tab_bytes + 15) / 16;
+        for (int i = threadIdx.x; i < n16; i += NT) dst[i] = src[i];
+    } else if constexpr (RT) {  // the row-tap table from the workspace
+        const uint4 *src = (const uint4 *)P.rt_global;
+        uint4 *dst = (uint4 *)(smem + P.off_taps);
+        const int n16 = (P.tab_bytes + 15) / 16;
+        for (int i = threadIdx.x; i < n16; i += NT) dst[i] = __ldg(src + i);
+    }
+    int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&bar_full[b], 1);
+            s_done[b] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();  // barriers initialised, taps staged
+    // prologue: warp 0 stages this CTA's first NBUF tiles
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int b = 0; b < NBUF; ++b)
+            if (t + b * (int)gridDim.x < ntiles)
+                stage_tile<!PAT>(P, planes + b * P.buf_stride, t + b * gridDim.x, s_org[b],
+                                 &s_cov[b], &bar_full[b]);
+    }
+    // No CTA-wide barrier in the loop: a warp waits only for its tile's data.
+    // The LAST warp to finish tile t (buffer b) refills b with tile t + NBUF*G,
+    // so warps that finish early run up to NBUF-1 tiles ahead instead of idling
+    // at a __syncthreads while the slowest warp of the tile completes.
+    constexpr int NWARPS = NT / 32;
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        const int b = i % NBUF;
+        unsigned char *pb = planes + b * P.buf_stride;
+        mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
+        const int tn = t + NBUF * (int)gridDim.x;
+        if (tn < ntiles) {  // CTA-uniform
+            __syncwarp();
+            unsigned last = 0;
+            if ((threadIdx.x & 31) == 0) {
+                __threadfence_block();  // this warp's reads of buffer b precede the count
+                last = atomicAdd(&s_done[b], 1u) == NWARPS - 1;
+                if (last) {
+                    s_done[b] = 0;
+                    __threadfence_block();
+                }
+            }
+            if (__shfl_sync(0xffffffffu, last, 0))
+                stage_tile<!PAT>(P, pb, tn, s_org[b], &s_cov[b], &bar_full[b]);
+        }
+    }
+}
+
+}  // namespace hdrlpa

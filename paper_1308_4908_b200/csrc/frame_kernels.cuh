@@ -1,0 +1,124 @@
+// frame_kernels.cuh -- per-frame radiometric kernels (LUT, phase-plane
+// pre-pass, float64 sample planes, saturation masks) and the DFMA probe.
+#pragma once
+
+#include "config.cuh"
+
+namespace hdrlpa {
+
+// Exact radiometry LUT (scalar calibration): entry v = radiance_exact of a
+// raw value v below saturation, for the slow path's float64 sweeps.
+__global__ void radiance_lut_kernel(const __grid_constant__ DevParams P) {
+    const DevSensor &S = P.s[blockIdx.y];
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (S.planes || v >= S.sat) return;
+    double f, iv;
+    radiometry_exact(S, v, S.bias, S.nonuni, S.readvar, P.use_sigma, f, iv);
+    S.lut[v] = make_double2(f, iv);
+}
+
+// Per-frame radiometric pre-pass: every raw pixel converted once into the
+// de-interleaved phase planes (radiometry.py:303-336 for the whole frame);
+// out-of-frame padding gets 1/den = 0 (no sample).  HBM-bound.
+// One thread per (sensor, phase row j, group of 4 phase columns): raw rows
+// 2j and 2j+1, columns 8g..8g+7 read as 16-B vectors (when the frame's pitch
+// and base allow), the four phase planes written as 2 x 16-B per plane.
+__global__ void __launch_bounds__(128) radiance_phase_kernel(const __grid_constant__ DevParams P) {
+    const DevSensor &S = P.s[blockIdx.z];
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= S.pwg || j >= S.phg) return;
+    const int x0 = 2 * i0;
+    const bool vec = S.vec_raw && x0 + 8 <= S.pitch;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int y = 2 * j + r;
+        uint16_t v[8];
+        if (y < S.height && vec) {
+            const uint4 q = __ldg((const uint4 *)(S.raw + (size_t)y * S.pitch + x0));
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[2 * k] = (uint16_t)(w[k] & 0xffffu);
+                v[2 * k + 1] = (uint16_t)(w[k] >> 16);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                v[k] = (y < S.height && x0 + k < S.width) ? __ldg(S.raw + (size_t)y * S.pitch + x0 + k)
+                                                          : (uint16_t)0;
+        }
+        float2 o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            o[k] = (y < S.height && x0 + k < S.width)
+                       ? radiance_from_raw(S, (int)v[k], x0 + k, y, P.use_sigma)
+                       : make_float2(0.f, 0.f);  // padding: no sample
+#pragma unroll
+        for (int px = 0; px < 2; ++px) {
+            float4 *dst = (float4 *)(S.phase + ((size_t)(2 * r + px) * S.phg + j) * S.pwg + i0);
+            dst[0] = make_float4(o[px].x, o[px].y, o[px + 2].x, o[px + 2].y);
+            dst[1] = make_float4(o[px + 4].x, o[px + 4].y, o[px + 6].x, o[px + 6].y);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Saturation mask bit-planes (radiometry.py:298-300, :316-317)
+// ---------------------------------------------------------------------------
+__global__ void saturation_mask_kernel(const DevSensor S, uint32_t *bits, int wpr) {
+    const int y = blockIdx.y;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    bool m = false;
+    if (x < S.width) {
+        const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+        m = raw >= S.sat || (S.defective && __ldg(S.defective + (size_t)y * S.width + x));
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && x < S.width) bits[(size_t)y * wpr + (x >> 5)] = word;
+}
+
+__global__ void radiance_planes_kernel(const DevSensor S, int use_sigma, float *value,
+                                       float *inv_den) {
+    const int y = blockIdx.y;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= S.width) return;
+    const float2 e = radiance_sample(S, x, y, use_sigma);
+    value[(size_t)y * S.width + x] = e.x;
+    inv_den[(size_t)y * S.width + x] = e.y;
+}
+
+// The reference's sample columns as float64 planes (radiometry.py:303-336):
+// value = f_hat, sigma = sqrt(max(var, quantisation floor)); sigma = 0 marks
+// "no sample" (saturated / defective).
+__global__ void sample_planes_kernel(const DevSensor S, double *value, double *sigma) {
+    const int y = blockIdx.y;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= S.width) return;
+    const size_t i = (size_t)y * S.width + x;
+    const int raw = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+    double f = 0.0, sg = 0.0;
+    if (raw < S.sat && !(S.defective && __ldg(S.defective + i))) {
+        const double b = S.bias_p ? __ldg(S.bias_p + i) : S.bias;
+        const double a = S.nonuni_p ? __ldg(S.nonuni_p + i) : S.nonuni;
+        const double vr = S.readvar_p ? __ldg(S.readvar_p + i) : S.readvar;
+        radiometry_sigma(S, raw, b, a, vr, f, sg);
+    }
+    value[i] = f;
+    sigma[i] = sg;
+}
+
+// DFMA throughput probe: 8 independent chains per thread, full occupancy.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double *sink, int iters, double a,
+                                                         double b) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5) sink[threadIdx.x] = s;  // keep the chains alive
+}
+
+}  // namespace hdrlpa

@@ -1,0 +1,151 @@
+// staging.cuh -- TMA / mbarrier helpers and the per-tile staging of the
+// fast kernels (region origins, coverage, coordinate tables, 3-D bulk copies).
+#pragma once
+
+#include "config.cuh"
+
+namespace hdrlpa {
+
+// ---------------------------------------------------------------------------
+// Fast path: persistent CTAs, double-buffered TMA staging of the raw tiles.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile(
+        "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(
+            smem_addr(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(
+                     smem_addr(bar))
+                 : "memory");
+}
+// Bounded wait: a barrier that never completes (a lost TMA transaction)
+// traps -- the launch fails with an error -- instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t spin = 0;; ++spin) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 24)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParams &P, int tx0,
+                                              int ty0, int tx1, int ty1, int &ox, int &oy) {
+    // union of the window bboxes of the tile's corner queries at radius fast_R;
+    // every bbox bound is a floor/ceil of a correctly rounded affine function
+    // of (qx, qy), monotone in each, so its extremes over the tile are
+    // attained at the corners.
+    int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double qx = qcoord((k & 1) ? tx1 : tx0, P.sx);
+        const double qy = qcoord((k & 2) ? ty1 : ty0, P.sy);
+        int xlo, xhi, ylo, yhi;
+        window_bbox(S, qx, qy, P.fast_R, xlo, xhi, ylo, yhi);
+        xmin = min(xmin, xlo);
+        ymin = min(ymin, ylo);
+        xmax = max(xmax, xhi);
+        ymax = max(ymax, yhi);
+    }
+    // x: multiple of 8 elements -- a TMA tile copy must start on a 16-byte
+    // boundary of the row (measured: unaligned starts raise an illegal-
+    // instruction fault; scripts/probes/tma_probe.cu).  Both even, so the
+    // Bayer phase of a staged pixel equals the parity of its coordinates.
+    ox = xmin & ~7;
+    oy = ymin & ~1;
+    // true: every window of every pixel of the tile lies inside the region
+    return xmax < ox + S.rw && ymax < oy + S.rh;
+}
+
+__device__ __forceinline__ void tile_bounds(const DevParams &P, int t, int &tx0, int &ty0, int &tx1,
+                                            int &ty1) {
+    tx0 = (t % P.tiles_x) * TW;
+    ty0 = P.row_begin + (t / P.tiles_x) * TH;
+    tx1 = min(tx0 + TW, P.out_w) - 1;
+    ty1 = min(ty0 + TH, P.row_end) - 1;
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// One warp stages tile t into plane buffer `pb`: region origins + tile
+// coverage (lane s: sensor s), the f64 coordinate tables (rotated path), then
+// lane 0 issues one 3-D TMA copy per sensor of the four (f_hat, 1/den) phase
+// planes' staged regions, completing on `full` (arrive + expect_tx; the
+// arrive releases the origins and tables to the consumers).
+template <bool TABLES>
+__device__ __forceinline__ void stage_tile(const DevParams &P, unsigned char *pb, int t,
+                                           int (*org)[2], int *cov, uint64_t *full) {
+    const int lane = threadIdx.x & 31;
+    int tx0, ty0, tx1, ty1;
+    tile_bounds(P, t, tx0, ty0, tx1, ty1);
+    bool in = true;
+    if (lane < P.n_sensors)
+        in = region_origin(P.s[lane], P, tx0, ty0, tx1, ty1, org[lane][0], org[lane][1]);
+    const bool all_in = __all_sync(0xffffffffu, in);
+    if (lane == 0) *cov = all_in ? 1 : 0;
+    __syncwarp();
+    if constexpr (TABLES) {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int ox = org[s][0], oy = org[s][1];
+            // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y)
+            // (exact, since fl(T01*y) = fl(T10*x) = 0); otherwise the four
+            // partial products.
+            double *tx0t = (double *)(pb + S.off_tx0), *tx3t = (double *)(pb + S.off_tx3);
+            double *ty1t = (double *)(pb + S.off_ty1), *ty4t = (double *)(pb + S.off_ty4);
+            for (int i = lane; i < S.rw; i += 32) {
+                const double xd = (double)(ox + i);
+                const double a = __dmul_rn(S.T[0], xd);
+                tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
+                tx3t[i] = __dmul_rn(S.T[3], xd);
+            }
+            for (int i = lane; i < S.rh; i += 32) {
+                const double yd = (double)(oy + i);
+                const double bb = __dmul_rn(S.T[4], yd);
+                ty1t[i] = __dmul_rn(S.T[1], yd);
+                ty4t[i] = S.separable ? __dadd_rn(bb, S.T[5]) : bb;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        // the buffer's previous contents were read through the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint32_t bytes = 0;
+        for (int s = 0; s < P.n_sensors; ++s) bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
+        mbar_expect_tx(full, bytes);
+        for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
+            tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
+    }
+}
+
+}  // namespace hdrlpa

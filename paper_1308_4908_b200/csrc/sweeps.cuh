@@ -1,0 +1,541 @@
+// sweeps.cuh -- window sweeps (global / staged tile) and the accumulation
+// policies (row-factored moments and variances) shared by all paths.
+#pragma once
+
+#include "config.cuh"
+
+namespace hdrlpa {
+
+// ---------------------------------------------------------------------------
+// Window sweeps.  A sweep enumerates the samples of one channel inside the
+// support disk |X - q| <= r, in the order (sensor, Bayer phase, row, column),
+// and calls body(value, 1/den, dx, dy, dx^2, dy^2, |d|^2 as fp32) for each
+// (value and 1/den: fp32 in the tile sweeps, float64 in the global sweep).
+// Offsets and the membership test are float64 in the reference's exact
+// operation order (radiometry.py:84, _kernels.py:160-163), so both sweeps
+// below select exactly the reference's sample set in the same order.
+// ---------------------------------------------------------------------------
+
+// Slow path: straight from the raw frames in global memory, float64 radiometry.
+// LANES > 1: the candidates of every window are split over an aligned group
+// of LANES lanes of a warp (candidate j -> group lane j % LANES) and the sums
+// are combined by a butterfly reduction, after which every lane of the group
+// holds bitwise-identical totals.  Groups of one warp may diverge.
+template <int LANES>
+struct GlobalSweep {
+    const DevParams &P;
+    double qx, qy;
+    __device__ __forceinline__ static unsigned group_mask() {
+        if constexpr (LANES >= 32)
+            return 0xffffffffu;
+        else
+            return ((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1));
+    }
+    template <int PN>
+    __device__ __forceinline__ void reduce(Acc<PN> &acc) const {
+        if constexpr (LANES > 1) {
+            const unsigned mask = group_mask();
+#pragma unroll
+            for (int m = LANES / 2; m >= 1; m >>= 1) {
+#pragma unroll
+                for (int i = 0; i < Acc<PN>::NS; ++i) acc.A[i] += __shfl_xor_sync(mask, acc.A[i], m);
+#pragma unroll
+                for (int i = 0; i < PN; ++i) acc.b[i] += __shfl_xor_sync(mask, acc.b[i], m);
+                acc.count += __shfl_xor_sync(mask, acc.count, m);
+            }
+        }
+    }
+    __device__ __forceinline__ double reduce(double v) const {
+        if constexpr (LANES > 1) {
+            const unsigned mask = group_mask();
+#pragma unroll
+            for (int m = LANES / 2; m >= 1; m >>= 1) v += __shfl_xor_sync(mask, v, m);
+        }
+        return v;
+    }
+    template <class Body>
+    __device__ __forceinline__ void operator()(int c, int /*k*/, double r, double r2,
+                                               Body body) const {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int pm = S.phmask[c];
+            if (!pm) continue;
+            int xlo, xhi, ylo, yhi;
+            window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
+            const double T0 = S.T[0], T1 = S.T[1], T2 = S.T[2];
+            const double T3 = S.T[3], T4 = S.T[4], T5 = S.T[5];
+            for (int ph = 0; ph < 4; ++ph) {
+                if (!((pm >> ph) & 1)) continue;
+                const int py = ph >> 1, px = ph & 1;
+                const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
+                const int nrow = yhi >= ys ? ((yhi - ys) >> 1) + 1 : 0;
+                const int ncol = xhi >= xs ? ((xhi - xs) >> 1) + 1 : 0;
+                const int lane = LANES > 1 ? (int)(threadIdx.x & (LANES - 1)) : 0;
+                for (int j = lane; j < nrow * ncol; j += LANES) {
+                    const int y = ys + 2 * (j / ncol), x = xs + 2 * (j % ncol);
+                    const double yd = (double)y;
+                    const double t1y = __dmul_rn(T1, yd), t4y = __dmul_rn(T4, yd);
+                    double f, iv;  // float64 radiometry straight from the raw frame
+                    if (!radiance_exact(S, x, y, P.use_sigma, f, iv)) continue;
+                    const double xd = (double)x;
+                    const double X = __dadd_rn(__dadd_rn(__dmul_rn(T0, xd), t1y), T2);
+                    const double Y = __dadd_rn(__dadd_rn(__dmul_rn(T3, xd), t4y), T5);
+                    const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                    const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
+                    const double d2 = __dadd_rn(dxx, dyy);
+                    if (d2 > r2) continue;  // _kernels.py:162
+                    body(true, f, iv, dx, dy, dxx, dyy, (float)d2);
+                }
+            }
+        }
+    }
+};
+
+// Adapter: a per-sample body as a traversal policy (no row hooks).
+template <class Body>
+struct PerSample {
+    Body &body;
+    __device__ __forceinline__ void begin_row(double, double) {}
+    __device__ __forceinline__ void end_row(double, double) {}
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
+                                           double dxx, double dyy, float d2f) {
+        body(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        body(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+};
+
+template <int MAXC, bool BRANCHY, bool RT = false>
+struct TileSweep {
+    const DevParams &P;
+    const unsigned char *sm;
+    const int (*org)[2];
+    double qx, qy;
+    int px, py;                 // the output pixel (RT: parity class, phase-plane base)
+    const unsigned char *rt;    // RT: row-tap table in shared memory (rows, then taps)
+    template <int PN>
+    __device__ __forceinline__ void reduce(Acc<PN> &) const {}
+    __device__ __forceinline__ double reduce(double v) const { return v; }
+    // Per-sample traversal (same interface as GlobalSweep).
+    template <class Body>
+    __device__ __forceinline__ void operator()(int c, int k, double r, double r2, Body body) const {
+        PerSample<Body> pol{body};
+        rows(c, k, r, r2, pol);
+    }
+
+    // RT: the pre-computed rows of a translation-only sensor at scale k (all
+    // taps inside r_k by construction; masked samples contribute weight 0).
+    template <class Pol>
+    __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol) const {
+        const DevSensor &S = P.s[s];
+        const int pm = P.rt_period - 1;
+        const int cls = (py & pm) * P.rt_period + (px & pm);
+        const RtHeader &hd = *(const RtHeader *)rt;
+        const int r0 = hd.row0[s][c][cls], nr = hd.nrow[s][c][cls];
+        const TapRow *rows = (const TapRow *)(rt + sizeof(RtHeader));
+        const RowTap *taps =
+            (const RowTap *)(rt + sizeof(RtHeader) + (size_t)hd.n_rows * sizeof(TapRow));
+        const int pw = S.rw >> 1;
+        // the pixel's anchor: its own sensor pixel (sx = 1) or cell (sx = 1/2)
+        const int ax = px >> P.rt_shift, ay = py >> P.rt_shift;
+        const unsigned char *vb = sm + S.off_vi +
+                                  8 * (((ay - org[s][1]) >> 1) * pw + ((ax - org[s][0]) >> 1));
+        for (int ri = r0; ri < r0 + nr; ++ri) {
+            const TapRow &R = rows[ri];
+            const int lo = R.lo[k], hi = R.hi[k];
+            if (lo >= hi) continue;
+            const double dy = R.dy, dyy = dy * dy;
+            pol.begin_row(dy, dyy);
+            for (int t = R.first + lo; t < R.first + hi; ++t) {
+                const RowTap T = taps[t];
+                const float2 e = *(const float2 *)(vb + T.off);
+                pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f);
+            }
+            pol.end_row(dy, dyy);
+        }
+    }
+
+    // Traversal with row hooks: for separable sensors every sample of a row
+    // shares dy, so a policy can accumulate per-row sums (begin_row / sample /
+    // end_row); rotated sensors go through pol.general() per sample.
+    template <class Pol>
+    __device__ __forceinline__ void rows(int c, int k, double r, double r2, Pol &pol) const {
+        for (int s = 0; s < P.n_sensors; ++s) {
+            const DevSensor &S = P.s[s];
+            const int pm = S.phmask[c];
+            if (!pm) continue;
+            if constexpr (RT) {
+                // RT mode: every separable sensor is translation-only and tapped
+                if (S.separable) {
+                    tap_rows(s, c, k, pol);
+                    continue;
+                }
+            }
+            const int ox = org[s][0], oy = org[s][1];
+            const float2 *vi = (const float2 *)(sm + S.off_vi);
+            const double *tx0 = (const double *)(sm + S.off_tx0);
+            const double *ty4 = (const double *)(sm + S.off_ty4);
+            const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
+            int xlo, xhi, ylo, yhi;
+            window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
+            if (!RT && S.separable) {
+                for (int ph = 0; ph < 4; ++ph) {
+                    if (!((pm >> ph) & 1)) continue;
+                    const int py = ph >> 1, px = ph & 1;
+                    const int ys = ylo + ((py - ylo) & 1);
+                    const int xs0 = xlo + ((px - xlo) & 1);
+                    const int nc = xhi >= xs0 ? ((xhi - xs0) >> 1) + 1 : 0;
+                    for (int c0 = 0; c0 < nc; c0 += MAXC) {
+                        const int xs = xs0 + 2 * c0;
+                        double cdx[MAXC], cdxx[MAXC];
+#pragma unroll
+                        for (int i = 0; i < MAXC; ++i) {
+                            if (c0 + i < nc) {
+                                cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx);  // X(x) - qx
+                                cdxx[i] = __dmul_rn(cdx[i], cdx[i]);
+                            } else {
+                                // finite sentinel: never inside, and 0 * phi stays 0
+                                cdx[i] = 0.0;
+                                cdxx[i] = 1e150;  // (1e150)^2 stays finite: 0 * dx^4 = 0
+                            }
+                        }
+                        const int colbase = ph * plane + ((xs - ox) >> 1);
+                        for (int y = ys; y <= yhi; y += 2) {
+                            const int ly = y - oy;
+                            const double dy = __dsub_rn(ty4[ly], qy);  // Y(y) - qy
+                            const double dyy = __dmul_rn(dy, dy);
+                            if (dyy > r2) continue;
+                            const int rb = colbase + (ly >> 1) * pw;
+                            pol.begin_row(dy, dyy);
+                            // orders 0-1: branch-free over the row (candidates outside the
+                            // disk or without a sample contribute with weight 0); order 2
+                            // (27 DFMA per sample) only visits the samples inside.
+#pragma unroll
+                            for (int i = 0; i < MAXC; ++i) {
+                                const double d2 = __dadd_rn(cdxx[i], dyy);
+                                if constexpr (BRANCHY) {
+                                    if (d2 <= r2) {
+                                        const float2 e = vi[rb + i];
+                                        if (e.y > 0.f)
+                                            pol.sample(true, (double)e.x, e.y, cdx[i], dy, cdxx[i],
+                                                       dyy, (float)d2);
+                                    }
+                                } else {
+                                    const float2 e = vi[rb + i];
+                                    const bool ok = (d2 <= r2) && (e.y > 0.f);
+                                    pol.sample(ok, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy,
+                                               (float)d2);
+                                }
+                            }
+                            pol.end_row(dy, dyy);
+                        }
+                    }
+                }
+            } else {
+                const double *tx3 = (const double *)(sm + S.off_tx3);
+                const double *ty1 = (const double *)(sm + S.off_ty1);
+                const double T2 = S.T[2], T5 = S.T[5];
+                // sensor-space position of q relative to the bbox corner (fp32 pre-test)
+                const double u = qx - T2, v = qy - T5;
+                const float fcx = (float)(S.N[0] * u + S.N[1] * v - (double)xlo);
+                const float fcy = (float)(S.N[2] * u + S.N[3] * v - (double)ylo);
+                const float r2hi = (float)r2 + 1e-3f;
+                const float a0 = S.Tf[0], a1 = S.Tf[1], a3 = S.Tf[2], a4 = S.Tf[3];
+                for (int ph = 0; ph < 4; ++ph) {
+                    if (!((pm >> ph) & 1)) continue;
+                    const int py = ph >> 1, px = ph & 1;
+                    const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
+                    float ey = (float)(ys - ylo) - fcy;
+                    for (int y = ys; y <= yhi; y += 2, ey += 2.f) {
+                        const int ly = y - oy;
+                        const double t1y = ty1[ly], t4y = ty4[ly];
+                        const int rb = ph * plane + (ly >> 1) * pw - (ox >> 1);
+                        float ex = (float)(xs - xlo) - fcx;
+                        for (int x = xs; x <= xhi; x += 2, ex += 2.f) {
+                            const float fx = fmaf(a0, ex, a1 * ey), fy = fmaf(a3, ex, a4 * ey);
+                            if (fmaf(fx, fx, fy * fy) > r2hi) continue;
+                            const int k = rb + (x >> 1);
+                            const float2 e = vi[k];
+                            if (!(e.y > 0.f)) continue;
+                            const int lx = x - ox;
+                            const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
+                            const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
+                            const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                            const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
+                            const double d2 = __dadd_rn(dxx, dyy);
+                            if (d2 > r2) continue;
+                            pol.general(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                        }
+                    }
+                }
+            }
+        }
+    }
+};
+
+// Window weight (_kernels.py:164-168) W = exp(-dX^T Hinv dX), Hinv = I/h.
+// Fast path: fp32 MUFU ex2 (q <= 9 at the base/ICI radii).  Exact path:
+// float64 exp in the reference's operation order, because the radius ladder
+// reaches q ~ 1e2 where fp32 would underflow.
+template <bool EXACT>
+__device__ __forceinline__ double window_w(const DevParams &P, int c, int k, double dx, double dy,
+                                           float d2f) {
+    if constexpr (EXACT) {
+        const double hi = P.hinv[c][k];
+        const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
+        return exp(-q);
+    } else {
+        return (double)ex2_approx(-P.hl[c][k] * d2f);
+    }
+}
+
+// Row-factored moments (fast path, separable sensors).  Along a sensor row
+// dy is constant, so with phi_a = dx^i_a dy^j_a the row contributes
+//   A_ab += dy^(j_a+j_b) * S_(i_a+i_b),  b_a += dy^j_a * T_i_a,
+//   S_n = sum w dx^n (n <= 2*ORDER),  T_n = sum w y dx^n (n <= ORDER),
+// i.e. 2*ORDER+1 + ORDER+1 sums per sample instead of P(P+1)/2 + P.
+// Rotated sensors accumulate per sample.
+template <int ORDER>
+struct RowMoments {
+    static constexpr int PN = NC<ORDER>::P;
+    Acc<PN> &acc;
+    float hl;
+    double S[2 * ORDER + 1], T[ORDER + 1];
+    int cnt;
+    __device__ __forceinline__ void begin_row(double, double) {
+#pragma unroll
+        for (int n = 0; n <= 2 * ORDER; ++n) S[n] = 0.0;
+#pragma unroll
+        for (int n = 0; n <= ORDER; ++n) T[n] = 0.0;
+        cnt = 0;
+    }
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double,
+                                           double dxx, double, float d2f) {
+        const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
+        const double w = (double)w32, y = ok ? v : 0.0;
+        acc.sabs = fmaf(w32, fabsf((float)y), acc.sabs);
+        // w dx^n from independent products (dx^2 is the cached column square):
+        // dependency depth 2 instead of a 2*ORDER-long multiply chain
+        double p[5];
+        p[0] = w;
+        if (ORDER >= 1) {
+            p[1] = w * dx;
+            p[2] = w * dxx;
+        }
+        if (ORDER >= 2) {
+            p[3] = w * (dx * dxx);
+            p[4] = w * (dxx * dxx);
+        }
+#pragma unroll
+        for (int n = 0; n <= 2 * ORDER; ++n) {
+            S[n] += p[n];
+            if (n <= ORDER) T[n] = fma(p[n], y, T[n]);
+        }
+        cnt += ok ? 1 : 0;
+    }
+    __device__ __forceinline__ void end_row(double dy, double dyy) {
+        double dp[5];
+        dp[0] = 1.0;
+        dp[1] = dy;
+        dp[2] = dyy;
+        dp[3] = dyy * dy;
+        dp[4] = dyy * dyy;
+#pragma unroll
+        for (int a = 0; a < PN; ++a) {
+            const int ia = basis_i(a), ja = basis_j(a);
+            acc.b[a] = (ja == 0) ? acc.b[a] + T[ia] : fma(T[ia], dp[ja], acc.b[a]);
+        }
+        if constexpr (Acc<PN>::MOM) {
+            // moments M_ij += S_i dy^j, i + j <= 2 ORDER
+#pragma unroll
+            for (int d = 0; d <= 2 * ORDER; ++d)
+#pragma unroll
+                for (int j = 0; j <= d; ++j) {
+                    const int k = midx(d - j, j);
+                    acc.A[k] = j == 0 ? acc.A[k] + S[d - j] : fma(S[d - j], dp[j], acc.A[k]);
+                }
+        } else {
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < PN; ++a) {
+#pragma unroll
+                for (int bb = a; bb < PN; ++bb) {
+                    const int ii = basis_i(a) + basis_i(bb), jj = basis_j(a) + basis_j(bb);
+                    acc.A[k] = jj == 0 ? acc.A[k] + S[ii] : fma(S[ii], dp[jj], acc.A[k]);
+                    ++k;
+                }
+            }
+        }
+        acc.count += cnt;
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
+        const double y = ok ? v : 0.0;
+        acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+        acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+    }
+};
+
+// Row-factored variance sweep (ICI, fast path): phi.g = c0(dy) + dx (c1(dy) + g3 dx).
+// Also accumulates T = sum w |phi.g| |y| (fp32): the sharp precision bound of
+// c0 (fit_precise_sharp).
+template <int ORDER>
+struct RowVariance {
+    const double *g;
+    float hl;
+    bool sig;
+    double v, c0, c1;
+    float T;
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        c0 = g[0];
+        c1 = 0.0;
+        if (ORDER >= 1) {
+            c0 += g[2] * dy;
+            c1 = g[1];
+        }
+        if (ORDER >= 2) {
+            c0 += g[5] * dyy;
+            c1 += g[4] * dy;
+        }
+    }
+    __device__ __forceinline__ void end_row(double, double) {}
+    __device__ __forceinline__ void sample(bool ok, double y, float iv, double dx, double, double,
+                                           double, float d2f) {
+        const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+        const double t = (double)(sig ? W * W : W * W * iv);
+        double pg = c0;
+        if (ORDER == 1) pg = fma(dx, c1, c0);
+        if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
+        if (ok) {
+            v = fma(t, pg * pg, v);
+            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+        }
+    }
+    __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f) {
+        const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+        const double t = (double)(sig ? W * W : W * W * iv);
+        double pg = g[0];
+        if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
+        if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
+        if (ok) {
+            v = fma(t, pg * pg, v);
+            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+        }
+    }
+};
+
+template <class Sweep>
+struct HasRows {
+    static constexpr bool value = false;
+};
+template <int MAXC, bool BRANCHY, bool RT>
+struct HasRows<TileSweep<MAXC, BRANCHY, RT>> {
+    static constexpr bool value = true;
+};
+
+template <int ORDER, bool EXACT, class Sweep>
+__device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, double r, double r2,
+                                           const Sweep &sweep, Acc<NC<ORDER>::P> &acc) {
+    if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
+        acc.zero();
+        RowMoments<ORDER> pol{acc, P.hl[c][k]};
+        sweep.rows(c, k, r, r2, pol);
+        return;
+    }
+    acc.zero();
+    if constexpr (EXACT) {
+        const double hi = P.hinv[c][k];
+        sweep(c, k, r, r2, [&](bool, double v, auto iv, double dx, double dy, double dxx, double dyy,
+                            float) {
+            const double q =
+                __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
+            acc.add(exp(-q) * (double)iv, v, dx, dy, dxx, dyy);
+        });
+        sweep.reduce(acc);
+    } else {
+        const float hl = P.hl[c][k];
+        sweep(c, k, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
+                            double dyy, float d2f) {
+            const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;  // w = W / den
+            const double y = ok ? v : 0.0;
+            acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
+            acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+        });
+    }
+}
+
+// Variance of the constant term (ICI spec): v = sum w^2 var (phi . g)^2,
+// with w^2 var = W^2/den for variance weights and W^2 for sigma weights.
+template <int ORDER, bool EXACT, class Sweep>
+__device__ __forceinline__ double fit_variance(const DevParams &P, int c, int k, const Sweep &sweep,
+                                               const double *g, float *tsum = nullptr) {
+    if constexpr (!EXACT && ORDER >= 1 && HasRows<Sweep>::value) {
+        RowVariance<ORDER> pol{g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0, 0.f};
+        sweep.rows(c, k, P.r[c][k], P.r2[c][k], pol);
+        if (tsum) *tsum = pol.T;
+        return pol.v;
+    }
+    const bool sig = P.use_sigma;
+    const double hi = P.hinv[c][k];
+    const float hl = P.hl[c][k];
+    const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3], g4 = g[4], g5 = g[5];
+    double v = 0.0;
+    float T = 0.f;
+    sweep(c, k, P.r[c][k], P.r2[c][k],
+          [&](bool ok, double y, auto iv, double dx, double dy, double dxx, double dyy, float d2f) {
+              double t;
+              if constexpr (EXACT) {
+                  const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx),
+                                             __dmul_rn(__dmul_rn(hi, dy), dy));
+                  const double W = exp(-q);
+                  t = sig ? W * W : W * W * (double)iv;
+              } else {
+                  const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+                  t = (double)(sig ? W * W : W * W * iv);
+              }
+              double pg = g0;
+              if (ORDER >= 1) pg += dx * g1 + dy * g2;
+              if (ORDER >= 2) pg += dxx * g3 + __dmul_rn(dx, dy) * g4 + dyy * g5;
+              if (ok) v = fma(t, pg * pg, v);  // select: unused columns carry sentinels
+              if constexpr (!EXACT) {
+                  const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+                  if (ok) T = fmaf(W * (float)iv, fabsf((float)pg) * fabsf((float)y), T);
+              }
+          });
+    if (tsum) *tsum = T;
+    return sweep.reduce(v);
+}
+
+struct PixelResult {
+    double val, gx, gy;
+    int outcome;  // order*16 + radius step, or HDR_OUTCOME_NAN
+    int sidx;
+    int count;     // samples in the accepted window
+    int work = 0;  // inside-window samples over every moment sweep evaluated
+};
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+__device__ __forceinline__ void write_result(const DevParams &P, int pix, int c,
+                                             const PixelResult &R) {
+    const double v = R.val;
+    // np.maximum(val, 0).astype(float32) (lpa.py:428) keeps NaN
+    const float o = (v != v) ? __int_as_float(0x7fc00000) : __double2float_rn(fmax(v, 0.0));
+    P.rgb[(size_t)pix * 3 + c] = o;
+    const size_t plane = (size_t)P.out_w * P.out_h;
+    if (P.grad) {
+        P.grad[(size_t)(2 * c) * plane + pix] = (float)R.gx;
+        P.grad[(size_t)(2 * c + 1) * plane + pix] = (float)R.gy;
+    }
+    if (P.sidx) P.sidx[(size_t)c * plane + pix] = (uint8_t)R.sidx;
+    if (P.outcome) P.outcome[(size_t)c * plane + pix] = (uint8_t)R.outcome;
+    if (P.value) P.value[(size_t)c * plane + pix] = (float)v;
+    if (P.count) P.count[(size_t)c * plane + pix] = (uint16_t)min(R.count, 65535);
+    if (P.work) P.work[(size_t)c * plane + pix] = (uint32_t)R.work;
+}
+
+}  // namespace hdrlpa
