@@ -208,22 +208,27 @@ def test_errors_map_to_reference_exceptions(cuda):
         hl.ReconstructionParams(order=3)
 
 
-@pytest.mark.parametrize("rig_name,order,J,rows", [("aligned", 1, 1, (840, 856)),
-                                                  ("misaligned", 2, 4, (600, 612))])
-def test_full_size_band_parity(cuda, rig_name, order, J, rows):
-    """BASELINE cfg2 / cfg3 at their full 2400x1700 size: the whole frame is
-    reconstructed on the GPU (tiles, slow-path work list and escalations at
-    production scale) and a band of rows is checked against the oracle."""
+@pytest.mark.parametrize("rig_name,order,J,rows,n_sensors,up", [
+    ("aligned", 1, 1, (840, 856), 3, 1),      # cfg2
+    ("misaligned", 2, 4, (600, 612), 3, 1),   # cfg3
+    ("misaligned", 2, 4, (2001, 2009), 3, 2),  # cfg4: 4800x3400 output
+    ("misaligned", 2, 4, (1300, 1308), 4, 1),  # cfg5: 4 sensors
+])
+def test_full_size_band_parity(cuda, rig_name, order, J, rows, n_sensors, up):
+    """BASELINE cfg2-cfg5 at their full size: the whole frame is reconstructed
+    on the GPU (tiles, slow-path work list and escalations at production
+    scale) and a band of rows is checked against the oracle."""
     W, H = 2400, 1700
-    frames, cfgs, cals = _case(rig_name, W, H, seed=21)
+    frames, cfgs, cals = _case(rig_name, W, H, seed=21, n_sensors=n_sensors)
     p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
+    out_size = (W * up, H * up)
     dev = hl.frames_to_samples(frames, cfgs, cals).device()
-    out = dev.reconstruct((W, H), p, want_scale_idx=True, want_outcome=True)
+    out = dev.reconstruct(out_size, p, ref_size=(W, H), want_scale_idx=True, want_outcome=True)
     r0, r1 = rows
     got = {"rgb": out["rgb"][r0:r1].cpu().numpy(),
            "outcome": out["outcome"][:, r0:r1].cpu().numpy(),
            "scale_idx": out["scale_idx"][:, r0:r1].cpu().numpy()}
-    ref = oracle.reconstruct(frames, cfgs, cals, (W, H), p, rows=rows)
+    ref = oracle.reconstruct(frames, cfgs, cals, out_size, p, ref_size=(W, H), rows=rows)
     _check(got, ref)
 
 
