@@ -22,11 +22,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
         "r"(bytes)
         : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(
-                     smem_addr(bar))
-                 : "memory");
-}
 // Bounded wait: a barrier that never completes (a lost TMA transaction)
 // traps -- the launch fails with an error -- instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -42,15 +37,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if (spin > (1u << 24)) __trap();
     }
 }
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
-        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_addr(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParams &P, int tx0,
                                               int ty0, int tx1, int ty1, int &ox, int &oy) {
     // union of the window bboxes of the tile's corner queries at radius fast_R;

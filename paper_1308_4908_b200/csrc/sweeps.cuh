@@ -275,22 +275,6 @@ struct TileSweep {
     }
 };
 
-// Window weight (_kernels.py:164-168) W = exp(-dX^T Hinv dX), Hinv = I/h.
-// Fast path: fp32 MUFU ex2 (q <= 9 at the base/ICI radii).  Exact path:
-// float64 exp in the reference's operation order, because the radius ladder
-// reaches q ~ 1e2 where fp32 would underflow.
-template <bool EXACT>
-__device__ __forceinline__ double window_w(const DevParams &P, int c, int k, double dx, double dy,
-                                           float d2f) {
-    if constexpr (EXACT) {
-        const double hi = P.hinv[c][k];
-        const double q = __dadd_rn(__dmul_rn(__dmul_rn(hi, dx), dx), __dmul_rn(__dmul_rn(hi, dy), dy));
-        return exp(-q);
-    } else {
-        return (double)ex2_approx(-P.hl[c][k] * d2f);
-    }
-}
-
 // Row-factored moments (fast path, separable sensors).  Along a sensor row
 // dy is constant, so with phi_a = dx^i_a dy^j_a the row contributes
 //   A_ab += dy^(j_a+j_b) * S_(i_a+i_b),  b_a += dy^j_a * T_i_a,
