@@ -16,7 +16,8 @@ returns a :class:`RawFrameSet` -- the raw uint16 frames plus per-sensor
 scalars/planes -- which the CUDA kernels consume directly (mapping, masking
 and the radiometric conversion happen on the fly inside the reconstruction
 kernel).  :meth:`RawFrameSet.materialize` produces the reference's
-``RadianceSamples`` columns on the GPU when a caller needs them.
+``RadianceSamples`` columns (bit-exact, device-resident) when a caller needs
+them.
 """
 
 from __future__ import annotations
@@ -201,7 +202,9 @@ class RawFrameSet:
 
     def materialize(self, device=None):
         """The reference's ``RadianceSamples`` (sensor-major, raster order),
-        radiometry computed on the GPU from the raw frames (fp32-rounded)."""
+        computed and compacted on the GPU from the raw frames: values and
+        sigmas bit-identical to the reference's float64 columns
+        (``hdr_sample_planes``); the columns stay device-resident."""
         from .samples import RadianceSamples
 
         return RadianceSamples(*self.device(device).materialize_samples())
