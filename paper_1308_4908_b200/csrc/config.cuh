@@ -23,6 +23,10 @@ static const size_t WS_HEADER = 256;
 static_assert(sizeof(DevParams) + TAP_PARAM_BYTES <= 32764, "kernel parameter space");
 // plane buffers per CTA of the fast kernel's staging pipeline (measured: 3
 // buffers gain nothing on cfg2 and cost cfg3 5% through occupancy)
+// alternate the row parity each warp takes per tile (fast kernel)
+#ifndef HDR_ROW_ROT
+#define HDR_ROW_ROT 1
+#endif
 #ifndef HDR_NBUF
 #define HDR_NBUF 2
 #endif

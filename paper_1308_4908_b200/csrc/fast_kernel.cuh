@@ -142,12 +142,16 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
 template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT, bool STEER>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int t,
-                                             const int (*org)[2], bool tile_covered) {
+                                             const int (*org)[2], bool tile_covered,
+                                             int rot) {
     constexpr int PN = NC<ORDER>::P;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
     const int px = tx0 + (int)(threadIdx.x % TW);
-    const int py = ty0 + (int)(threadIdx.x / TW);
+    // warp w takes row w ^ rot: even and odd rows (different Bayer classes,
+    // different amounts of work) alternate between tiles, so no warp is
+    // systematically the slowest of its CTA
+    const int py = ty0 + ((int)(threadIdx.x / TW) ^ rot);
     if (px > tx1 || py > ty1) return;
     const int pix = py * P.out_w + px;
     const double qx = qcoord(px, P.sx), qy = qcoord(py, P.sy);
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
-        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0);
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0,
+                                                       HDR_ROW_ROT ? (i & 1) : 0);
         const int tn = t + NBUF * (int)gridDim.x;
         if (tn < ntiles) {  // CTA-uniform
             __syncwarp();
