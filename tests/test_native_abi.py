@@ -3,8 +3,10 @@ declared in include/hdr_lpa.h, struct layouts agree between C and ctypes,
 argument validation returns the documented status codes."""
 
 import ctypes
+import os
 import re
 import subprocess
+import sys
 from pathlib import Path
 
 import pytest
@@ -146,3 +148,15 @@ def test_status_codes_map_to_reference_exceptions():
     with pytest.raises(RuntimeError):
         N.check(N.HDR_ERR_CUDA, "x")
     N.check(N.HDR_OK, "x")
+
+
+def test_missing_native_library_fails_loudly():
+    """No CPU fallback: without the CUDA library the product path raises."""
+    code = ("import paper_1308_4908_b200 as hl\n"
+            "from paper_1308_4908_b200 import _native as N\n"
+            "N.lib()\n")
+    env = dict(os.environ, HDR_LPA_LIB=str(ROOT / "no_such_lib.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                       text=True)
+    assert r.returncode != 0
+    assert "no_such_lib.so" in r.stderr
