@@ -27,7 +27,7 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
     return v;
 }
 
-template <int ORDER>
+template <int ORDER, bool CNT>
 __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
                                                 const unsigned char *taps, const int (*org)[2],
                                                 int c, int px, int py, Acc<NC<ORDER>::P> &acc) {
@@ -60,12 +60,16 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
             const double dyy = ORDER >= 2 ? __dmul_rn(X.y, X.y) : 0.0;
             acc.add((double)w, (double)e.x, X.x, X.y, dxx, dyy, 0);
             // predicated increment (setp + @p add): one instruction less than a select
-            asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, 0f00000000;\n @p add.s32 %0, %0, 1;\n}"
-                : "+r"(count)
-                : "f"(w));
+            if constexpr (CNT)
+                asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, 0f00000000;\n @p add.s32 %0, %0, 1;\n}"
+                    : "+r"(count)
+                    : "f"(w));
         }
     }
-    acc.count = count;
+    // Without the count/work planes the count is not needed: a window with
+    // fewer than p weighted samples has a singular A, which the solve's
+    // positive-definiteness guards reject or route to the exact path.
+    acc.count = CNT ? count : 1 << 20;
     acc.sabs = sabs;
 }
 
@@ -139,7 +143,7 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
     }
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT, bool STEER>
+template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int t,
                                              const int (*org)[2], bool tile_covered,
@@ -196,7 +200,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
             } else {
                 Acc<PN> acc;
                 if constexpr (PAT)
-                    accumulate_taps<ORDER>(P, sm, taps, org, c, px, py, acc);
+                    accumulate_taps<ORDER, PAT == 1>(P, sm, taps, org, c, px, py, acc);
                 else
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 R.work = acc.count;
@@ -243,13 +247,15 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #ifndef HDR_PAT_MINBLOCKS
 #define HDR_PAT_MINBLOCKS 3
 #endif
-template <int ORDER, bool ICI, int MAXC, bool PAT, bool RT = false, bool STEER = false>
+// PAT: 0 no tap table, 1 taps (counting samples), 2 taps without the count
+// (no count/work output planes requested)
+template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
-                    typename std::conditional<PAT, TapParam, NoTaps>::type T) {
+                    typename std::conditional<(PAT != 0), TapParam, NoTaps>::type T) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];

@@ -116,7 +116,7 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
-template <int ORDER, bool ICI, int MAXC, bool PAT = false, bool RT = false, bool STEER = false>
+template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false>
 static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
     const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER>;
@@ -172,13 +172,14 @@ static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem
                       cudaStream_t st) {
     int rc;
     if (P.pat)
-        rc = launch_fast<ORDER, false, 4, true>(P, T, tiles, smem_bytes, st);
+        rc = (P.count || P.work) ? launch_fast<ORDER, false, 4, 1>(P, T, tiles, smem_bytes, st)
+                                 : launch_fast<ORDER, false, 4, 2>(P, T, tiles, smem_bytes, st);
     else if (P.rt && P.n_scales > 1)
-        rc = maxc <= 6 ? launch_fast<ORDER, true, 6, false, true>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, true, 8, false, true>(P, T, tiles, smem_bytes, st);
+        rc = maxc <= 6 ? launch_fast<ORDER, true, 6, 0, true>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, true, 8, 0, true>(P, T, tiles, smem_bytes, st);
     else if (P.rt)
-        rc = maxc <= 4 ? launch_fast<ORDER, false, 4, false, true>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, false, 8, false, true>(P, T, tiles, smem_bytes, st);
+        rc = maxc <= 4 ? launch_fast<ORDER, false, 4, 0, true>(P, T, tiles, smem_bytes, st)
+                       : launch_fast<ORDER, false, 8, 0, true>(P, T, tiles, smem_bytes, st);
     else if (P.n_scales > 1)
         rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, T, tiles, smem_bytes, st)
                        : launch_fast<ORDER, true, 8>(P, T, tiles, smem_bytes, st);
@@ -713,9 +714,9 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
         const int tiles = P.tiles_x * P.tiles_y;
         int rc2;
         switch (P.order) {
-            case 0: rc2 = launch_fast<0, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
-            case 1: rc2 = launch_fast<1, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
-            default: rc2 = launch_fast<2, false, 8, false, false, true>(P, T, tiles, smem_bytes, st); break;
+            case 0: rc2 = launch_fast<0, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
+            case 1: rc2 = launch_fast<1, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
+            default: rc2 = launch_fast<2, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
         }
         if (rc2 != HDR_OK) return rc2;
         if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;
