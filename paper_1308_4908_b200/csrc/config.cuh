@@ -27,6 +27,8 @@ static_assert(sizeof(DevParams) + TAP_PARAM_BYTES <= 32764, "kernel parameter sp
 #ifndef HDR_ROW_ROT
 #define HDR_ROW_ROT 1
 #endif
+// sensors of a tap-table (PAT) rig: per-pixel phase-plane bases in registers
+constexpr int PAT_MAXS = 4;
 #ifndef HDR_NBUF
 #define HDR_NBUF 2
 #endif

@@ -27,10 +27,25 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
     return v;
 }
 
+// the pixel's own position in each sensor's staged phase planes (origins are
+// even), computed once per pixel for all channels
+template <int NS>
+__device__ __forceinline__ void tap_bases(const DevParams &P, const unsigned char *sm,
+                                          const int (*org)[2], int px, int py, uint32_t (&vbs)[NS]) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        if (s >= P.n_sensors) break;
+        const DevSensor &S = P.s[s];
+        const int pw = S.rw >> 1;
+        vbs[s] = smem_addr(sm + S.off_vi) +
+                 8u * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+    }
+}
+
 template <int ORDER, bool CNT>
-__device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *sm,
-                                                const unsigned char *taps, const int (*org)[2],
-                                                int c, int px, int py, Acc<NC<ORDER>::P> &acc) {
+__device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsigned char *taps,
+                                                const uint32_t (&vbs)[PAT_MAXS], int c, int px,
+                                                int py, Acc<NC<ORDER>::P> &acc) {
     acc.zero();
     const int cls = ((py & 1) << 1) | (px & 1);
     // shared-window addresses: one LDS.128 (dx, dy), one LDS.64 (W, byte
@@ -39,15 +54,13 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
     const uint32_t tw = txy + (uint32_t)P.n_taps * (uint32_t)sizeof(TapXY);
     int count = 0;
     float sabs = 0.f;
-    for (int s = 0; s < P.n_sensors; ++s) {
+#pragma unroll
+    for (int s = 0; s < PAT_MAXS; ++s) {
+        if (s >= P.n_sensors) break;
         const int n = P.pat_cnt[s][c][py & 1];
-        if (!n) continue;
-        const DevSensor &S = P.s[s];
         const int o = P.pat_off[s][c][cls];
-        const int pw = S.rw >> 1;
-        // the pixel's own position in its phase plane (origins are even)
-        const uint32_t vb = smem_addr(sm + S.off_vi) +
-                            8u * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+        const uint32_t vb = vbs[s];
+#pragma unroll 4
         for (int t = o; t < o + n; ++t) {
             const double2 X = lds_d2(txy + 16u * (uint32_t)t);
             const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
@@ -172,6 +185,8 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     }
     const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org, qx, qy,
                                                                    px, py, taps};
+    uint32_t vbs[PAT_MAXS];
+    if constexpr (PAT) tap_bases<PAT_MAXS>(P, sm, org, px, py, vbs);
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
@@ -200,7 +215,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
             } else {
                 Acc<PN> acc;
                 if constexpr (PAT)
-                    accumulate_taps<ORDER, PAT == 1>(P, sm, taps, org, c, px, py, acc);
+                    accumulate_taps<ORDER, PAT == 1>(P, taps, vbs, c, px, py, acc);
                 else
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 R.work = acc.count;

@@ -347,7 +347,7 @@ static int upload_table(const std::vector<unsigned char> &table, unsigned char *
 
 static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
     taps.clear();
-    if (P.n_scales != 1 || P.sx != 1.0 || P.sy != 1.0) return false;
+    if (P.n_scales != 1 || P.sx != 1.0 || P.sy != 1.0 || P.n_sensors > PAT_MAXS) return false;
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
         if (!(S.T[0] == 1.0 && S.T[1] == 0.0 && S.T[3] == 0.0 && S.T[4] == 1.0)) return false;
