@@ -91,3 +91,57 @@ def test_random_steered_pass_parity(cuda, k):
         assert s["nan_map_equal"], s
         assert s["frac_over"] == 0 and s["max"] <= 1e-4, s
         assert int((out["outcome"][c].cpu().numpy() != oc).sum()) == 0
+
+
+@pytest.mark.parametrize("k", range(24))
+def test_random_affine_rig_parity(cuda, k):
+    """General affine rigs (translations of several pixels, rotations up to
+    5 deg, scales, shears), per-pixel calibration planes, defective pixels,
+    mixed exposure scalings and sensor sizes, 16-bit sensors."""
+    rng = np.random.default_rng(9000 + k)
+    W, H = int(rng.integers(48, 110)), int(rng.integers(40, 90))
+    n = int(rng.integers(2, 5))
+    bit16 = bool(rng.integers(0, 4) == 0)
+    sensors, noise, sizes = [], [], []
+    for i in range(n):
+        kind = int(rng.integers(0, 4))
+        if i == 0 or kind == 0:
+            T = sim.translate_T(*rng.uniform(-3, 3, 2)) if i else sim.identity_T()
+        elif kind == 1:
+            T = sim.rotate_T(float(rng.uniform(-5, 5)), W / 2, H / 2, *rng.uniform(-1, 1, 2))
+        elif kind == 2:
+            s = float(rng.uniform(0.95, 1.05))
+            T = np.array([[s, 0.0, float(rng.uniform(-1, 1))], [0.0, s, float(rng.uniform(-1, 1))]])
+        else:
+            sh = float(rng.uniform(-0.05, 0.05))
+            T = np.array([[1.0, sh, float(rng.uniform(-1, 1))], [0.0, 1.0, float(rng.uniform(-1, 1))]])
+        cfg = sim.kodak_sensor(i, float(2.0 ** -int(rng.integers(0, 10))), T)
+        if bit16:
+            cfg = dataclasses.replace(cfg, bit_depth=16, saturation_level=int(rng.integers(30000, 65536)))
+        if rng.integers(0, 3) == 0:
+            cfg = dataclasses.replace(cfg, defective=rng.choice(W * H, size=20, replace=False))
+        sensors.append(cfg)
+        noise.append(sim.kodak_noise())
+        sizes.append((W, H))
+    rig = sim.RigSpec(sensors=sensors, noise=noise, sensor_sizes=sizes, seed=int(rng.integers(0, 999)))
+    gt = sim.hdr_chart(W, H, top=float(rng.choice([4e5, 4e6])))
+    frames = sim.simulate_rig(gt, rig)
+    cals = rig.calibrations()
+    if rng.integers(0, 2) == 0:  # per-pixel calibration planes on one sensor
+        c0 = cals[0]
+        cals[0] = hl.NoiseCalibration(
+            bias=hl.FloatFrame(c0.bias.data + rng.uniform(-0.5, 0.5, c0.shape)),
+            readout_variance=hl.FloatFrame(c0.readout_variance.data * rng.uniform(0.9, 1.1, c0.shape)),
+            nonuniformity=hl.FloatFrame(rng.uniform(0.97, 1.03, c0.shape)))
+    p = hl.ReconstructionParams(order=int(rng.integers(0, 3)), scale=float(rng.choice([0.5, 0.7, 1.2])),
+                                ici_scales=int(rng.choice([1, 3])))
+    dev = hl.frames_to_samples(frames, sensors, cals).device()
+    out = dev.reconstruct((W, H), p, want_scale_idx=True, want_outcome=True)
+    got = {kk: v.cpu().numpy() for kk, v in out.items()}
+    ref = oracle.reconstruct(frames, sensors, cals, (W, H), p)
+    s = compare.summary(got["rgb"], ref["rgb"])
+    print(k, n, bit16, p, s)
+    assert s["nan_map_equal"], s
+    assert s["frac_over"] == 0 and s["max"] <= 1e-4, s
+    assert int((got["outcome"] != ref["outcome"]).sum()) == 0
+    assert int((got["scale_idx"] != ref["scale_idx"]).sum()) == 0
