@@ -266,3 +266,27 @@ def test_aligned_coincident_samples_at_corner(cuda):
     got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), (96, 64), p)
     assert ref["outcome"][2, 0, 0] == 17  # order 1, radius step 1
     _check(got, ref)
+
+
+@pytest.mark.parametrize("n_sensors,order,J", [(1, 1, 1), (1, 2, 3), (8, 1, 1), (8, 2, 4)])
+def test_sensor_count_extremes(cuda, n_sensors, order, J):
+    """One sensor (no HDR fusion) and the ABI's maximum of eight sensors
+    (translations, rotations and exposures mixed)."""
+    import dataclasses
+
+    W, H = 72, 56
+    gt = sim.hdr_chart(W, H)
+    base = sim.baseline_rig("misaligned", W, H, seed=40, n_sensors=4)
+    sensors, noise = [], []
+    for i in range(n_sensors):
+        src = base.sensors[i % 4]
+        T = np.array(src.transform, dtype=float)
+        T[:, 2] += (0.13 * (i // 4), -0.07 * (i // 4))
+        sensors.append(dataclasses.replace(src, sensor_id=i, transform=T,
+                                           exposure_scaling=2.0 ** -(i % 6)))
+        noise.append(base.noise[i % 4])
+    rig = sim.RigSpec(sensors=sensors, noise=noise, sensor_sizes=[(W, H)] * n_sensors, seed=3)
+    frames = sim.simulate_rig(gt, rig)
+    p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
+    got, ref, _ = _run(frames, sensors, rig.calibrations(), (W, H), p)
+    _check(got, ref)
