@@ -42,7 +42,7 @@ extern "C" {
 
 #define HDR_LPA_MAX_SENSORS 8
 #define HDR_LPA_MAX_SCALES 8
-#define HDR_LPA_ABI_VERSION 3
+#define HDR_LPA_ABI_VERSION 4
 
 /* status codes */
 #define HDR_OK 0
@@ -120,6 +120,12 @@ typedef struct HdrOutputs {
     uint32_t *work;             /* nullable: [3][out_h][out_w] inside-window samples summed over
                                    every moment sweep evaluated (all ICI scales / ladder steps):
                                    the algorithmic work behind the pixel (ABI v3) */
+    uint16_t *rgb_half;         /* nullable: out_h*out_w*3 HWC IEEE fp16 of
+                                   max(val,0)*half_scale (NaN kept) -- half the bytes of rgb for
+                                   streaming/display (ABI v4).  rgb may be NULL
+                                   when rgb_half is given. */
+    float half_scale;           /* scale applied before the fp16 rounding (e.g. 1/16 keeps
+                                   radiance up to ~1e6 e/s inside fp16's range) */
 } HdrOutputs;
 
 /* Bytes of device workspace hdr_lpa_reconstruct needs for these sensors and

@@ -92,6 +92,8 @@ class HdrOutputs(ctypes.Structure):
         ("value", ctypes.c_void_p),
         ("count", ctypes.c_void_p),
         ("work", ctypes.c_void_p),
+        ("rgb_half", ctypes.c_void_p),
+        ("half_scale", ctypes.c_float),
     ]
 
 
@@ -182,7 +184,7 @@ def lib():
                     getattr(L, name).restype = ctypes.c_int
             L.hdr_lpa_launch_count.restype = ctypes.c_ulonglong
             L.hdr_lpa_launch_count.argtypes = []
-            if L.hdr_lpa_abi_version() != 3:
+            if L.hdr_lpa_abi_version() != 4:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L
         return _lib

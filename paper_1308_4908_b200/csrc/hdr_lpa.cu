@@ -469,7 +469,9 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
                         int out_w, int out_h, double ref_w, double ref_h, int row_begin,
                         int row_end, const HdrOutputs *out, void *workspace,
                         size_t workspace_bytes, DevParams &P, double &fastR) {
-    if (!sensors || !params || !out || !out->rgb || !workspace) return HDR_ERR_ARG;
+    if (!sensors || !params || !out || (!out->rgb && !out->rgb_half) || !workspace)
+        return HDR_ERR_ARG;
+    if (out->rgb_half && !(out->half_scale > 0.f)) return HDR_ERR_ARG;
     if (n_sensors < 1 || n_sensors > MAXS) return HDR_ERR_ARG;
     if (out_w <= 0 || out_h <= 0 || !(ref_w > 0) || !(ref_h > 0)) return HDR_ERR_ARG;
     if (params->order < 0 || params->order > 2) return HDR_ERR_ARG;
@@ -526,6 +528,8 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
         }
     P.fast_R = fastR;
     P.rgb = out->rgb;
+    P.rgb_half = out->rgb_half;
+    P.half_scale = out->half_scale;
     P.grad = out->grad;
     P.sidx = out->scale_idx;
     P.outcome = out->outcome;

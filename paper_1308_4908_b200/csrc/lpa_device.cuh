@@ -120,6 +120,8 @@ struct DevParams {
     double max_radius, cond, gamma;
     double fast_R;            // radius the staged tiles cover
     float *rgb;
+    uint16_t *rgb_half;       // optional fp16 copy (scaled)
+    float half_scale;
     float *grad;
     uint8_t *sidx;
     uint8_t *outcome;

@@ -190,10 +190,14 @@ class DeviceRig:
 
     def allocate_outputs(self, out_size, want_grad=False, want_scale_idx=False,
                          want_outcome=False, raw_value=False, want_count=False,
-                         want_work=False):
+                         want_work=False, rgb_half=False, want_rgb=True):
         out_w, out_h = out_size
         dev = self.device
-        out = {"rgb": torch.empty((out_h, out_w, 3), dtype=torch.float32, device=dev)}
+        out = {}
+        if want_rgb or not rgb_half:
+            out["rgb"] = torch.empty((out_h, out_w, 3), dtype=torch.float32, device=dev)
+        if rgb_half:  # fp16 copy of the clamped radiance times half_scale (ABI v4)
+            out["rgb_half"] = torch.empty((out_h, out_w, 3), dtype=torch.float16, device=dev)
         if want_grad:
             out["grad"] = torch.empty((3, 2, out_h, out_w), dtype=torch.float32, device=dev)
         if want_scale_idx:
@@ -210,7 +214,8 @@ class DeviceRig:
 
     def reconstruct(self, out_size, params: ReconstructionParams, ref_size=None, rows=None,
                     want_grad=False, want_scale_idx=False, want_outcome=False, raw_value=False,
-                    want_count=False, want_work=False, out=None, stream=None, flags=0):
+                    want_count=False, want_work=False, out=None, stream=None, flags=0,
+                    half_scale=1.0 / 16):
         """Launch the reconstruction on the current (or given) stream.
 
         Returns the dict of output tensors (``rgb`` (H, W, 3) float32 and the
@@ -225,7 +230,10 @@ class DeviceRig:
             out = self.allocate_outputs((out_w, out_h), want_grad, want_scale_idx,
                                         want_outcome, raw_value, want_count, want_work)
         o = N.HdrOutputs()
-        o.rgb = out["rgb"].data_ptr()
+        o.rgb = out["rgb"].data_ptr() if "rgb" in out else None
+        if "rgb_half" in out:
+            o.rgb_half = out["rgb_half"].data_ptr()
+            o.half_scale = float(half_scale)
         o.grad = out["grad"].data_ptr() if "grad" in out else None
         o.scale_idx = out["scale_idx"].data_ptr() if "scale_idx" in out else None
         o.outcome = out["outcome"].data_ptr() if "outcome" in out else None
@@ -276,7 +284,7 @@ class DeviceRig:
         return out
 
     def capture(self, out_size, params: ReconstructionParams, ref_size=None, out=None,
-                **want) -> "CapturedReconstruction":
+                half_scale=1.0 / 16, **want) -> "CapturedReconstruction":
         """Record one reconstruction (pre-pass, fast and slow kernels) as a CUDA
         graph over this rig's current frame buffers: ``replay()`` re-runs it
         with one launch.  Refill the frames in place (``copy_`` into
@@ -287,13 +295,14 @@ class DeviceRig:
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         # one eager run first: workspace allocation, kernel attributes
-        self.reconstruct(out_size, params, ref_size=ref_size, out=out, stream=side)
+        self.reconstruct(out_size, params, ref_size=ref_size, out=out, stream=side,
+                         half_scale=half_scale)
         side.synchronize()
         graph = torch.cuda.CUDAGraph()
         n0 = N.lib().hdr_lpa_launch_count()
         with torch.cuda.graph(graph, stream=side):
             self.reconstruct(out_size, params, ref_size=ref_size, out=out,
-                             stream=torch.cuda.current_stream(self.device))
+                             stream=torch.cuda.current_stream(self.device), half_scale=half_scale)
         n_kernels = int(N.lib().hdr_lpa_launch_count() - n0)
         return CapturedReconstruction(graph, out, n_kernels, list(self.raws))
 

@@ -20,7 +20,7 @@ from .lpa import ReconstructionParams
 class FramePipeline:
     def __init__(self, configs, cals, sensor_shapes, out_size, params: ReconstructionParams,
                  ref_size=None, device=None, slots: int = 2, d2h_streams: int = 1,
-                 graphs: bool = True):
+                 graphs: bool = True, output: str = "float32", half_scale: float = 1.0 / 16):
         self.device = torch.device(device if device is not None else
                                    torch.device("cuda", torch.cuda.current_device()))
         self.out_size = (int(out_size[0]), int(out_size[1]))
@@ -34,10 +34,19 @@ class FramePipeline:
         ws = self.rigs[0].workspace(*self.out_size)
         for r in self.rigs[1:]:
             r._workspaces[self.out_size] = ws
-        self.outs = [self.rigs[0].allocate_outputs(self.out_size) for _ in range(slots)]
+        if output not in ("float32", "float16"):
+            raise ValueError(f"output must be float32 or float16, got {output!r}")
+        # float16: the streaming format of SURVEY s8(f)-3 -- max(val, 0) * half_scale
+        # rounded to IEEE half on the device, half the PCIe download
+        self.key = "rgb" if output == "float32" else "rgb_half"
+        self.outs = [self.rigs[0].allocate_outputs(self.out_size, rgb_half=output == "float16",
+                                                   want_rgb=output == "float32")
+                     for _ in range(slots)]
+        self.half_scale = half_scale
         # per slot, the reconstruction recorded once as a CUDA graph (its frame
         # buffers are the slot's fixed upload targets): one launch per frame
-        self.captured = [rig.capture(self.out_size, params, ref_size=ref_size, out=o)
+        self.captured = [rig.capture(self.out_size, params, ref_size=ref_size, out=o,
+                                     half_scale=half_scale)
                          for rig, o in zip(self.rigs, self.outs)] if graphs else None
         self.s_in = torch.cuda.Stream(self.device)
         self.s_comp = torch.cuda.Stream(self.device)
@@ -58,7 +67,8 @@ class FramePipeline:
 
     @property
     def d2h_bytes(self) -> int:
-        return self.outs[0]["rgb"].numel() * 4
+        t = self.outs[0][self.key]
+        return t.numel() * t.element_size()
 
     def submit(self, host_raws, host_rgb):
         """Queue one frame: ``host_raws`` pinned int16 (h, w) tensors, result
@@ -78,16 +88,17 @@ class FramePipeline:
                 self.captured[k].replay()
             else:
                 self.rigs[k].reconstruct(self.out_size, self.params, ref_size=self.ref_size,
-                                         out=self.outs[k], stream=self.s_comp)
+                                         out=self.outs[k], stream=self.s_comp,
+                                         half_scale=self.half_scale)
             self.ev_comp[k].record(self.s_comp)
             self.ev_free[k] = self.ev_comp[k]
         streams = [self.s_out] + self.s_out_extra
-        rows = self.outs[k]["rgb"].shape[0]
+        rows = self.outs[k][self.key].shape[0]
         cuts = [rows * i // len(streams) for i in range(len(streams) + 1)]
         for j, s in enumerate(streams):
             with torch.cuda.stream(s):
                 s.wait_event(self.ev_comp[k])
-                host_rgb[cuts[j]:cuts[j + 1]].copy_(self.outs[k]["rgb"][cuts[j]:cuts[j + 1]],
+                host_rgb[cuts[j]:cuts[j + 1]].copy_(self.outs[k][self.key][cuts[j]:cuts[j + 1]],
                                                     non_blocking=True)
         for s in self.s_out_extra:
             self.s_out.wait_stream(s)

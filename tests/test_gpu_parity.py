@@ -290,3 +290,28 @@ def test_sensor_count_extremes(cuda, n_sensors, order, J):
     p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
     got, ref, _ = _run(frames, sensors, rig.calibrations(), (W, H), p)
     _check(got, ref)
+
+
+def test_fp16_streaming_output(cuda):
+    """rgb_half (ABI v4) is the float32 output times half_scale rounded to
+    IEEE half, NaN kept; the pipeline streams it."""
+    import torch
+
+    frames, cfgs, cals = _case("misaligned", 80, 56, seed=50)
+    dev = hl.frames_to_samples(frames, cfgs, cals).device()
+    p = hl.ReconstructionParams(order=1, scale=0.7)
+    out = dev.reconstruct((80, 56), p, out=dev.allocate_outputs((80, 56), rgb_half=True),
+                          half_scale=1.0 / 16)
+    want = (out["rgb"] * (1.0 / 16)).half()
+    got = out["rgb_half"]
+    assert torch.equal(torch.isnan(got), torch.isnan(want))
+    assert torch.equal(torch.nan_to_num(got, nan=-1.0), torch.nan_to_num(want, nan=-1.0))
+    from paper_1308_4908_b200.pipeline import FramePipeline
+
+    pipe = FramePipeline(cfgs, cals, [f.data.shape for f in frames], (80, 56), p,
+                         output="float16")
+    host = [torch.from_numpy(f.data.view(np.int16)).pin_memory() for f in frames]
+    res = torch.empty((56, 80, 3), dtype=torch.float16).pin_memory()
+    pipe.submit(host, res)
+    pipe.synchronize()
+    assert torch.equal(torch.nan_to_num(res, nan=-1.0), torch.nan_to_num(want.cpu(), nan=-1.0))
