@@ -413,10 +413,24 @@ def run_ours(args, wl, world, rank, local):
     from paper_1308_4908_b200.engine import DeviceRig
     from paper_1308_4908_b200.pipeline import FramePipeline
 
+    # one process per GPU; HDR_DIST_BACKEND=gloo (CPU collectives) lets the
+    # multi-rank code path be exercised with several ranks sharing a GPU
+    backend = os.environ.get("HDR_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     W, H = wl["size"]
     out_w, out_h = wl["out"]
     params = _params(wl)
@@ -464,12 +478,7 @@ def run_ours(args, wl, world, rank, local):
             fn(i)
         e1.record(stream)
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return max_over_ranks(e0.elapsed_time(e1))
 
     for i in range(args.warmup):
         step(i)
@@ -543,11 +552,7 @@ def run_ours(args, wl, world, rank, local):
     e1.record(pipe.s_in)
     pipe.synchronize()
     barrier()
-    ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
     fps_e2e = world * args.steps / (ms_e2e / 1e3)
 
     # the same pipeline with the fp16 streaming output:
@@ -567,11 +572,7 @@ def run_ours(args, wl, world, rank, local):
     e1.record(pipe_h.s_in)
     pipe_h.synchronize()
     barrier()
-    ms_half = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_half], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_half = float(t.item())
+    ms_half = max_over_ranks(e0.elapsed_time(e1))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

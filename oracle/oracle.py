@@ -135,7 +135,12 @@ def has_lapack() -> bool:
 
 
 def max_threads() -> int:
-    return int(_load().oracle_max_threads())
+    """Host cores this process may use (not OMP_NUM_THREADS, which launchers
+    such as torchrun set to 1 per process)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return int(_load().oracle_max_threads())
 
 
 def _pattern_name(pattern) -> str:
