@@ -42,6 +42,17 @@ def hdr_params(params: ReconstructionParams, flags: int = 0) -> N.HdrParams:
     return P
 
 
+# one hdr_lpa_reconstruct call covers < 2^26 output pixels (work-item packing,
+# include/hdr_lpa.h); larger outputs are split into row bands here
+MAX_BAND_PIXELS = (1 << 26) - 1
+
+
+def band_split(r0: int, r1: int, out_w: int):
+    """Row bands [b0, b1) of at most MAX_BAND_PIXELS output pixels covering [r0, r1)."""
+    step = max(1, MAX_BAND_PIXELS // max(1, out_w))
+    return [(b, min(b + step, r1)) for b in range(r0, r1, step)]
+
+
 class DeviceRig:
     """Sensors of one rig resident on a CUDA device.
 
@@ -243,12 +254,14 @@ class DeviceRig:
         ws = self.workspace(out_w, out_h)
         r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        hp = hdr_params(params, flags)
         with torch.cuda.device(self.device):
-            rc = N.lib().hdr_lpa_reconstruct(
-                self._sensors, len(self.raws), ctypes.byref(hdr_params(params, flags)),
-                out_w, out_h, float(ref_size[0]), float(ref_size[1]), r0, r1,
-                ctypes.byref(o), ws.data_ptr(), ws.numel(), st.cuda_stream)
-        N.check(rc, "hdr_lpa_reconstruct")
+            for b0, b1 in band_split(r0, r1, out_w):  # stream-ordered, one workspace
+                rc = N.lib().hdr_lpa_reconstruct(
+                    self._sensors, len(self.raws), ctypes.byref(hp), out_w, out_h,
+                    float(ref_size[0]), float(ref_size[1]), b0, b1, ctypes.byref(o),
+                    ws.data_ptr(), ws.numel(), st.cuda_stream)
+                N.check(rc, "hdr_lpa_reconstruct")
         return out
 
     def reconstruct_steered(self, out_size, params: ReconstructionParams, field, ref_size=None,
@@ -275,12 +288,14 @@ class DeviceRig:
         ws = self.workspace(out_w, out_h)
         r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        hp = hdr_params(params)
         with torch.cuda.device(self.device):
-            rc = N.lib().hdr_lpa_reconstruct_steered(
-                self._sensors, len(self.raws), ctypes.byref(hdr_params(params)),
-                ctypes.byref(steer), out_w, out_h, float(ref_size[0]), float(ref_size[1]), r0, r1,
-                ctypes.byref(o), ws.data_ptr(), ws.numel(), st.cuda_stream)
-        N.check(rc, "hdr_lpa_reconstruct_steered")
+            for b0, b1 in band_split(r0, r1, out_w):
+                rc = N.lib().hdr_lpa_reconstruct_steered(
+                    self._sensors, len(self.raws), ctypes.byref(hp), ctypes.byref(steer), out_w,
+                    out_h, float(ref_size[0]), float(ref_size[1]), b0, b1, ctypes.byref(o),
+                    ws.data_ptr(), ws.numel(), st.cuda_stream)
+                N.check(rc, "hdr_lpa_reconstruct_steered")
         return out
 
     def capture(self, out_size, params: ReconstructionParams, ref_size=None, out=None,

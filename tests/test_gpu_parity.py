@@ -315,3 +315,21 @@ def test_fp16_streaming_output(cuda):
     pipe.submit(host, res)
     pipe.synchronize()
     assert torch.equal(torch.nan_to_num(res, nan=-1.0), torch.nan_to_num(want.cpu(), nan=-1.0))
+
+
+def test_output_larger_than_one_call(cuda):
+    """An output of more than 2^26 pixels (the per-call work-item limit) is
+    split into row bands by the engine; every band matches the oracle."""
+    W, H = 96, 64
+    frames, cfgs, cals = _case("misaligned", W, H, seed=60)
+    out_size = (8704, 8192)  # 71.3 M pixels
+    p = hl.ReconstructionParams(order=1, scale=0.7)
+    dev = hl.frames_to_samples(frames, cfgs, cals).device()
+    out = dev.reconstruct(out_size, p, ref_size=(W, H), want_outcome=True)
+    for rows in ((0, 2), (7709, 7711), (8190, 8192)):  # the second band starts at row 7710
+        got = {"rgb": out["rgb"][rows[0]:rows[1]].cpu().numpy(),
+               "outcome": out["outcome"][:, rows[0]:rows[1]].cpu().numpy()}
+        ref = oracle.reconstruct(frames, cfgs, cals, out_size, p, ref_size=(W, H), rows=rows)
+        s = compare.summary(got["rgb"], ref["rgb"])
+        assert s["nan_map_equal"] and s["frac_over"] == 0 and s["max"] <= 1e-4, s
+        assert int((got["outcome"] != ref["outcome"]).sum()) == 0

@@ -227,3 +227,14 @@ class TestRigSchema:
         for p in sorted(Path("/root/reference/pkg/configs").glob("*.json")):
             r = rigmod.load_rig(p)
             assert r.params().order in (0, 1, 2)
+
+
+def test_band_split_limits_pixels_per_call():
+    from paper_1308_4908_b200.engine import MAX_BAND_PIXELS, band_split
+
+    for out_w, r0, r1 in ((2400, 0, 1700), (16384, 0, 8192), (9000, 37, 9001), (70000000, 0, 3)):
+        bands = band_split(r0, r1, out_w)
+        assert bands[0][0] == r0 and bands[-1][1] == r1
+        assert all(a[1] == b[0] for a, b in zip(bands, bands[1:]))
+        assert all((b1 - b0) * out_w <= MAX_BAND_PIXELS or b1 - b0 == 1 for b0, b1 in bands)
+    assert band_split(0, 1700, 2400) == [(0, 1700)]
