@@ -333,3 +333,20 @@ def test_output_larger_than_one_call(cuda):
         s = compare.summary(got["rgb"], ref["rgb"])
         assert s["nan_map_equal"] and s["frac_over"] == 0 and s["max"] <= 1e-4, s
         assert int((got["outcome"] != ref["outcome"]).sum()) == 0
+
+
+@pytest.mark.parametrize("top,order,J", [(30.0, 1, 1), (30.0, 2, 4), (3e9, 1, 1), (3e9, 2, 3)])
+def test_extreme_scenes(cuda, top, order, J):
+    """Near-black scenes (radiance around the noise floor: many negative
+    samples, where the relative-error floor matters) and blinding scenes
+    (every sensor but the shortest exposure saturated; NaN where none is
+    left)."""
+    W, H = 80, 60
+    gt = sim.hdr_chart(W, H, top=top)
+    if top < 100:
+        gt = hl.HDRImage(gt.data * (top / float(np.nanmax(gt.data))))
+    rig = sim.baseline_rig("misaligned", W, H, seed=70)
+    frames = sim.simulate_rig(gt, rig)
+    p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
+    got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), (W, H), p)
+    _check(got, ref)
