@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];
     __shared__ unsigned s_done[NBUF];
+    __shared__ int s_tile[NBUF];
     __shared__ __align__(8) uint64_t bar_full[NBUF];
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
@@ -290,7 +291,6 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         const int n16 = (P.tab_bytes + 15) / 16;
         for (int i = threadIdx.x; i < n16; i += NT) dst[i] = __ldg(src + i);
     }
-    int t = blockIdx.x;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int b = 0; b < NBUF; ++b) {
@@ -300,40 +300,51 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();  // barriers initialised, taps staged
-    // prologue: warp 0 stages this CTA's first NBUF tiles
+    // Tiles are handed out dynamically from a global counter (the workspace
+    // header): a CTA whose tiles were cheap takes more, so all CTAs finish
+    // together.  The staging warp takes the next index, publishes it in
+    // s_tile[b] and releases it with the buffer's mbarrier (a plain arrive, no
+    // copies, when the counter is exhausted: s_tile = -1 ends the loop).
+    auto refill = [&](int b) {  // one whole warp
+        int tn = 0;
+        if ((threadIdx.x & 31) == 0) tn = (int)atomicAdd(P.tile_counter, 1u);
+        tn = __shfl_sync(0xffffffffu, tn, 0);
+        if (tn < ntiles) {
+            if ((threadIdx.x & 31) == 0) s_tile[b] = tn;
+            stage_tile<!PAT>(P, planes + b * P.buf_stride, tn, s_org[b], &s_cov[b], &bar_full[b]);
+        } else if ((threadIdx.x & 31) == 0) {
+            s_tile[b] = -1;
+            mbar_expect_tx(&bar_full[b], 0);
+        }
+    };
     if (threadIdx.x < 32) {
 #pragma unroll
-        for (int b = 0; b < NBUF; ++b)
-            if (t + b * (int)gridDim.x < ntiles)
-                stage_tile<!PAT>(P, planes + b * P.buf_stride, t + b * gridDim.x, s_org[b],
-                                 &s_cov[b], &bar_full[b]);
+        for (int b = 0; b < NBUF; ++b) refill(b);
     }
     // No CTA-wide barrier in the loop: a warp waits only for its tile's data.
-    // The LAST warp to finish tile t (buffer b) refills b with tile t + NBUF*G,
-    // so warps that finish early run up to NBUF-1 tiles ahead instead of idling
-    // at a __syncthreads while the slowest warp of the tile completes.
+    // The LAST warp to finish the tile of buffer b refills b, so warps that
+    // finish early run up to NBUF-1 tiles ahead instead of idling at a
+    // __syncthreads while the slowest warp of the tile completes.
     constexpr int NWARPS = NT / 32;
-    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+    for (int i = 0;; ++i) {
         const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
+        const int t = s_tile[b];
+        if (t < 0) break;
         tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0,
                                                        HDR_ROW_ROT ? (i & 1) : 0);
-        const int tn = t + NBUF * (int)gridDim.x;
-        if (tn < ntiles) {  // CTA-uniform
-            __syncwarp();
-            unsigned last = 0;
-            if ((threadIdx.x & 31) == 0) {
-                __threadfence_block();  // this warp's reads of buffer b precede the count
-                last = atomicAdd(&s_done[b], 1u) == NWARPS - 1;
-                if (last) {
-                    s_done[b] = 0;
-                    __threadfence_block();
-                }
+        __syncwarp();
+        unsigned last = 0;
+        if ((threadIdx.x & 31) == 0) {
+            __threadfence_block();  // this warp's reads of buffer b precede the count
+            last = atomicAdd(&s_done[b], 1u) == NWARPS - 1;
+            if (last) {
+                s_done[b] = 0;
+                __threadfence_block();
             }
-            if (__shfl_sync(0xffffffffu, last, 0))
-                stage_tile<!PAT>(P, pb, tn, s_org[b], &s_cov[b], &bar_full[b]);
         }
+        if (__shfl_sync(0xffffffffu, last, 0)) refill(b);
     }
 }
 
