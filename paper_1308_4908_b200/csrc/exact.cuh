@@ -131,9 +131,15 @@ template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
     constexpr int G = SLOW_LANES;  // lanes per work item
     const uint32_t n = *P.work_count;
-    const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const uint32_t ngrp = (gridDim.x * blockDim.x) / G;
-    for (uint32_t i = grp; i < n; i += ngrp) {
+    // items are fetched dynamically (their cost varies by orders of magnitude)
+    const unsigned gmask = G >= 32 ? 0xffffffffu
+                                   : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+    const int leader = (threadIdx.x & 31) & ~(G - 1);
+    for (;;) {
+        uint32_t i = 0;
+        if ((threadIdx.x & (G - 1)) == 0) i = atomicAdd(P.slow_counter, 1u);
+        i = __shfl_sync(gmask, i, leader);
+        if (i >= n) break;
         const uint32_t item = P.work_items[i];
         const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
         const int kk = (int)((item >> 2) & 15);

@@ -539,6 +539,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.flags = params->flags;
     P.work_count = (uint32_t *)workspace;
     P.tile_counter = (uint32_t *)workspace + 1;
+    P.slow_counter = (uint32_t *)workspace + 2;
     P.rt_global = (const unsigned char *)workspace + WS_HEADER;
     char *wsp = (char *)workspace + WS_HEADER + RT_TABLE_BYTES;
     for (int s = 0; s < n_sensors; ++s) {
@@ -670,7 +671,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.tiles_y = (row_end - row_begin + TH - 1) / TH;
     P.tiles_x = (out_w + TW - 1) / TW;
     const int tiles = P.tiles_x * P.tiles_y;
-    if (cudaMemsetAsync(workspace, 0, 2 * sizeof(uint32_t), st) != cudaSuccess)
+    if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (P.rt && upload_table(rt_table, (unsigned char *)P.rt_global, st) != HDR_OK)
         return HDR_ERR_CUDA;
@@ -707,7 +708,7 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     P.fast_R = P.max_radius;
     const bool staged =
         setup_staging(P, n_sensors, P.max_radius, false, T, rt_table, smem_bytes, maxc) == HDR_OK;
-    if (cudaMemsetAsync(workspace, 0, 2 * sizeof(uint32_t), st) != cudaSuccess)
+    if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148;

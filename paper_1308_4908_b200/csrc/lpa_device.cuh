@@ -139,6 +139,7 @@ struct DevParams {
     int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
     uint32_t *work_count;
     uint32_t *tile_counter;          // fast kernel: next tile to hand out (workspace header)
+    uint32_t *slow_counter;          // exact path: next work item to evaluate
     uint32_t *work_items;
     // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)
     const double *st_theta, *st_sigma, *st_gamma;
