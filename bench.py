@@ -550,17 +550,18 @@ def run_ours(args, wl, world, rank, local):
     # end to end through the public pipeline API: pinned host frames in, pinned RGB out
     host_sets = [[t.cpu().pin_memory() for t in fs] for fs in frame_sets]
     host_out = [torch.empty((out_h, out_w, 3), dtype=torch.float32).pin_memory()
-                for _ in range(2)]
+                for _ in range(max(2, args.e2e_slots))]
     pipe = FramePipeline(rigspec.sensors, cals, [tuple(t.shape) for t in frame_sets[0]],
-                         (out_w, out_h), params, ref_size=(W, H), device=dev)
+                         (out_w, out_h), params, ref_size=(W, H), device=dev,
+                         slots=args.e2e_slots)
     for i in range(args.warmup):
-        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % 2])
+        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % len(host_out)])
     pipe.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(pipe.s_in)
     for i in range(args.steps):
-        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % 2])
+        pipe.submit(host_sets[i % N_DISTINCT], host_out[i % len(host_out)])
     pipe.s_in.wait_stream(pipe.s_out)
     e1.record(pipe.s_in)
     pipe.synchronize()
@@ -573,7 +574,8 @@ def run_ours(args, wl, world, rank, local):
     host_half = [torch.empty((out_h, out_w, 3), dtype=torch.float16).pin_memory()
                  for _ in range(2)]
     pipe_h = FramePipeline(rigspec.sensors, cals, [tuple(t.shape) for t in frame_sets[0]],
-                           (out_w, out_h), params, ref_size=(W, H), device=dev, output="float16")
+                           (out_w, out_h), params, ref_size=(W, H), device=dev, output="float16",
+                           slots=args.e2e_slots)
     for i in range(args.warmup):
         pipe_h.submit(host_sets[i % N_DISTINCT], host_half[i % 2])
     pipe_h.synchronize()
@@ -668,6 +670,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-slots", type=int, default=3,
+                    help="device slots (frames in flight) of the end-to-end pipeline")
     ap.add_argument("--lanes", type=int, default=3,
                     help="streams consecutive frames alternate between (CUDA-graph mode)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
