@@ -469,8 +469,11 @@ def run_ours(args, wl, world, rank, local):
 
     def step(i, flags=0):
         if graphs and not flags:
-            with torch.cuda.stream(lane_streams[i % lanes]):
-                graphs[i % N_DISTINCT].replay()
+            g = i % N_DISTINCT
+            # a graph always runs on the stream of the lane whose workspace and
+            # output it was captured with, so graphs sharing them never overlap
+            with torch.cuda.stream(lane_streams[g % lanes]):
+                graphs[g].replay()
         else:
             step_eager(i, flags)
 
@@ -672,7 +675,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-slots", type=int, default=3,
                     help="device slots (frames in flight) of the end-to-end pipeline")
-    ap.add_argument("--lanes", type=int, default=3,
+    ap.add_argument("--lanes", type=int, default=2,
                     help="streams consecutive frames alternate between (CUDA-graph mode)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="eager launches instead of CUDA-graph replay per step")
