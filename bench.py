@@ -506,6 +506,22 @@ def run_ours(args, wl, world, rank, local):
             n_launches = sum(graphs[i % N_DISTINCT].n_kernels for i in range(args.steps))
     clk = clocks.summary()
     ms_step = ms / args.steps
+
+    # the frames left in each lane's output by the timed loop must equal an
+    # eager, single-stream reconstruction of the same frame bit for bit (catches
+    # any overlap of graphs sharing a workspace or output)
+    if graphs:
+        for lane in range(lanes):
+            last = [i for i in range(args.steps) if (i % N_DISTINCT) % lanes == lane]
+            if not last:
+                continue
+            i = last[-1]
+            rig.set_frames(frame_sets[i % N_DISTINCT])
+            chk = rig.reconstruct((out_w, out_h), params, ref_size=(W, H), stream=stream)
+            torch.cuda.synchronize()
+            if not torch.equal(chk["rgb"].view(torch.int32), lane_out[lane]["rgb"].view(torch.int32)):
+                raise RuntimeError(f"timed frame {i} on lane {lane} differs from an eager "
+                                   "reconstruction of the same frame")
     fps = world * args.steps / (ms / 1e3)
     mpx = fps * out_w * out_h / 1e6
 
@@ -622,6 +638,8 @@ def run_ours(args, wl, world, rank, local):
                               f"{in_bytes / 1e6:.2f} MB), no flush"),
                        "launch": (f"CUDA graph replay per step, frames alternating over "
                                   f"{lanes} streams" if graphs else "eager"),
+                       "verified": ("each lane's last timed frame bit-equal to an eager "
+                                    "single-stream reconstruction" if graphs else None),
                        "parallelism": f"frame-parallel x{world}"},
             "mpix_per_s": mpx,
             "roofline": {"bound": bound, "achieved": achieved / 1e12, "peak": peak / 1e12,
