@@ -57,14 +57,14 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
 #pragma unroll
     for (int s = 0; s < PAT_MAXS; ++s) {
         if (s >= P.n_sensors) break;
-        const int n = P.pat_cnt[s][c][py & 1];
+        const int n = P.pat_cnt[s][c][cls];
         const int o = P.pat_off[s][c][cls];
         const uint32_t vb = vbs[s];
 #pragma unroll 4
         for (int t = o; t < o + n; ++t) {
             const double2 X = lds_d2(txy + 16u * (uint32_t)t);
             const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
-            // masked samples carry (0, 0) and padding taps W = 0, so w and the
+            // masked samples carry (0, 0), so w and the
             // value are already zero exactly when the tap must not count
             const float2 e = lds_f2(vb + Q.y);
             const float w = __uint_as_float(Q.x) * e.y;
@@ -164,11 +164,25 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     constexpr int PN = NC<ORDER>::P;
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
-    const int px = tx0 + (int)(threadIdx.x % TW);
-    // warp w takes row w ^ rot: even and odd rows (different Bayer classes,
-    // different amounts of work) alternate between tiles, so no warp is
-    // systematically the slowest of its CTA
-    const int py = ty0 + ((int)(threadIdx.x / TW) ^ rot);
+    int px, py;
+    if constexpr (PAT != 0) {
+        // tap kernels: each warp holds 32 pixels of ONE Bayer class (16
+        // columns x 2 rows of equal parity), so the tap list is uniform across
+        // the warp -- no padding of the shorter class list, broadcast tap
+        // loads.  Two warps per class; rot swaps the x class between tiles so
+        // light and heavy classes alternate per warp.
+        static_assert(TW == 32 && TH == 8 && NT == 256, "class mapping assumes 32x8 tiles");
+        const int slot = (int)(threadIdx.x >> 5) ^ (rot << 1);
+        const int cl = slot >> 1, lane = (int)(threadIdx.x & 31);
+        px = tx0 + (cl & 1) + 2 * (lane & 15);
+        py = ty0 + (cl >> 1) + 4 * (slot & 1) + 2 * (lane >> 4);
+    } else {
+        px = tx0 + (int)(threadIdx.x % TW);
+        // warp w takes row w ^ rot: even and odd rows (different Bayer classes,
+        // different amounts of work) alternate between tiles, so no warp is
+        // systematically the slowest of its CTA
+        py = ty0 + ((int)(threadIdx.x / TW) ^ rot);
+    }
     if (px > tx1 || py > ty1) return;
     const int pix = py * P.out_w + px;
     const double qx = qcoord(px, P.sx), qy = qcoord(py, P.sy);

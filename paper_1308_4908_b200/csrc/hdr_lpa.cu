@@ -392,17 +392,12 @@ static bool build_taps(DevParams &P, std::vector<Tap> &taps) {
                         cls[cl].push_back(t);
                     }
             }
-            for (int py = 0; py < 2; ++py) {
-                const size_t n = std::max(cls[py * 2].size(), cls[py * 2 + 1].size());
-                P.pat_cnt[s][c][py] = (int)n;
-                for (int px = 0; px < 2; ++px) {
-                    std::vector<Tap> &v = cls[py * 2 + px];
-                    Tap pad;
-                    memset(&pad, 0, sizeof(pad));  // W = 0: no contribution, not counted
-                    while (v.size() < n) v.push_back(pad);
-                    P.pat_off[s][c][py * 2 + px] = (int)taps.size();
-                    taps.insert(taps.end(), v.begin(), v.end());
-                }
+            // a warp of the tap kernel holds pixels of one class only, so each
+            // class keeps its own tap count (no padding to the longer list)
+            for (int cl = 0; cl < 4; ++cl) {
+                P.pat_cnt[s][c][cl] = (int)cls[cl].size();
+                P.pat_off[s][c][cl] = (int)taps.size();
+                taps.insert(taps.end(), cls[cl].begin(), cls[cl].end());
             }
         }
     }

@@ -59,7 +59,7 @@ struct DevSensor {
 
 // Pre-computed window tap (aligned / translation-only rigs on the reference
 // grid): sensor offset (k, m) from the output pixel, exact float64 offset
-// d = X - q and window weight W = exp(-|d|^2 / h).  W == 0 marks padding.
+// d = X - q and window weight W = exp(-|d|^2 / h).
 struct Tap {
     double dx, dy;
     float W;
@@ -136,7 +136,7 @@ struct DevParams {
     const unsigned char *rt_global; // RT: the table in the workspace (copied to shared memory)
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
-    int pat_cnt[MAXS][3][2];        // taps per (sensor, channel, y parity); both x classes padded
+    int pat_cnt[MAXS][3][4];        // taps of (sensor, channel, class)
     uint32_t *work_count;
     uint32_t *tile_counter;          // fast kernel: next tile to hand out (workspace header)
     uint32_t *slow_counter;          // exact path: next work item to evaluate
