@@ -165,17 +165,27 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     int tx0, ty0, tx1, ty1;
     tile_bounds(P, t, tx0, ty0, tx1, ty1);
     int px, py;
-    if constexpr (PAT != 0) {
-        // tap kernels: each warp holds 32 pixels of ONE Bayer class (16
+    if constexpr (PAT != 0 || RT) {
+        // tap and row-tap kernels: each warp holds 32 pixels of ONE Bayer class (16
         // columns x 2 rows of equal parity), so the tap list is uniform across
         // the warp -- no padding of the shorter class list, broadcast tap
         // loads.  Two warps per class; rot swaps the x class between tiles so
         // light and heavy classes alternate per warp.
         static_assert(TW == 32 && TH == 8 && NT == 256, "class mapping assumes 32x8 tiles");
-        const int slot = (int)(threadIdx.x >> 5) ^ (rot << 1);
-        const int cl = slot >> 1, lane = (int)(threadIdx.x & 31);
-        px = tx0 + (cl & 1) + 2 * (lane & 15);
-        py = ty0 + (cl >> 1) + 4 * (slot & 1) + 2 * (lane >> 4);
+        const int lane = (int)(threadIdx.x & 31);
+        if (RT && P.rt_period == 4) {
+            // 2x output grid (16 classes): a warp takes one row class (py & 3)
+            // and the pixel pairs of one anchor parity ((px >> 1) & 1) --
+            // two classes that share their anchor, i.e. nearly the same rows
+            const int slot = (int)(threadIdx.x >> 5) ^ rot;
+            px = tx0 + 4 * ((lane & 15) >> 1) + 2 * (slot & 1) + (lane & 1);
+            py = ty0 + (slot >> 1) + 4 * (lane >> 4);
+        } else {
+            const int slot = (int)(threadIdx.x >> 5) ^ (rot << 1);
+            const int cl = slot >> 1;
+            px = tx0 + (cl & 1) + 2 * (lane & 15);
+            py = ty0 + (cl >> 1) + 4 * (slot & 1) + 2 * (lane >> 4);
+        }
     } else {
         px = tx0 + (int)(threadIdx.x % TW);
         // warp w takes row w ^ rot: even and odd rows (different Bayer classes,
