@@ -243,19 +243,30 @@ struct TileSweep {
                 const float fcy = (float)(S.N[2] * u + S.N[3] * v - (double)ylo);
                 const float r2hi = (float)r2 + 1e-3f;
                 const float a0 = S.Tf[0], a1 = S.Tf[1], a3 = S.Tf[2], a4 = S.Tf[3];
+                // |T_lin e|^2 <= r2hi as a quadratic in e_x along a sensor row:
+                // al ex^2 + 2 be ey ex + ga ey^2 - r2hi <= 0 (fp32, widened by
+                // 0.01 px: a superset of the exact float64 test below)
+                const float al = fmaf(a0, a0, a3 * a3), be = fmaf(a0, a1, a3 * a4),
+                            ga = fmaf(a1, a1, a4 * a4), inva = 1.f / al;
                 for (int ph = 0; ph < 4; ++ph) {
                     if (!((pm >> ph) & 1)) continue;
                     const int py = ph >> 1, px = ph & 1;
                     const int ys = ylo + ((py - ylo) & 1), xs = xlo + ((px - xlo) & 1);
                     float ey = (float)(ys - ylo) - fcy;
                     for (int y = ys; y <= yhi; y += 2, ey += 2.f) {
+                        const float bq = be * ey;
+                        const float disc = fmaf(bq, bq, -al * fmaf(ga * ey, ey, -r2hi));
+                        if (!(disc >= 0.f)) continue;
+                        const float sq = sqrtf(disc);
+                        // the row's chord, relative to xlo: x - xlo = ex + fcx
+                        int x0 = xlo + (int)ceilf(fmaf(-bq - sq, inva, fcx) - 0.01f);
+                        const int x1 = min(xhi, xlo + (int)floorf(fmaf(-bq + sq, inva, fcx) + 0.01f));
+                        x0 = max(x0, xs);
+                        x0 += (x0 - xs) & 1;
                         const int ly = y - oy;
                         const double t1y = ty1[ly], t4y = ty4[ly];
                         const int rb = ph * plane + (ly >> 1) * pw - (ox >> 1);
-                        float ex = (float)(xs - xlo) - fcx;
-                        for (int x = xs; x <= xhi; x += 2, ex += 2.f) {
-                            const float fx = fmaf(a0, ex, a1 * ey), fy = fmaf(a3, ex, a4 * ey);
-                            if (fmaf(fx, fx, fy * fy) > r2hi) continue;
+                        for (int x = x0; x <= x1; x += 2) {
                             const int k = rb + (x >> 1);
                             const float2 e = vi[k];
                             if (!(e.y > 0.f)) continue;
