@@ -60,6 +60,10 @@ extern "C" {
  * (its work items stay unprocessed, their outputs unwritten); used by the
  * bench to time the fast kernel on its own. */
 #define HDR_FLAG_FAST_ONLY 1
+/* NO_MERGE keeps one tap stream per sensor where co-sited sensors (same
+ * transform, frame size and Bayer phase) would be merged into one sample per
+ * position (A/B comparisons of the two tap kernels). */
+#define HDR_FLAG_NO_MERGE 2
 
 /* Outcome plane codes (optional diagnostics): order*16 + radius-step of the
  * accepted fit (radius step 0 = base radius), or HDR_OUTCOME_NAN. */

@@ -29,6 +29,7 @@ HDR_OK, HDR_ERR_ARG, HDR_ERR_CONFIG, HDR_ERR_SHAPE, HDR_ERR_WORKSPACE, HDR_ERR_C
 HDR_WEIGHT_VARIANCE, HDR_WEIGHT_SIGMA = 0, 1
 HDR_OUTCOME_NAN = 0xFF
 HDR_FLAG_FAST_ONLY = 1
+HDR_FLAG_NO_MERGE = 2
 
 EXPORTED = (
     "hdr_lpa_workspace_bytes",

@@ -29,7 +29,16 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
 
 // the pixel's own position in each sensor's staged phase planes (origins are
 // even), computed once per pixel for all channels
-template <int NS>
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+
+// ESZ: bytes per staged phase-plane element (8: (f_hat, 1/den); 16: merged)
+template <int NS, int ESZ = 8>
 __device__ __forceinline__ void tap_bases(const DevParams &P, const unsigned char *sm,
                                           const int (*org)[2], int px, int py, uint32_t (&vbs)[NS]) {
 #pragma unroll
@@ -38,8 +47,39 @@ __device__ __forceinline__ void tap_bases(const DevParams &P, const unsigned cha
         const DevSensor &S = P.s[s];
         const int pw = S.rw >> 1;
         vbs[s] = smem_addr(sm + S.off_vi) +
-                 8u * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
+                 (uint32_t)ESZ * (uint32_t)(((py - org[s][1]) >> 1) * pw + ((px - org[s][0]) >> 1));
     }
+}
+
+// Co-sited taps (PAT 3/4): one merged sample per position, (sum 1/den,
+// sum f_hat/den, sum |f_hat|/den, count) over the sensors, so one float64
+// update per position instead of one per sensor sample.
+template <int ORDER, bool CNT>
+__device__ __forceinline__ void accumulate_merged_taps(const DevParams &P, const unsigned char *taps,
+                                                       uint32_t vb, int c, int px, int py,
+                                                       Acc<NC<ORDER>::P> &acc) {
+    acc.zero();
+    const int cls = ((py & 1) << 1) | (px & 1);
+    const uint32_t txy = smem_addr(taps);
+    const uint32_t tw = txy + (uint32_t)P.n_taps * (uint32_t)sizeof(TapXY);
+    float count = 0.f;
+    float sabs = 0.f;
+    const int n = P.pat_cnt[0][c][cls];
+    const int o = P.pat_off[0][c][cls];
+#pragma unroll 4
+    for (int t = o; t < o + n; ++t) {
+        const double2 X = lds_d2(txy + 16u * (uint32_t)t);
+        const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
+        const float4 e = lds_f4(vb + Q.y);
+        const float W = __uint_as_float(Q.x);
+        sabs = fmaf(W, e.z, sabs);
+        const double dxx = ORDER >= 2 ? __dmul_rn(X.x, X.x) : 0.0;
+        const double dyy = ORDER >= 2 ? __dmul_rn(X.y, X.y) : 0.0;
+        acc.add_wy((double)(W * e.x), (double)(W * e.y), X.x, X.y, dxx, dyy);
+        if constexpr (CNT) count += e.w;
+    }
+    acc.count = CNT ? (int)count : 1 << 20;
+    acc.sabs = sabs;
 }
 
 template <int ORDER, bool CNT>
@@ -209,8 +249,11 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     }
     const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org, qx, qy,
                                                                    px, py, taps};
+    // PAT: 1 taps (counting samples), 2 taps without the count, 3 / 4 the same
+    // over co-sited merged samples
+    constexpr bool MRG = PAT >= 3;
     uint32_t vbs[PAT_MAXS];
-    if constexpr (PAT) tap_bases<PAT_MAXS>(P, sm, org, px, py, vbs);
+    if constexpr (PAT) tap_bases<PAT_MAXS, MRG ? 16 : 8>(P, sm, org, px, py, vbs);
 
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
@@ -238,14 +281,17 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                 st = ici<ORDER, false>(P, c, sweep, R);
             } else {
                 Acc<PN> acc;
-                if constexpr (PAT)
+                if constexpr (MRG)
+                    accumulate_merged_taps<ORDER, PAT == 3>(P, taps, vbs[0], c, px, py, acc);
+                else if constexpr (PAT)
                     accumulate_taps<ORDER, PAT == 1>(P, taps, vbs, c, px, py, acc);
                 else
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 R.work = acc.count;
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
-                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor)) {
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor,
+                                                     MRG ? FAST_EPS_MERGED : FAST_EPS)) {
                     // loose bound failed: the sharp one needs a sweep with g (not
                     // for the tap path, where this is rare); else the exact path
                     float tk = 0.f;
@@ -287,7 +333,8 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #define HDR_PAT_MINBLOCKS 3
 #endif
 // PAT: 0 no tap table, 1 taps (counting samples), 2 taps without the count
-// (no count/work output planes requested)
+// (no count/work output planes requested), 3 / 4 the same over co-sited
+// merged samples (radiance_merge_kernel)
 template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.

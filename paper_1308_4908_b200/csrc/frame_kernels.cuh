@@ -63,6 +63,66 @@ __global__ void __launch_bounds__(128) radiance_phase_kernel(const __grid_consta
     }
 }
 
+// Co-sited pre-pass (PAT 3/4: every sensor has the same transform, frame size
+// and Bayer phase, so the samples of all sensors at a sensor pixel share one
+// position, offset and window weight): the sensors' samples of a pixel merged
+// into one float4 (sum 1/den, sum f_hat/den, sum |f_hat|/den, count) in the
+// phase-plane layout [4][phg][pwg] (sensor 0's geometry; the planes occupy
+// the workspace of sensors 0 and 1).  Sensors are summed in index order.
+__device__ __forceinline__ void load_raw8(const DevSensor &S, int x0, int y, uint16_t (&v)[8]) {
+    if (S.vec_raw && x0 + 8 <= S.pitch) {
+        const uint4 q = __ldg((const uint4 *)(S.raw + (size_t)y * S.pitch + x0));
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[2 * k] = (uint16_t)(w[k] & 0xffffu);
+            v[2 * k + 1] = (uint16_t)(w[k] >> 16);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = x0 + k < S.width ? __ldg(S.raw + (size_t)y * S.pitch + x0 + k) : (uint16_t)0;
+    }
+}
+
+__global__ void __launch_bounds__(128) radiance_merge_kernel(const __grid_constant__ DevParams P) {
+    const DevSensor &S0 = P.s[0];
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= S0.pwg || j >= S0.phg) return;
+    const int x0 = 2 * i0;
+    float4 *planes = (float4 *)S0.phase;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int y = 2 * j + r;
+        float4 o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (y < S0.height) {
+            for (int s = 0; s < P.n_sensors; ++s) {
+                const DevSensor &S = P.s[s];
+                uint16_t v[8];
+                load_raw8(S, x0, y, v);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (x0 + k >= S.width) continue;
+                    const float2 e = radiance_from_raw(S, (int)v[k], x0 + k, y, P.use_sigma);
+                    o[k].x += e.y;
+                    o[k].y = fmaf(e.x, e.y, o[k].y);
+                    o[k].z = fmaf(fabsf(e.x), e.y, o[k].z);
+                    o[k].w += e.y > 0.f ? 1.f : 0.f;
+                }
+            }
+        }
+#pragma unroll
+        for (int px = 0; px < 2; ++px) {
+            float4 *dst = planes + ((size_t)(2 * r + px) * S0.phg + j) * S0.pwg + i0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = o[px + 2 * k];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Saturation mask bit-planes (radiometry.py:298-300, :316-317)
 // ---------------------------------------------------------------------------

@@ -154,26 +154,35 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // 3-D float32 tensor map over one sensor's phase planes [4][phg][2*pwg]
 // (float2 = 2 floats); the box is the staged region (rw floats = rw/2 float2,
 // rh/2 rows, 4 phases).  The planes live in the workspace, 16-B aligned with
-// 16-B row pitch, so TMA is always applicable.
-static bool encode_phase_map(const DevSensor &d, CUtensorMap *map) {
+// 16-B row pitch, so TMA is always applicable.  Co-sited merged planes hold
+// float4 elements: [4][phg][4*pwg] floats, box 2*rw floats.
+static bool encode_phase_map(const DevSensor &d, CUtensorMap *map, bool merged = false) {
     auto enc = tensor_map_encoder();
-    if (!enc || d.rw > 256 || (d.rh >> 1) > 256) return false;
-    const cuuint64_t dims[3] = {(cuuint64_t)d.pwg * 2, (cuuint64_t)d.phg, 4};
-    const cuuint64_t strides[2] = {(cuuint64_t)d.pwg * 8, (cuuint64_t)d.pwg * 8 * d.phg};
-    const cuuint32_t box[3] = {(cuuint32_t)d.rw, (cuuint32_t)(d.rh >> 1), 4};
+    const int fpe = merged ? 4 : 2;  // floats per element
+    if (!enc || d.rw * fpe / 2 > 256 || (d.rh >> 1) > 256) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)d.pwg * fpe, (cuuint64_t)d.phg, 4};
+    const cuuint64_t strides[2] = {(cuuint64_t)d.pwg * 4 * fpe,
+                                   (cuuint64_t)d.pwg * 4 * fpe * d.phg};
+    const cuuint32_t box[3] = {(cuuint32_t)(d.rw * fpe / 2), (cuuint32_t)(d.rh >> 1), 4};
     const cuuint32_t estr[3] = {1, 1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)d.phase, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Pf: the fast kernel's parameters (a one-sensor view over the merged planes
+// in co-sited mode), P: the full rig for the exact path.
 template <int ORDER>
-static int launch_all(const DevParams &P, const TapParam &T, int tiles, int smem_bytes, int maxc,
-                      cudaStream_t st) {
+static int launch_all(const DevParams &Pf, const DevParams &P, const TapParam &T, int tiles,
+                      int smem_bytes, int maxc, cudaStream_t st) {
     int rc;
-    if (P.pat)
-        rc = (P.count || P.work) ? launch_fast<ORDER, false, 4, 1>(P, T, tiles, smem_bytes, st)
-                                 : launch_fast<ORDER, false, 4, 2>(P, T, tiles, smem_bytes, st);
+    const bool cnt = P.count || P.work;
+    if (Pf.merged)
+        rc = cnt ? launch_fast<ORDER, false, 4, 3>(Pf, T, tiles, smem_bytes, st)
+                 : launch_fast<ORDER, false, 4, 4>(Pf, T, tiles, smem_bytes, st);
+    else if (P.pat)
+        rc = cnt ? launch_fast<ORDER, false, 4, 1>(P, T, tiles, smem_bytes, st)
+                 : launch_fast<ORDER, false, 4, 2>(P, T, tiles, smem_bytes, st);
     else if (P.rt && P.n_scales > 1)
         rc = maxc <= 6 ? launch_fast<ORDER, true, 6, 0, true>(P, T, tiles, smem_bytes, st)
                        : launch_fast<ORDER, true, 8, 0, true>(P, T, tiles, smem_bytes, st);
@@ -553,7 +562,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     return HDR_OK;
 }
 
-static int launch_prepass(const DevParams &P, cudaStream_t st) {
+static int launch_prepass(const DevParams &P, cudaStream_t st, bool merged = false) {
     int maxsat = 0;
     for (int s = 0; s < P.n_sensors; ++s)
         if (!P.s[s].planes) maxsat = max(maxsat, P.s[s].sat);
@@ -567,10 +576,36 @@ static int launch_prepass(const DevParams &P, cudaStream_t st) {
         maxpw = max(maxpw, P.s[s].pwg);
         maxph = max(maxph, P.s[s].phg);
     }
-    dim3 grid((maxpw / 4 + 31) / 32, (maxph + 3) / 4, P.n_sensors);
     COUNT_LAUNCH();
+    if (merged) {  // co-sited sensors: one merged plane set (sensor 0's geometry)
+        dim3 grid((P.s[0].pwg / 4 + 31) / 32, (P.s[0].phg + 3) / 4, 1);
+        radiance_merge_kernel<<<grid, dim3(32, 4), 0, st>>>(P);
+        return cudaPeekAtLastError() == cudaSuccess ? HDR_OK
+                                                    : cuda_fail("radiance_merge_kernel launch");
+    }
+    dim3 grid((maxpw / 4 + 31) / 32, (maxph + 3) / 4, P.n_sensors);
     radiance_phase_kernel<<<grid, dim3(32, 4), 0, st>>>(P);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("radiance_phase_kernel launch");
+}
+
+// Co-sited rig: at least two sensors, all with sensor 0's translation-only
+// transform (bitwise), frame size and Bayer phase, fixed scale on the
+// reference grid -- the conditions under which every sensor's sample of a
+// sensor pixel has the same position, offset and weight, and the tap table
+// applies.  Their samples can then be merged per position (PAT 3/4).  The
+// merged float4 planes need sensor 0's and sensor 1's plane workspace.
+static bool cosited(const DevParams &P) {
+    if (P.n_sensors < 2 || P.n_sensors > PAT_MAXS || (P.flags & HDR_FLAG_NO_MERGE)) return false;
+    if (P.n_scales != 1 || P.sx != 1.0 || P.sy != 1.0) return false;
+    const DevSensor &a = P.s[0];
+    for (int s = 1; s < P.n_sensors; ++s) {
+        const DevSensor &b = P.s[s];
+        if (b.width != a.width || b.height != a.height) return false;
+        for (int c = 0; c < 3; ++c)
+            if (b.phmask[c] != a.phmask[c]) return false;
+        if (memcmp(a.T, b.T, sizeof(a.T)) != 0) return false;
+    }
+    return (char *)P.s[1].phase == (char *)a.phase + (size_t)4 * a.pwg * a.phg * sizeof(float2);
 }
 
 // Staged-region geometry, shared-memory layout, tap tables (when allowed) and
@@ -615,9 +650,11 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
             xy[i].dx = taps[i].dx;
             xy[i].dy = taps[i].dy;
             w[i].W = taps[i].W;
-            w[i].off = taps[i].delta * (int)sizeof(float2);
+            w[i].off = taps[i].delta * (P.merged ? (int)sizeof(float4) : (int)sizeof(float2));
         }
         P.tab_bytes = (int)(n * sizeof(Tap));
+    } else if (P.merged) {
+        return HDR_ERR_ARG;  // the merged view exists only for the tap kernel
     } else if (allow_taps) {
         P.rt = build_rowtaps(P, rt_table) ? 1 : 0;
         if (P.rt) P.off_taps = take(P.tab_bytes);
@@ -626,7 +663,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
     smem = 0;
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
-        d.off_vi = take(d.rw * d.rh * 8);  // [4][rh/2][rw/2] float2
+        d.off_vi = take(d.rw * d.rh * (P.merged ? 16 : 8));  // [4][rh/2][rw/2] float2 / float4
         d.off_tx0 = take(d.rw * 8);
         d.off_tx3 = take(d.rw * 8);
         d.off_ty1 = take(d.rh * 8);
@@ -636,7 +673,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
     smem_bytes = P.plane_base + NBUF * P.buf_stride;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
     for (int s = 0; s < n_sensors; ++s)
-        if (!encode_phase_map(P.s[s], &P.tmap[s])) {
+        if (!encode_phase_map(P.s[s], &P.tmap[s], P.merged != 0)) {
             snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled failed (sensor %d)", s);
             return HDR_ERR_CUDA;
         }
@@ -658,7 +695,18 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     static thread_local TapParam T;  // kernel-parameter image of the tap table
     std::vector<unsigned char> rt_table;
     int smem_bytes = 0, maxc = 1;
-    {
+    // co-sited sensors: the fast kernel sees one sensor whose staged planes
+    // are the merged ones (falls back to the per-sensor tap / sweep kernels
+    // when the tap table does not apply)
+    static thread_local DevParams Pf;
+    bool merged = false;
+    if (cosited(P)) {
+        Pf = P;
+        Pf.n_sensors = 1;
+        Pf.merged = 1;
+        merged = setup_staging(Pf, 1, fastR, true, T, rt_table, smem_bytes, maxc) == HDR_OK;
+    }
+    if (!merged) {
         const int rc = setup_staging(P, n_sensors, fastR, true, T, rt_table, smem_bytes, maxc);
         if (rc != HDR_OK) return rc;
     }
@@ -666,16 +714,21 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.tiles_y = (row_end - row_begin + TH - 1) / TH;
     P.tiles_x = (out_w + TW - 1) / TW;
     const int tiles = P.tiles_x * P.tiles_y;
+    if (merged) {
+        Pf.tiles_x = P.tiles_x;
+        Pf.tiles_y = P.tiles_y;
+    }
+    const DevParams &PF = merged ? Pf : P;
     if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (P.rt && upload_table(rt_table, (unsigned char *)P.rt_global, st) != HDR_OK)
         return HDR_ERR_CUDA;
-    if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;  // per-frame radiometry
+    if (launch_prepass(P, st, merged) != HDR_OK) return HDR_ERR_CUDA;  // per-frame radiometry
     int rc;
     switch (P.order) {
-        case 0: rc = launch_all<0>(P, T, tiles, smem_bytes, maxc, st); break;
-        case 1: rc = launch_all<1>(P, T, tiles, smem_bytes, maxc, st); break;
-        default: rc = launch_all<2>(P, T, tiles, smem_bytes, maxc, st); break;
+        case 0: rc = launch_all<0>(PF, P, T, tiles, smem_bytes, maxc, st); break;
+        case 1: rc = launch_all<1>(PF, P, T, tiles, smem_bytes, maxc, st); break;
+        default: rc = launch_all<2>(PF, P, T, tiles, smem_bytes, maxc, st); break;
     }
     return rc;
 }

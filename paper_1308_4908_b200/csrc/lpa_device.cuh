@@ -110,7 +110,9 @@ struct DevParams {
     DevSensor s[MAXS];
     int n_sensors, order, n_scales, use_sigma;
     int out_w, out_h, row_begin, row_end;
-    int tiles_x, tiles_y, pad0, pad1b;
+    int tiles_x, tiles_y;
+    int merged;               // co-sited tap mode: one merged plane set replaces the sensors' (PAT 3/4)
+    int pad1b;
     double sx, sy;            // ref_w / out_w, ref_h / out_h  (lpa.py:222-223)
     double r[3][MAXJ];        // min(3 sqrt(h), max_radius)     (lpa.py:353, _kernels.py:276-277)
     double r2[3][MAXJ];       // r * r
@@ -346,6 +348,55 @@ struct Acc {
         }
         count += inc;
     }
+    // Co-sited samples merged (PAT 3/4): the weight wd = W sum_s 1/den_s and
+    // the weighted value wyd = W sum_s y_s/den_s of one position, so
+    // b += wyd phi (the same sums as add() over the position's samples).
+    __device__ __forceinline__ void add_wy(double wd, double wyd, double dx, double dy, double dxx,
+                                           double dyy) {
+        if constexpr (MOM) {
+            double m[15];
+            m[1] = dx;
+            m[2] = dy;
+            m[3] = dxx;
+            m[4] = __dmul_rn(dx, dy);
+            m[5] = dyy;
+            m[6] = dxx * dx;
+            m[7] = dxx * dy;
+            m[8] = dx * dyy;
+            m[9] = dyy * dy;
+            m[10] = dxx * dxx;
+            m[11] = dxx * m[4];
+            m[12] = dxx * dyy;
+            m[13] = m[4] * dyy;
+            m[14] = dyy * dyy;
+            A[0] += wd;
+#pragma unroll
+            for (int k = 1; k < 15; ++k) A[k] = fma(wd, m[k], A[k]);
+            b[0] += wyd;
+#pragma unroll
+            for (int a = 1; a < 6; ++a) b[a] = fma(wyd, m[midx(basis_i(a), basis_j(a))], b[a]);
+        } else {
+            double phi[3];
+            phi[0] = 1.0;
+            if (P >= 3) {
+                phi[1] = dx;
+                phi[2] = dy;
+            }
+            b[0] += wyd;
+#pragma unroll
+            for (int a = 1; a < P; ++a) b[a] = fma(wyd, phi[a], b[a]);
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                const double wa = (a == 0) ? wd : wd * phi[a];
+#pragma unroll
+                for (int c = a; c < P; ++c) {
+                    A[k] = (c == 0) ? A[k] + wa : fma(wa, phi[c], A[k]);
+                    ++k;
+                }
+            }
+        }
+    }
     // packed upper triangle of A
     __device__ __forceinline__ void fill_A(double *out) const {
         if constexpr (MOM) {
@@ -521,16 +572,20 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
 // pixels next to much brighter samples, where order-2 kernels' negative
 // lobes amplify the rounding -- is re-done by the exact path.
 constexpr double FAST_EPS = 4e-7;
+// co-sited merged planes (PAT 3/4): + the product y_s/den_s, the sums over
+// <= PAT_MAXS sensors and W * sum (<= 5 more fp32 roundings)
+constexpr double FAST_EPS_MERGED = 7e-7;
 constexpr double FAST_TOL = 2e-5;
 // relative error allowance of the fast path's ICI standard deviations (fp32
 // weights through g = A^-1 e1; ~25x FAST_EPS)
 constexpr double ICI_SD_EPS = 1e-5;
 template <int P>
-__device__ __forceinline__ bool fit_precise(const Fit &fit, float sabs, double r, double floor) {
+__device__ __forceinline__ bool fit_precise(const Fit &fit, float sabs, double r, double floor,
+                                            double eps = FAST_EPS) {
     double G = fabs(fit.g[0]);
     if (P >= 3) G += r * (fabs(fit.g[1]) + fabs(fit.g[2]));
     if (P >= 6) G += r * r * (fabs(fit.g[3]) + fabs(fit.g[4]) + fabs(fit.g[5]));
-    return FAST_EPS * G * (double)sabs <= FAST_TOL * fmax(fabs(fit.c0), floor);
+    return eps * G * (double)sabs <= FAST_TOL * fmax(fabs(fit.c0), floor);
 }
 // Sharp form: with T = sum w |g.phi| |y|, first-order perturbation of the
 // weights (by the residuals y - phi.c) and values gives |dc0| <~ 2 FAST_EPS T.

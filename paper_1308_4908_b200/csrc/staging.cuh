@@ -127,10 +127,14 @@ __device__ __forceinline__ void stage_tile(const DevParams &P, unsigned char *pb
         // the buffer's previous contents were read through the generic proxy
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         uint32_t bytes = 0;
-        for (int s = 0; s < P.n_sensors; ++s) bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * 8);
+        // element: float2 (f_hat, 1/den), or float4 for co-sited merged planes
+        const int esz = P.merged ? 16 : 8;
+        for (int s = 0; s < P.n_sensors; ++s) bytes += (uint32_t)(P.s[s].rw * P.s[s].rh * esz);
         mbar_expect_tx(full, bytes);
-        for (int s = 0; s < P.n_sensors; ++s)  // phase-plane coords: ox/2 float2 = ox floats, oy/2
-            tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], org[s][0], org[s][1] >> 1, 0, full);
+        // phase-plane coords: ox/2 elements = ox (float2) or 2 ox (float4) floats, oy/2
+        for (int s = 0; s < P.n_sensors; ++s)
+            tma_load_3d(pb + P.s[s].off_vi, &P.tmap[s], P.merged ? 2 * org[s][0] : org[s][0],
+                        org[s][1] >> 1, 0, full);
     }
 }
 

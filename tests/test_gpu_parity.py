@@ -350,3 +350,70 @@ def test_extreme_scenes(cuda, top, order, J):
     p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
     got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), (W, H), p)
     _check(got, ref)
+
+
+def _cosited_rig(W, H, seed, n_sensors=3, shift=(0.0, 0.0)):
+    """Every sensor with the same (translation-only) transform: the co-sited
+    tap kernel (one merged sample per position) applies."""
+    import dataclasses
+
+    rig = sim.baseline_rig("aligned", W, H, seed=seed, n_sensors=n_sensors)
+    T = np.array([[1.0, 0.0, shift[0]], [0.0, 1.0, shift[1]]])
+    sensors = [dataclasses.replace(s, transform=T) for s in rig.sensors]
+    return dataclasses.replace(rig, sensors=sensors)
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_cosited_merge_matches_per_sensor_taps(cuda, order):
+    """The merged tap kernel against the per-sensor tap kernel
+    (HDR_FLAG_NO_MERGE) and the oracle: identical sample counts, outcomes and
+    NaN maps, radiance within the parity bar."""
+    from paper_1308_4908_b200 import _native as N
+
+    W, H = 131, 77  # odd sizes: padded phase-plane columns and rows
+    rig = _cosited_rig(W, H, seed=21)
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    cfgs, cals = list(rig.sensors), rig.calibrations()
+    p = hl.ReconstructionParams(order=order, scale=0.7)
+    dev = hl.frames_to_samples(frames, cfgs, cals).device()
+    kw = dict(want_outcome=True, want_count=True)
+    a = {k: v.cpu().numpy() for k, v in dev.reconstruct((W, H), p, **kw).items()}
+    b = {k: v.cpu().numpy() for k, v in
+         dev.reconstruct((W, H), p, flags=N.HDR_FLAG_NO_MERGE, **kw).items()}
+    assert np.array_equal(a["count"], b["count"])
+    assert np.array_equal(a["outcome"], b["outcome"])
+    s = compare.summary(a["rgb"], b["rgb"])
+    assert s["nan_map_equal"] and s["max"] <= 2e-5, s
+    got, ref, _ = _run(frames, cfgs, cals, (W, H), p)
+    _check(got, ref)
+
+
+@pytest.mark.parametrize("n_sensors,shift", [(2, (0.0, 0.0)), (4, (0.4, -0.45)),
+                                             (3, (3.25, 1.5))])
+def test_cosited_shifted_and_sensor_counts(cuda, n_sensors, shift):
+    W, H = 96, 64
+    rig = _cosited_rig(W, H, seed=22, n_sensors=n_sensors, shift=shift)
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    p = hl.ReconstructionParams(order=1, scale=0.7)
+    got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), (W, H), p)
+    _check(got, ref)
+
+
+def test_cosited_sigma_weights_planes_and_defects(cuda):
+    import dataclasses
+
+    W, H = 96, 80
+    rig = _cosited_rig(W, H, seed=23)
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    cfgs, cals = list(rig.sensors), rig.calibrations()
+    rng = np.random.default_rng(1)
+    cals = [hl.NoiseCalibration(
+        bias=hl.FloatFrame(c.bias.data + rng.uniform(-1, 1, c.shape)),
+        readout_variance=hl.FloatFrame(c.readout_variance.data * rng.uniform(0.8, 1.2, c.shape)),
+        nonuniformity=hl.FloatFrame(rng.uniform(0.95, 1.05, c.shape))) for c in cals]
+    cfgs = [dataclasses.replace(cfgs[1], defective=np.array([3, 97, 1500, 4000]))
+            if i == 1 else c for i, c in enumerate(cfgs)]
+    for mode in ("variance", "sigma"):
+        p = hl.ReconstructionParams(order=1, scale=0.7, weight_mode=mode)
+        got, ref, _ = _run(frames, cfgs, cals, (W, H), p)
+        _check(got, ref)
