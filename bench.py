@@ -21,6 +21,7 @@ sides, max over ranks.  Inputs: 8 distinct pre-simulated frames per rank cycled
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -144,6 +145,18 @@ class ClockSampler:
 # CPU samples: full frames where one takes ~1 s, else a band of output rows
 REF_BAND_ROWS = {"cfg1": None, "cfg2": None, "cfg3": 24, "cfg4": 24, "cfg5": 16, "calpa": None,
                  "samples": None}
+
+
+def _cosited(sensors, wl):
+    """The library's co-sited tap mode applies (hdr_lpa.cu cosited()): 2-4
+    sensors with one translation-only transform and one Bayer pattern, fixed
+    scale on the reference grid."""
+    Ts = [np.asarray(s.transform, dtype=np.float64) for s in sensors]
+    lin = Ts[0][:, :2]
+    return (2 <= len(sensors) <= 4 and wl["J"] == 1 and tuple(wl["out"]) == tuple(wl["size"])
+            and all(np.array_equal(T, Ts[0]) for T in Ts)
+            and np.array_equal(lin, np.eye(2))
+            and len({str(s.pattern) for s in sensors}) == 1)
 
 
 def _cpu_model():
@@ -525,11 +538,34 @@ def run_ours(args, wl, world, rank, local):
     fps = world * args.steps / (ms / 1e3)
     mpx = fps * out_w * out_h / 1e6
 
-    # fast kernel alone (the dominant kernel), same stream, same inputs
+    # fast path without the exact kernel (memset, LUT, pre-pass, tile kernel)
     for i in range(2):
         step(i, flags=N.HDR_FLAG_FAST_ONLY)
-    ms_fast = timed(lambda i: step(i, flags=N.HDR_FLAG_FAST_ONLY), args.steps) / args.steps
+    ms_fastpath = timed(lambda i: step(i, flags=N.HDR_FLAG_FAST_ONLY), args.steps) / args.steps
     slow_items = rig.slow_items((out_w, out_h))
+
+    # the dominant kernel alone: the library's event pair around each fast
+    # tile-kernel launch (same stream, same inputs); a GPU sleep queued ahead
+    # of each call keeps the device behind the host, so the pair brackets the
+    # kernel and not host-side launch gaps
+    def fast_kernel_ms(k):
+        lib = N.lib()
+        N.check(lib.hdr_lpa_kernel_timer(1), "hdr_lpa_kernel_timer")
+        tot = 0.0
+        try:
+            for i in range(k):
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(1_000_000)
+                step_eager(i, flags=N.HDR_FLAG_FAST_ONLY)
+                v = ctypes.c_float()
+                N.check(lib.hdr_lpa_kernel_timer_read(ctypes.byref(v)), "kernel timer")
+                tot += v.value
+        finally:
+            lib.hdr_lpa_kernel_timer(0)
+        return max_over_ranks(tot / k)
+
+    fast_kernel_ms(2)
+    ms_fast = fast_kernel_ms(args.steps)
 
     # algorithmic work of one launch: inside-window samples of the accepted fits
     # (the kernel's own work plane: inside-window samples over every moment
@@ -554,8 +590,12 @@ def run_ours(args, wl, world, rank, local):
     in_bytes = sum(t.numel() * 2 for t in frame_sets[0])
     out_bytes = out_w * out_h * 12
     # the fast kernel reads the per-frame (f_hat, 1/den) phase planes (8 B per sensor pixel)
-    # written by the radiometric pre-pass, and writes the RGB frame
+    # written by the radiometric pre-pass, and writes the RGB frame; co-sited rigs
+    # (one transform for all sensors, fixed scale, reference grid) read one merged
+    # float4 plane set instead (16 B per sensor-0 pixel)
     planes_bytes = sum(t.numel() * 8 for t in frame_sets[0])
+    if _cosited(rigspec.sensors, wl):
+        planes_bytes = frame_sets[0][0].numel() * 16
     traffic, traffic_src = None, None
     tpath = ROOT / "profiles" / "r01_traffic.json"
     if tpath.exists():
@@ -647,7 +687,12 @@ def run_ours(args, wl, world, rank, local):
                          "traffic_unit": "bytes/launch (DRAM read+write, ncu)",
                          "traffic_source": traffic_src,
                          "peak_source": peak_src, "kernel": "lpa_fast_kernel",
-                         "kernel_ms": ms_fast, "inside_samples_per_launch": n_inside,
+                         "kernel_ms": ms_fast,
+                         "kernel_ms_source": "library event pair around each fast-kernel "
+                                             "launch (hdr_lpa_kernel_timer), mean of steps",
+                         "fast_path_ms": ms_fastpath,
+                         "cosited_merge": _cosited(rigspec.sensors, wl),
+                         "inside_samples_per_launch": n_inside,
                          "flop64_per_launch": flop64, "flop32_per_launch": flop32,
                          "fp32": {"achieved_tflops": flop32 / (ms_fast * 1e-3) / 1e12,
                                   "peak_tflops": fp32_peak / 1e12,

@@ -254,6 +254,14 @@ int hdr_lpa_abi_version(void);
  * a timed region (bench.py's gpu_launches). */
 unsigned long long hdr_lpa_launch_count(void);
 
+/* Dominant-kernel timer (diagnostics, bench.py's roofline): while enabled on
+ * the calling thread, every eager hdr_lpa_reconstruct records a CUDA event
+ * pair around its fast tile kernel on the call's stream (not while the stream
+ * is being captured into a graph).  hdr_lpa_kernel_timer_read waits for the
+ * last pair and writes its elapsed milliseconds. */
+int hdr_lpa_kernel_timer(int enable);
+int hdr_lpa_kernel_timer_read(float *ms);
+
 #ifdef __cplusplus
 }
 #endif

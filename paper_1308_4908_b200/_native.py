@@ -46,6 +46,8 @@ EXPORTED = (
     "hdr_lpa_last_error",
     "hdr_lpa_abi_version",
     "hdr_lpa_launch_count",
+    "hdr_lpa_kernel_timer",
+    "hdr_lpa_kernel_timer_read",
 )
 
 
@@ -185,6 +187,8 @@ def lib():
                     getattr(L, name).restype = ctypes.c_int
             L.hdr_lpa_launch_count.restype = ctypes.c_ulonglong
             L.hdr_lpa_launch_count.argtypes = []
+            L.hdr_lpa_kernel_timer.argtypes = [ctypes.c_int]
+            L.hdr_lpa_kernel_timer_read.argtypes = [ctypes.POINTER(ctypes.c_float)]
             if L.hdr_lpa_abi_version() != 4:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L

@@ -34,6 +34,13 @@ constexpr int PAT_MAXS = 4;
 #define HDR_NBUF 2
 #endif
 constexpr int NBUF = HDR_NBUF;
+// tap kernels (PAT): a tile costs a few microseconds, so warps of the light
+// Bayer classes run further ahead of the tile's last warp with more buffers
+#ifndef HDR_NBUF_TAP
+#define HDR_NBUF_TAP 4
+#endif
+constexpr int NBUF_TAP = HDR_NBUF_TAP;
+__host__ __device__ constexpr int nbuf_for(int pat) { return pat ? NBUF_TAP : NBUF; }
 static const size_t LUT_BYTES = 65536 * sizeof(double2);
 static const size_t RT_TABLE_BYTES = 64 * 1024;  // row-tap table (workspace, then shared memory)
 

@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
                     typename std::conditional<(PAT != 0), TapParam, NoTaps>::type T) {
+    constexpr int NBUF = nbuf_for(PAT);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];

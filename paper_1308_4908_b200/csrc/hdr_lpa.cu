@@ -116,6 +116,16 @@ static int set_smem_attr(const void *fn, int bytes) {
     return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
+// hdr_lpa_kernel_timer: an event pair around each eager fast-kernel launch
+static thread_local bool g_timer_on = false;
+static thread_local cudaEvent_t g_timer_ev[2] = {nullptr, nullptr};
+static thread_local bool g_timer_recorded = false;
+static bool timer_active(cudaStream_t st) {
+    if (!g_timer_on) return false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+}
+
 template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false>
 static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
@@ -128,12 +138,19 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
         per_sm < 1)
         return cuda_fail("occupancy query");
     const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
+    const bool timed = timer_active(st);
+    if (timed) cudaEventRecord(g_timer_ev[0], st);
     COUNT_LAUNCH();
     if constexpr (PAT)
         lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, T);
     else
         lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
-    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_fast_kernel launch");
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_fast_kernel launch");
+    if (timed) {
+        cudaEventRecord(g_timer_ev[1], st);
+        g_timer_recorded = true;
+    }
+    return HDR_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -428,6 +445,25 @@ int hdr_lpa_abi_version(void) { return HDR_LPA_ABI_VERSION; }
 
 unsigned long long hdr_lpa_launch_count(void) { return g_launches.load(); }
 
+int hdr_lpa_kernel_timer(int enable) {
+    if (enable && !g_timer_ev[0]) {
+        if (cudaEventCreate(&g_timer_ev[0]) != cudaSuccess ||
+            cudaEventCreate(&g_timer_ev[1]) != cudaSuccess)
+            return cuda_fail("cudaEventCreate");
+    }
+    g_timer_on = enable != 0;
+    g_timer_recorded = false;
+    return HDR_OK;
+}
+
+int hdr_lpa_kernel_timer_read(float *ms) {
+    if (!ms || !g_timer_recorded) return HDR_ERR_ARG;
+    if (cudaEventSynchronize(g_timer_ev[1]) != cudaSuccess) return cuda_fail("cudaEventSynchronize");
+    if (cudaEventElapsedTime(ms, g_timer_ev[0], g_timer_ev[1]) != cudaSuccess)
+        return cuda_fail("cudaEventElapsedTime");
+    return HDR_OK;
+}
+
 const char *hdr_lpa_last_error(void) { return g_last_error; }
 
 const char *hdr_lpa_status_string(int status) {
@@ -670,7 +706,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
         d.off_ty4 = take(d.rh * 8);
     }
     P.buf_stride = smem;
-    smem_bytes = P.plane_base + NBUF * P.buf_stride;
+    smem_bytes = P.plane_base + nbuf_for(P.pat) * P.buf_stride;
     if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
     for (int s = 0; s < n_sensors; ++s)
         if (!encode_phase_map(P.s[s], &P.tmap[s], P.merged != 0)) {
