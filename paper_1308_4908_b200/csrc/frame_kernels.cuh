@@ -85,28 +85,80 @@ __device__ __forceinline__ void load_raw8(const DevSensor &S, int x0, int y, uin
     }
 }
 
+// Scalar-calibration radiometry of a raw value for the merged planes, branch
+// free: (f_hat, 1/den) as radiance_from_raw (same fp32 operations; the
+// reciprocal is MUFU + one Newton step, within 1 ulp of the rounded one),
+// 1/den = 0 at or above saturation.
+__device__ __forceinline__ void merge_scalar(const DevSensor &S, uint32_t raw, int use_sigma,
+                                             float4 &o) {
+    const float f = ((float)raw - S.bias_f) * S.inv_denom_f;
+    const float shot = S.c_shot_f * fmaxf(f, 0.f);
+    const float var = fmaxf((shot + S.readvar_f) * S.inv_denom2_f, S.qv_f);
+    float iv;
+    if (use_sigma) {
+        iv = rsqrtf(var);
+    } else {
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(var));
+        iv = fmaf(r, fmaf(-var, r, 1.f), r);
+    }
+    iv = (int)raw < S.sat ? iv : 0.f;
+    o.x += iv;
+    o.y = fmaf(f, iv, o.y);
+    o.z = fmaf(fabsf(f), iv, o.z);
+    o.w += iv > 0.f ? 1.f : 0.f;
+}
+
+// One thread per (phase row j, raw row 2j + r, group of 4 phase columns): the
+// raw 16-B vectors of every sensor are loaded before any conversion (the
+// loads overlap), then merged and stored as 2 x 4 float4.  Sensors with
+// scalar calibration, no defect map and 16-B rows take a branch-free path.
 __global__ void __launch_bounds__(128) radiance_merge_kernel(const __grid_constant__ DevParams P) {
     const DevSensor &S0 = P.s[0];
-    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int jr = blockIdx.y * blockDim.y + threadIdx.y;
+    const int j = jr >> 1, r = jr & 1;
     const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i0 >= S0.pwg || j >= S0.phg) return;
     const int x0 = 2 * i0;
-    float4 *planes = (float4 *)S0.phase;
+    const int y = 2 * j + r;
+    float4 o[8];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const int y = 2 * j + r;
-        float4 o[8];
+    for (int k = 0; k < 8; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (y < S0.height) {
+        bool simple = x0 + 8 <= S0.width;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (y < S0.height) {
-            for (int s = 0; s < P.n_sensors; ++s) {
+        for (int s = 0; s < PAT_MAXS; ++s)
+            if (s < P.n_sensors)
+                simple &= !P.s[s].planes && !P.s[s].defective && P.s[s].vec_raw;
+        if (simple) {
+            uint4 q[PAT_MAXS];
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s)
+                if (s < P.n_sensors)
+                    q[s] = __ldg((const uint4 *)(P.s[s].raw + (size_t)y * P.s[s].pitch + x0));
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s) {
+                if (s >= P.n_sensors) break;
+                const uint32_t w[4] = {q[s].x, q[s].y, q[s].z, q[s].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    merge_scalar(P.s[s], w[k] & 0xffffu, P.use_sigma, o[2 * k]);
+                    merge_scalar(P.s[s], w[k] >> 16, P.use_sigma, o[2 * k + 1]);
+                }
+            }
+        } else {
+            uint16_t v[PAT_MAXS][8];
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s)
+                if (s < P.n_sensors) load_raw8(P.s[s], x0, y, v[s]);
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s) {
+                if (s >= P.n_sensors) break;
                 const DevSensor &S = P.s[s];
-                uint16_t v[8];
-                load_raw8(S, x0, y, v);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     if (x0 + k >= S.width) continue;
-                    const float2 e = radiance_from_raw(S, (int)v[k], x0 + k, y, P.use_sigma);
+                    const float2 e = radiance_from_raw(S, (int)v[s][k], x0 + k, y, P.use_sigma);
                     o[k].x += e.y;
                     o[k].y = fmaf(e.x, e.y, o[k].y);
                     o[k].z = fmaf(fabsf(e.x), e.y, o[k].z);
@@ -114,12 +166,13 @@ __global__ void __launch_bounds__(128) radiance_merge_kernel(const __grid_consta
                 }
             }
         }
+    }
+    float4 *planes = (float4 *)S0.phase;
 #pragma unroll
-        for (int px = 0; px < 2; ++px) {
-            float4 *dst = planes + ((size_t)(2 * r + px) * S0.phg + j) * S0.pwg + i0;
+    for (int px = 0; px < 2; ++px) {
+        float4 *dst = planes + ((size_t)(2 * r + px) * S0.phg + j) * S0.pwg + i0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) dst[k] = o[px + 2 * k];
-        }
+        for (int k = 0; k < 4; ++k) dst[k] = o[px + 2 * k];
     }
 }
 

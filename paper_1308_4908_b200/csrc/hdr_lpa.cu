@@ -614,7 +614,7 @@ static int launch_prepass(const DevParams &P, cudaStream_t st, bool merged = fal
     }
     COUNT_LAUNCH();
     if (merged) {  // co-sited sensors: one merged plane set (sensor 0's geometry)
-        dim3 grid((P.s[0].pwg / 4 + 31) / 32, (P.s[0].phg + 3) / 4, 1);
+        dim3 grid((P.s[0].pwg / 4 + 31) / 32, (2 * P.s[0].phg + 3) / 4, 1);
         radiance_merge_kernel<<<grid, dim3(32, 4), 0, st>>>(P);
         return cudaPeekAtLastError() == cudaSuccess ? HDR_OK
                                                     : cuda_fail("radiance_merge_kernel launch");

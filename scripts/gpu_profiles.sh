@@ -8,6 +8,6 @@ python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain_bench.
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench_cfg2.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 python scripts/profile_run.py cfg2 2 > gpurun_out/plain_p2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:lpa_fast_kernel -s 1 -c 1 -o gpurun_out/prof_cfg2_r01 python scripts/profile_run.py cfg2 2 > gpurun_out/ncu_p2.log 2>&1
-ncu --set full --clock-control none -k regex:radiance_phase_kernel -s 1 -c 1 -o gpurun_out/prof_cfg2_prepass_r01 python scripts/profile_run.py cfg2 2 > gpurun_out/ncu_pp.log 2>&1
+ncu --set full --clock-control none -k regex:"radiance_(phase|merge)_kernel" -s 1 -c 1 -o gpurun_out/prof_cfg2_prepass_r01 python scripts/profile_run.py cfg2 2 > gpurun_out/ncu_pp.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:lpa_slow_kernel -s 1 -c 1 -o gpurun_out/prof_cfg2_slow_r01 python scripts/profile_run.py cfg2 2 > gpurun_out/ncu_ps.log 2>&1
 ls -la gpurun_out
