@@ -311,23 +311,22 @@ struct RowMoments {
         const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double w = (double)w32, y = ok ? v : 0.0;
         acc.sabs = fmaf(w32, fabsf((float)y), acc.sabs);
-        // w dx^n from independent products (dx^2 is the cached column square):
-        // dependency depth 2 instead of a 2*ORDER-long multiply chain
-        double p[5];
-        p[0] = w;
-        if (ORDER >= 1) {
-            p[1] = w * dx;
-            p[2] = w * dxx;
-        }
+        // S_n += w dx^n and T_n += (w y) dx^n as fused multiply-adds (dx^2 is
+        // the cached column square, dx^3 and dx^4 independent products)
+        double px[5];
+        px[1] = dx;
+        px[2] = dxx;
         if (ORDER >= 2) {
-            p[3] = w * (dx * dxx);
-            p[4] = w * (dxx * dxx);
+            px[3] = dx * dxx;
+            px[4] = dxx * dxx;
         }
+        S[0] += w;
 #pragma unroll
-        for (int n = 0; n <= 2 * ORDER; ++n) {
-            S[n] += p[n];
-            if (n <= ORDER) T[n] = fma(p[n], y, T[n]);
-        }
+        for (int n = 1; n <= 2 * ORDER; ++n) S[n] = fma(w, px[n], S[n]);
+        const double wy = w * y;
+        T[0] += wy;
+#pragma unroll
+        for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
         cnt += ok ? 1 : 0;
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) {
@@ -370,7 +369,7 @@ struct RowMoments {
         const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double y = ok ? v : 0.0;
         acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
-        acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+        acc.add_fast((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
     }
 };
 
@@ -458,7 +457,7 @@ __device__ __forceinline__ void accumulate(const DevParams &P, int c, int k, dou
             const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;  // w = W / den
             const double y = ok ? v : 0.0;
             acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
-            acc.add((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+            acc.add_fast((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
         });
     }
 }
