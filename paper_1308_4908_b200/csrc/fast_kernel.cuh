@@ -289,7 +289,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                     accumulate<ORDER, false>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
                 R.work = acc.count;
                 Fit fit;
-                st = solve_fast<PN>(acc, P.cond, fit);
+                st = solve_fast<PN>(acc, P.cond, fit, P.grad != nullptr);
                 if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, P.r[c][0], P.prec_floor,
                                                      MRG ? FAST_EPS_MERGED : FAST_EPS)) {
                     // loose bound failed: the sharp one needs a sweep with g (not

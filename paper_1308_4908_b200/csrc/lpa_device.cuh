@@ -538,8 +538,11 @@ __device__ __forceinline__ void chol_finish(const double *A, const double *b, co
 
 // Fast decision: OK / FAIL / AMBIG, with the reference's tests
 // (_kernels.py:184-199): count < p, A00 <= 0 (p == 1), cond > threshold, pivot <= 0.
+// grad = false: the gradient coefficients c1, c2 are not needed (no gradient
+// plane requested) and are left unset by the 3x3 path.
 template <int P>
-__device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &fit) {
+__device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &fit,
+                                          bool grad = true) {
     if (acc.count < P) return FIT_FAIL;
     if constexpr (P == 1) {
         if (!(acc.A[0] > 0)) return FIT_FAIL;
@@ -573,16 +576,21 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         const double rd = 1.0 / det;
         const double b0 = acc.b[0], b1 = acc.b[1], b2 = acc.b[2];
         fit.c0 = fma(C00, b0, fma(C01, b1, C02 * b2)) * rd;
-        fit.c1 = fma(C01, b0, fma(C11, b1, C12 * b2)) * rd;
-        fit.c2 = fma(C02, b0, fma(C12, b1, C22 * b2)) * rd;
+        if (grad) {
+            fit.c1 = fma(C01, b0, fma(C11, b1, C12 * b2)) * rd;
+            fit.c2 = fma(C02, b0, fma(C12, b1, C22 * b2)) * rd;
+        } else {
+            fit.c1 = fit.c2 = 0.0;
+        }
         fit.g[0] = C00 * rd;
         fit.g[1] = C01 * rd;
         fit.g[2] = C02 * rd;
         const double cu = (a + d + f) * ((C00 + C11 + C22) * rd);
-        const double cl = fmax(a, fmax(d, f)) * (fmax(C00, fmax(C11, C22)) * rd);
         if (!(cu >= 9.0 * (1.0 - 1e-6))) return FIT_AMBIG;  // tr A tr A^-1 >= p^2 always
         const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
         if (cu <= cond * (1.0 - margin)) return FIT_OK;
+        // the lower bound only for windows the upper one does not clear
+        const double cl = fmax(a, fmax(d, f)) * (fmax(C00, fmax(C11, C22)) * rd);
         if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
         return FIT_AMBIG;
     } else {
@@ -619,7 +627,7 @@ __device__ __forceinline__ bool fit_precise(const Fit &fit, float sabs, double r
     double G = fabs(fit.g[0]);
     if (P >= 3) G += r * (fabs(fit.g[1]) + fabs(fit.g[2]));
     if (P >= 6) G += r * r * (fabs(fit.g[3]) + fabs(fit.g[4]) + fabs(fit.g[5]));
-    return eps * G * (double)sabs <= FAST_TOL * fmax(fabs(fit.c0), floor);
+    return G * (double)sabs <= (FAST_TOL / eps) * fmax(fabs(fit.c0), floor);
 }
 // Sharp form: with T = sum w |g.phi| |y|, first-order perturbation of the
 // weights (by the residuals y - phi.c) and values gives |dc0| <~ 2 FAST_EPS T.
