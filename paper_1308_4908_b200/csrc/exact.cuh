@@ -60,8 +60,13 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     Fit fit;
     double L = 0.0, U = 0.0, eL = 0.0, eU = 0.0;  // running bounds and their error bounds
     bool precise = true;
+    // fast row sweeps: the variance sweep of scale k and the moment sweep of
+    // scale k+1 share one traversal (FusedVarMom); the moments of k+1 are
+    // wasted only when the search ends at k
+    constexpr bool FUSED = !EXACT && ORDER >= 1 && HasRows<Sweep>::value;
+    if constexpr (FUSED) accumulate<ORDER, EXACT>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
     for (int k = 0; k < P.n_scales; ++k) {
-        accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
+        if constexpr (!FUSED) accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
         R.work += acc.count;
         const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
         if (st == FIT_AMBIG) return FIT_AMBIG;
@@ -69,8 +74,25 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
             if (k == 0) return FIT_FAIL;
             break;  // an invalid scale ends the search at k-1
         }
+        const int count_k = acc.count;
         float tk = 0.f;
-        const double sd = sqrt(fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk));
+        double var_k;
+        if constexpr (FUSED) {
+            RowVariance<ORDER> V{fit.g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0, 0.f};
+            if (k + 1 < P.n_scales) {
+                acc.zero();
+                RowMoments<ORDER> M{acc, P.hl[c][k + 1]};
+                FusedVarMom<ORDER> F{V, M};
+                sweep.rows(c, k + 1, P.r[c][k + 1], P.r2[c][k + 1], F, k);
+            } else {
+                sweep.rows(c, k, P.r[c][k], P.r2[c][k], V);
+            }
+            tk = V.T;
+            var_k = V.v;
+        } else {
+            var_k = fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk);
+        }
+        const double sd = sqrt(var_k);
         const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
         // fast path: error bound of lo/hi (fp32 rounding of c0: fit_precise_sharp;
         // of sd: ICI_SD_EPS relative) -- an intersection test closer than the
@@ -92,7 +114,7 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         R.gx = fit.c1;
         R.gy = fit.c2;
         R.sidx = k;
-        R.count = acc.count;
+        R.count = count_k;
         if constexpr (!EXACT) precise = fit_precise_sharp(fit.c0, tk, P.prec_floor);
     }
     if (!precise) return FIT_PREC;  // selected estimate too close to fp32 rounding limits

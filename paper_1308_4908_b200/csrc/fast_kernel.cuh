@@ -163,13 +163,13 @@ struct RowAniso {
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) { m.end_row(dy, dyy); }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
-                                           double dxx, double dyy, float) {
+                                           double dxx, double dyy, float, bool = true) {
         const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
         // RowMoments' weight is ex2(-hl * d2f) * iv: feed it q2 with hl = 1
         m.sample(ok, v, iv, dx, dy, dxx, dyy, q2);
     }
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
-                                            double dxx, double dyy, float) {
+                                            double dxx, double dyy, float, bool = true) {
         const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
         m.general(ok, v, iv, dx, dy, dxx, dyy, q2);
     }

@@ -98,11 +98,11 @@ struct PerSample {
     __device__ __forceinline__ void begin_row(double, double) {}
     __device__ __forceinline__ void end_row(double, double) {}
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
-                                           double dxx, double dyy, float d2f) {
+                                           double dxx, double dyy, float d2f, bool = true) {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
-                                            double dxx, double dyy, float d2f) {
+                                            double dxx, double dyy, float d2f, bool = true) {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
 };
@@ -127,8 +127,10 @@ struct TileSweep {
 
     // RT: the pre-computed rows of a translation-only sensor at scale k (all
     // taps inside r_k by construction; masked samples contribute weight 0).
+    // kin >= 0: each sample also carries `inner` = inside the window of scale
+    // kin <= k (a fused traversal: variance at kin, moments at k)
     template <class Pol>
-    __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol) const {
+    __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol, int kin = -1) const {
         const DevSensor &S = P.s[s];
         const int pm = P.rt_period - 1;
         const int cls = (py & pm) * P.rt_period + (px & pm);
@@ -146,12 +148,16 @@ struct TileSweep {
             const TapRow &R = rows[ri];
             const int lo = R.lo[k], hi = R.hi[k];
             if (lo >= hi) continue;
+            // the inner scale's run [ilo, ihi) lies inside [lo, hi) (nested disks)
+            const int ilo = kin >= 0 ? R.first + R.lo[kin] : 0;
+            const int ihi = kin >= 0 ? R.first + R.hi[kin] : 1 << 30;
             const double dy = R.dy, dyy = dy * dy;
             pol.begin_row(dy, dyy);
             for (int t = R.first + lo; t < R.first + hi; ++t) {
                 const RowTap T = taps[t];
                 const float2 e = *(const float2 *)(vb + T.off);
-                pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f);
+                pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f,
+                           t >= ilo && t < ihi);
             }
             pol.end_row(dy, dyy);
         }
@@ -161,7 +167,9 @@ struct TileSweep {
     // shares dy, so a policy can accumulate per-row sums (begin_row / sample /
     // end_row); rotated sensors go through pol.general() per sample.
     template <class Pol>
-    __device__ __forceinline__ void rows(int c, int k, double r, double r2, Pol &pol) const {
+    __device__ __forceinline__ void rows(int c, int k, double r, double r2, Pol &pol,
+                                         int kin = -1) const {
+        const double r2in = kin >= 0 ? P.r2[c][kin] : r2;  // exact float64 membership
         for (int s = 0; s < P.n_sensors; ++s) {
             const DevSensor &S = P.s[s];
             const int pm = S.phmask[c];
@@ -169,7 +177,7 @@ struct TileSweep {
             if constexpr (RT) {
                 // RT mode: every separable sensor is translation-only and tapped
                 if (S.separable) {
-                    tap_rows(s, c, k, pol);
+                    tap_rows(s, c, k, pol, kin);
                     continue;
                 }
             }
@@ -220,13 +228,13 @@ struct TileSweep {
                                         const float2 e = vi[rb + i];
                                         if (e.y > 0.f)
                                             pol.sample(true, (double)e.x, e.y, cdx[i], dy, cdxx[i],
-                                                       dyy, (float)d2);
+                                                       dyy, (float)d2, d2 <= r2in);
                                     }
                                 } else {
                                     const float2 e = vi[rb + i];
                                     const bool ok = (d2 <= r2) && (e.y > 0.f);
                                     pol.sample(ok, (double)e.x, e.y, cdx[i], dy, cdxx[i], dyy,
-                                               (float)d2);
+                                               (float)d2, d2 <= r2in);
                                 }
                             }
                             pol.end_row(dy, dyy);
@@ -277,7 +285,8 @@ struct TileSweep {
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);
                             if (d2 > r2) continue;
-                            pol.general(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2);
+                            pol.general(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2,
+                                        d2 <= r2in);
                         }
                     }
                 }
@@ -307,7 +316,7 @@ struct RowMoments {
         cnt = 0;
     }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double,
-                                           double dxx, double, float d2f) {
+                                           double dxx, double, float d2f, bool = true) {
         const float w32 = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double w = (double)w32, y = ok ? v : 0.0;
         acc.sabs = fmaf(w32, fabsf((float)y), acc.sabs);
@@ -365,7 +374,7 @@ struct RowMoments {
         acc.count += cnt;
     }
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
-                                            double dxx, double dyy, float d2f) {
+                                            double dxx, double dyy, float d2f, bool = true) {
         const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
         const double y = ok ? v : 0.0;
         acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
@@ -397,7 +406,7 @@ struct RowVariance {
     }
     __device__ __forceinline__ void end_row(double, double) {}
     __device__ __forceinline__ void sample(bool ok, double y, float iv, double dx, double, double,
-                                           double, float d2f) {
+                                           double, float d2f, bool = true) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
         const double t = (double)(sig ? W * W : W * W * iv);
         double pg = c0;
@@ -409,7 +418,7 @@ struct RowVariance {
         }
     }
     __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
-                                            double dxx, double dyy, float d2f) {
+                                            double dxx, double dyy, float d2f, bool = true) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
         const double t = (double)(sig ? W * W : W * W * iv);
         double pg = g[0];
@@ -419,6 +428,33 @@ struct RowVariance {
             v = fma(t, pg * pg, v);
             T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
         }
+    }
+};
+
+// Fused traversal of ICI: the variance sweep of scale kin (samples flagged
+// `inner`) and the moment sweep of the next scale k (all samples of its
+// larger window) in one pass over the window of scale k.
+template <int ORDER>
+struct FusedVarMom {
+    RowVariance<ORDER> &V;
+    RowMoments<ORDER> &M;
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        V.begin_row(dy, dyy);
+        M.begin_row(dy, dyy);
+    }
+    __device__ __forceinline__ void end_row(double dy, double dyy) {
+        M.end_row(dy, dyy);
+        V.end_row(dy, dyy);
+    }
+    __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
+                                           double dxx, double dyy, float d2f, bool inner) {
+        M.sample(ok, v, iv, dx, dy, dxx, dyy, d2f);
+        if (inner) V.sample(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
+                                            double dxx, double dyy, float d2f, bool inner) {
+        M.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
+        if (inner) V.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
 };
 
