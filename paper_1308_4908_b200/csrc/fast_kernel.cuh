@@ -247,7 +247,12 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         covered &= xlo >= org[s][0] && ylo >= org[s][1] && xhi < org[s][0] + S.rw &&
                    yhi < org[s][1] + S.rh;
     }
-    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org, qx, qy,
+    __shared__ double2 s_q[NT];  // this thread's query point (TileSweep::qx / qy)
+    // volatile store: stays ordered before TileSweep's volatile loads
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_addr(&s_q[threadIdx.x])), "d"(qx),
+                 "d"(qy));
+    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org,
+                                                                   smem_addr(&s_q[threadIdx.x]),
                                                                    px, py, taps};
     // PAT: 1 taps (counting samples), 2 taps without the count, 3 / 4 the same
     // over co-sited merged samples

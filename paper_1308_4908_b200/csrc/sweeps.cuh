@@ -112,7 +112,20 @@ struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
     const int (*org)[2];
-    double qx, qy;
+    // the query point lives in a per-thread shared-memory slot and is re-read
+    // at each use: under the order-2 kernels' register pressure the compiler
+    // otherwise re-derives it (three float64 operations) inside the sample loops
+    uint32_t qslot;
+    __device__ __forceinline__ double qx() const {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(qslot));
+        return v;
+    }
+    __device__ __forceinline__ double qy() const {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(qslot + 8u));
+        return v;
+    }
     int px, py;                 // the output pixel (RT: parity class, phase-plane base)
     const unsigned char *rt;    // RT: row-tap table in shared memory (rows, then taps)
     template <int PN>
@@ -187,7 +200,7 @@ struct TileSweep {
             const double *ty4 = (const double *)(sm + S.off_ty4);
             const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
             int xlo, xhi, ylo, yhi;
-            window_bbox(S, qx, qy, r, xlo, xhi, ylo, yhi);
+            window_bbox(S, qx(), qy(), r, xlo, xhi, ylo, yhi);
             if (!RT && S.separable) {
                 for (int ph = 0; ph < 4; ++ph) {
                     if (!((pm >> ph) & 1)) continue;
@@ -201,7 +214,7 @@ struct TileSweep {
 #pragma unroll
                         for (int i = 0; i < MAXC; ++i) {
                             if (c0 + i < nc) {
-                                cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx);  // X(x) - qx
+                                cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx());  // X(x) - qx
                                 cdxx[i] = __dmul_rn(cdx[i], cdx[i]);
                             } else {
                                 // finite sentinel: never inside, and 0 * phi stays 0
@@ -212,7 +225,7 @@ struct TileSweep {
                         const int colbase = ph * plane + ((xs - ox) >> 1);
                         for (int y = ys; y <= yhi; y += 2) {
                             const int ly = y - oy;
-                            const double dy = __dsub_rn(ty4[ly], qy);  // Y(y) - qy
+                            const double dy = __dsub_rn(ty4[ly], qy());  // Y(y) - qy
                             const double dyy = __dmul_rn(dy, dy);
                             if (dyy > r2) continue;
                             const int rb = colbase + (ly >> 1) * pw;
@@ -246,7 +259,7 @@ struct TileSweep {
                 const double *ty1 = (const double *)(sm + S.off_ty1);
                 const double T2 = S.T[2], T5 = S.T[5];
                 // sensor-space position of q relative to the bbox corner (fp32 pre-test)
-                const double u = qx - T2, v = qy - T5;
+                const double u = qx() - T2, v = qy() - T5;
                 const float fcx = (float)(S.N[0] * u + S.N[1] * v - (double)xlo);
                 const float fcy = (float)(S.N[2] * u + S.N[3] * v - (double)ylo);
                 const float r2hi = (float)r2 + 1e-3f;
@@ -281,7 +294,7 @@ struct TileSweep {
                             const int lx = x - ox;
                             const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
                             const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
-                            const double dx = __dsub_rn(X, qx), dy = __dsub_rn(Y, qy);
+                            const double dx = __dsub_rn(X, qx()), dy = __dsub_rn(Y, qy());
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);
                             if (d2 > r2) continue;
