@@ -577,6 +577,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.count = out->count;
     P.work = out->work;
     P.flags = params->flags;
+    P.diag = (P.grad || P.sidx || P.outcome || P.value || P.count || P.work) ? 1 : 0;
     P.work_count = (uint32_t *)workspace;
     P.tile_counter = (uint32_t *)workspace + 1;
     P.slow_counter = (uint32_t *)workspace + 2;

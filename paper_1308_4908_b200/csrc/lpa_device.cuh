@@ -130,7 +130,8 @@ struct DevParams {
     float *value;
     uint16_t *count;
     uint32_t *work;
-    int flags, pad1;
+    int flags;
+    int diag;                 // any diagnostic plane (grad, sidx, outcome, value, count, work) requested
     // pre-computed-weight mode: taps per (sensor, channel, pixel parity class)
     int pat, n_taps, off_taps, tab_bytes;  // tab_bytes: kernel-parameter table size (PAT or RT)
     int rt;                         // row-tap mode (ICI / order 2 with translation-only sensors)

@@ -24,17 +24,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 }
 // Bounded wait: a barrier that never completes (a lost TMA transaction)
 // traps -- the launch fails with an error -- instead of hanging the GPU.
+// try_wait carries a suspend-time hint, so a waiting warp is parked until
+// the phase completes instead of spinning through the issue slots of the
+// warps that compute (busy polling was ~10 % of the tap kernel's
+// instructions); the bound is 2 s of %globaltimer.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
-    for (uint32_t spin = 0;; ++spin) {
+    uint64_t t0 = 0;
+    for (;;) {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             " selp.u32 %0, 1, 0, p;\n}"
             : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
+            : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
             : "memory");
         if (done) return;
-        if (spin > (1u << 24)) __trap();
+        const uint64_t now = global_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 2000000000ull) __trap();
     }
 }
 __device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParams &P, int tx0,

@@ -570,6 +570,7 @@ __device__ __forceinline__ void write_result(const DevParams &P, int pix, int c,
     const float o = (v != v) ? __int_as_float(0x7fc00000) : __double2float_rn(fmax(v, 0.0));
     if (P.rgb) P.rgb[(size_t)pix * 3 + c] = o;
     if (P.rgb_half) P.rgb_half[(size_t)pix * 3 + c] = __half_as_ushort(__float2half_rn(o * P.half_scale));
+    if (!P.diag) return;
     const size_t plane = (size_t)P.out_w * P.out_h;
     if (P.grad) {
         P.grad[(size_t)(2 * c) * plane + pix] = (float)R.gx;
