@@ -198,12 +198,13 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
 
 template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
-                                             const unsigned char *taps, int t,
+                                             const unsigned char *taps, int tcol, int trow,
                                              const int (*org)[2], bool tile_covered,
                                              int rot) {
     constexpr int PN = NC<ORDER>::P;
-    int tx0, ty0, tx1, ty1;
-    tile_bounds(P, t, tx0, ty0, tx1, ty1);
+    // tile origin from its (column, row) index, published by the staging warp
+    const int tx0 = tcol * TW, ty0 = P.row_begin + trow * TH;
+    const int tx1 = min(tx0 + TW, P.out_w) - 1, ty1 = min(ty0 + TH, P.row_end) - 1;
     int px, py;
     if constexpr (PAT != 0 || RT) {
         // tap and row-tap kernels: each warp holds 32 pixels of ONE Bayer class (16
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
     __shared__ int s_cov[NBUF];
     __shared__ unsigned s_done[NBUF];
     __shared__ int s_tile[NBUF];
+    __shared__ int s_tcol[NBUF], s_trow[NBUF];  // the tile's column / row index
     __shared__ __align__(8) uint64_t bar_full[NBUF];
     const int ntiles = P.tiles_x * P.tiles_y;
     const unsigned char *taps = smem + P.off_taps;
@@ -387,7 +389,11 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         if ((threadIdx.x & 31) == 0) tn = (int)atomicAdd(P.tile_counter, 1u);
         tn = __shfl_sync(0xffffffffu, tn, 0);
         if (tn < ntiles) {
-            if ((threadIdx.x & 31) == 0) s_tile[b] = tn;
+            if ((threadIdx.x & 31) == 0) {
+                s_tile[b] = tn;
+                s_trow[b] = tn / P.tiles_x;
+                s_tcol[b] = tn - s_trow[b] * P.tiles_x;
+            }
             stage_tile<!PAT>(P, planes + b * P.buf_stride, tn, s_org[b], &s_cov[b], &bar_full[b]);
         } else if ((threadIdx.x & 31) == 0) {
             s_tile[b] = -1;
@@ -409,8 +415,8 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
         const int t = s_tile[b];
         if (t < 0) break;
-        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, t, s_org[b], s_cov[b] != 0,
-                                                       HDR_ROW_ROT ? (i & 1) : 0);
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, s_tcol[b], s_trow[b], s_org[b],
+                                                       s_cov[b] != 0, HDR_ROW_ROT ? (i & 1) : 0);
         __syncwarp();
         unsigned last = 0;
         if ((threadIdx.x & 31) == 0) {
