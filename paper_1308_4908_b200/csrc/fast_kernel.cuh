@@ -168,6 +168,11 @@ struct RowAniso {
         // RowMoments' weight is ex2(-hl * d2f) * iv: feed it q2 with hl = 1
         m.sample(ok, v, iv, dx, dy, dxx, dyy, q2);
     }
+    __device__ __forceinline__ void sample4(bool ok, float4 e, double dx, double dy, double dxx,
+                                            double dyy, float) {
+        const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
+        m.sample4(ok, e, dx, dxx, ex2_approx(-q2));
+    }
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float, bool = true) {
         const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
@@ -196,7 +201,7 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
     }
 }
 
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER>
+template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER, bool MRGS>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int tcol, int trow,
                                              const int (*org)[2], bool tile_covered,
@@ -252,7 +257,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     // volatile store: stays ordered before TileSweep's volatile loads
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_addr(&s_q[threadIdx.x])), "d"(qx),
                  "d"(qy));
-    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT> sweep{P, sm, org,
+    const TileSweep<MAXC, HDR_BRANCHY_O2 && (ORDER >= 2), RT, MRGS> sweep{P, sm, org,
                                                                    smem_addr(&s_q[threadIdx.x]),
                                                                    px, py, taps};
     // PAT: 1 taps (counting samples), 2 taps without the count, 3 / 4 the same
@@ -275,7 +280,9 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                 R.work = acc.count;
                 Fit fit;
                 st = solve_fast<PN>(acc, P.cond, fit);
-                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, r, P.prec_floor)) st = FIT_AMBIG;
+                if (st == FIT_OK && !fit_precise<PN>(fit, acc.sabs, r, P.prec_floor,
+                                                     MRGS ? FAST_EPS_MERGED : FAST_EPS))
+                    st = FIT_AMBIG;
                 if (st == FIT_OK) {
                     R.count = acc.count;
                     R.val = fit.c0;
@@ -341,7 +348,9 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 // PAT: 0 no tap table, 1 taps (counting samples), 2 taps without the count
 // (no count/work output planes requested), 3 / 4 the same over co-sited
 // merged samples (radiance_merge_kernel)
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false>
+// MRGS: CALPA's steered pass over co-sited merged planes (ORDER >= 1)
+template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false,
+          bool MRGS = false>
 // Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
 // by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
@@ -415,7 +424,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HD
         mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
         const int t = s_tile[b];
         if (t < 0) break;
-        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER>(P, pb, taps, s_tcol[b], s_trow[b], s_org[b],
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>(P, pb, taps, s_tcol[b], s_trow[b], s_org[b],
                                                        s_cov[b] != 0, HDR_ROW_ROT ? (i & 1) : 0);
         __syncwarp();
         unsigned last = 0;

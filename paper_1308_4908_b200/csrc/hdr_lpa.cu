@@ -126,10 +126,11 @@ static bool timer_active(cudaStream_t st) {
     return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
 }
 
-template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false>
+template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false,
+          bool MRGS = false>
 static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
-    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER>;
+    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148, per_sm = 1;
     cudaGetDevice(&dev);
@@ -142,9 +143,10 @@ static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
     if (timed) cudaEventRecord(g_timer_ev[0], st);
     COUNT_LAUNCH();
     if constexpr (PAT)
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, T);
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS><<<grid, NT, smem_bytes, st>>>(P, T);
     else
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER><<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
+        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>
+            <<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_fast_kernel launch");
     if (timed) {
         cudaEventRecord(g_timer_ev[1], st);
@@ -690,8 +692,8 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
             w[i].off = taps[i].delta * (P.merged ? (int)sizeof(float4) : (int)sizeof(float2));
         }
         P.tab_bytes = (int)(n * sizeof(Tap));
-    } else if (P.merged) {
-        return HDR_ERR_ARG;  // the merged view exists only for the tap kernel
+    } else if (P.merged && allow_taps) {
+        return HDR_ERR_ARG;  // merged planes: the tap kernel or the steered sweep only
     } else if (allow_taps) {
         P.rt = build_rowtaps(P, rt_table) ? 1 : 0;
         if (P.rt) P.off_taps = take(P.tab_bytes);
@@ -791,11 +793,21 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     std::vector<unsigned char> rt_table;
     int smem_bytes = 0, maxc = 1;
     P.fast_R = P.max_radius;
+    // co-sited sensors (orders 1-2): the steered sweep reads the merged planes
+    static thread_local DevParams Pf;
+    bool merged = false;
+    if (P.order >= 1 && cosited(P)) {
+        Pf = P;
+        Pf.n_sensors = 1;
+        Pf.merged = 1;
+        merged = setup_staging(Pf, 1, P.max_radius, false, T, rt_table, smem_bytes, maxc) == HDR_OK;
+    }
     const bool staged =
+        merged ||
         setup_staging(P, n_sensors, P.max_radius, false, T, rt_table, smem_bytes, maxc) == HDR_OK;
     if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
-    if (launch_prepass(P, st) != HDR_OK) return HDR_ERR_CUDA;
+    if (launch_prepass(P, st, merged) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -803,11 +815,19 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
         P.tiles_y = (P.row_end - P.row_begin + TH - 1) / TH;
         P.tiles_x = (out_w + TW - 1) / TW;
         const int tiles = P.tiles_x * P.tiles_y;
+        Pf.tiles_x = P.tiles_x;
+        Pf.tiles_y = P.tiles_y;
         int rc2;
         switch (P.order) {
             case 0: rc2 = launch_fast<0, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
-            case 1: rc2 = launch_fast<1, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
-            default: rc2 = launch_fast<2, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
+            case 1:
+                rc2 = merged ? launch_fast<1, false, 8, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
+                             : launch_fast<1, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st);
+                break;
+            default:
+                rc2 = merged ? launch_fast<2, false, 8, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
+                             : launch_fast<2, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st);
+                break;
         }
         if (rc2 != HDR_OK) return rc2;
         if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;

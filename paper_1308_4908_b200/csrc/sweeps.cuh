@@ -107,7 +107,10 @@ struct PerSample {
     }
 };
 
-template <int MAXC, bool BRANCHY, bool RT = false>
+// MRG4: the staged planes are the co-sited merged float4 planes
+// (sum 1/den, sum f_hat/den, sum |f_hat|/den, count; one "sensor"), and the
+// policy takes them through sample4() (CALPA's steered pass on co-sited rigs).
+template <int MAXC, bool BRANCHY, bool RT = false, bool MRG4 = false>
 struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
@@ -236,7 +239,11 @@ struct TileSweep {
 #pragma unroll
                             for (int i = 0; i < MAXC; ++i) {
                                 const double d2 = __dadd_rn(cdxx[i], dyy);
-                                if constexpr (BRANCHY) {
+                                if constexpr (MRG4) {
+                                    const float4 e = ((const float4 *)vi)[rb + i];
+                                    const bool ok = (d2 <= r2) && (e.x > 0.f);
+                                    pol.sample4(ok, e, cdx[i], dy, cdxx[i], dyy, (float)d2);
+                                } else if constexpr (BRANCHY) {
                                     if (d2 <= r2) {
                                         const float2 e = vi[rb + i];
                                         if (e.y > 0.f)
@@ -350,6 +357,27 @@ struct RowMoments {
 #pragma unroll
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
         cnt += ok ? 1 : 0;
+    }
+    // co-sited merged sample: w = W sum 1/den, wy = W sum f_hat/den (fp32),
+    // the bound's sum w |y| from W sum |f_hat|/den, count = the sensors' samples
+    __device__ __forceinline__ void sample4(bool ok, float4 e, double dx, double dxx, float W) {
+        W = ok ? W : 0.f;
+        const double w = (double)(W * e.x), wy = (double)(W * e.y);
+        acc.sabs = fmaf(W, e.z, acc.sabs);
+        double px[5];
+        px[1] = dx;
+        px[2] = dxx;
+        if (ORDER >= 2) {
+            px[3] = dx * dxx;
+            px[4] = dxx * dxx;
+        }
+        S[0] += w;
+#pragma unroll
+        for (int n = 1; n <= 2 * ORDER; ++n) S[n] = fma(w, px[n], S[n]);
+        T[0] += wy;
+#pragma unroll
+        for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
+        cnt += ok ? (int)e.w : 0;
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) {
         double dp[5];
@@ -475,8 +503,8 @@ template <class Sweep>
 struct HasRows {
     static constexpr bool value = false;
 };
-template <int MAXC, bool BRANCHY, bool RT>
-struct HasRows<TileSweep<MAXC, BRANCHY, RT>> {
+template <int MAXC, bool BRANCHY, bool RT, bool MRG4>
+struct HasRows<TileSweep<MAXC, BRANCHY, RT, MRG4>> {
     static constexpr bool value = true;
 };
 

@@ -266,7 +266,7 @@ class DeviceRig:
 
     def reconstruct_steered(self, out_size, params: ReconstructionParams, field, ref_size=None,
                             rows=None, out=None, want_outcome=False, raw_value=False,
-                            want_work=False, stream=None):
+                            want_work=False, stream=None, flags=0):
         """CALPA second pass with a steering field (theta, sigma, gamma float64
         device tensors over the output grid): hdr_lpa_reconstruct_steered."""
         out_w, out_h = int(out_size[0]), int(out_size[1])
@@ -288,7 +288,7 @@ class DeviceRig:
         ws = self.workspace(out_w, out_h)
         r0, r1 = (0, out_h) if rows is None else (int(rows[0]), int(rows[1]))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        hp = hdr_params(params)
+        hp = hdr_params(params, flags)
         with torch.cuda.device(self.device):
             for b0, b1 in band_split(r0, r1, out_w):
                 rc = N.lib().hdr_lpa_reconstruct_steered(

@@ -145,3 +145,36 @@ def test_random_affine_rig_parity(cuda, k):
     assert s["frac_over"] == 0 and s["max"] <= 1e-4, s
     assert int((got["outcome"] != ref["outcome"]).sum()) == 0
     assert int((got["scale_idx"] != ref["scale_idx"]).sum()) == 0
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_cosited_steered_pass_merge_ab(cuda, order):
+    """CALPA's steered sweep over co-sited merged planes against the per-sensor
+    sweep (HDR_FLAG_NO_MERGE) and the oracle, on one random steering field."""
+    import torch
+    from paper_1308_4908_b200 import _native as N
+
+    rng = np.random.default_rng(77 + order)
+    W, H = 83, 61
+    rig = sim.baseline_rig("aligned", W, H, seed=11)
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    cals = rig.calibrations()
+    base = hl.ReconstructionParams(order=order, scale=0.7)
+    th = rng.uniform(-np.pi, np.pi, (H, W))
+    sg = np.exp(rng.uniform(0.0, np.log(6.0), (H, W)))
+    gm = rng.uniform(0.3, 1.5, (H, W))
+    dev = hl.frames_to_samples(frames, list(rig.sensors), cals).device()
+    field = tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (th, sg, gm))
+    a = dev.reconstruct_steered((W, H), base, field, want_outcome=True)
+    b = dev.reconstruct_steered((W, H), base, field, want_outcome=True, flags=N.HDR_FLAG_NO_MERGE)
+    assert torch.equal(a["outcome"], b["outcome"])
+    s = compare.summary(a["rgb"].cpu().numpy(), b["rgb"].cpu().numpy())
+    assert s["nan_map_equal"] and s["max"] <= 2e-5, s
+    rgb = a["rgb"].cpu().numpy()
+    for c in range(3):
+        steer = oracle.kernel_inputs(th, sg, gm, oracle.channel_scale(base, c))
+        val, _, _, oc = oracle.reconstruct_channel_steered(frames, list(rig.sensors), cals,
+                                                           (W, H), base, c, steer)
+        s = compare.summary(rgb[:, :, c], np.maximum(val, 0.0).astype(np.float32))
+        assert s["nan_map_equal"] and s["frac_over"] == 0 and s["max"] <= 1e-4, s
+        assert int((a["outcome"][c].cpu().numpy() != oc).sum()) == 0
