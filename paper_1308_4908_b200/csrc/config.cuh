@@ -34,10 +34,10 @@ constexpr int PAT_MAXS = 4;
 #define HDR_NBUF 2
 #endif
 constexpr int NBUF = HDR_NBUF;
-// tap kernels (PAT): a tile costs a few microseconds, so warps of the light
-// Bayer classes run further ahead of the tile's last warp with more buffers
+// tap kernels (PAT): measured 2 / 3 / 4 / 6 buffers on cfg2 -- more buffers
+// only cost occupancy (4 CTAs/SM of the co-sited kernel need 2)
 #ifndef HDR_NBUF_TAP
-#define HDR_NBUF_TAP 4
+#define HDR_NBUF_TAP 2
 #endif
 constexpr int NBUF_TAP = HDR_NBUF_TAP;
 __host__ __device__ constexpr int nbuf_for(int pat) { return pat ? NBUF_TAP : NBUF; }

@@ -345,15 +345,22 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 #ifndef HDR_PAT_MINBLOCKS
 #define HDR_PAT_MINBLOCKS 3
 #endif
+// co-sited tap kernels (PAT 3/4): 64 registers, 4 CTAs = 32 warps/SM (cfg2
+// 0.198 -> 0.186 ms; the per-sensor tap kernel measured best at 3)
+#ifndef HDR_MRG_MINBLOCKS
+#define HDR_MRG_MINBLOCKS 4
+#endif
 // PAT: 0 no tap table, 1 taps (counting samples), 2 taps without the count
 // (no count/work output planes requested), 3 / 4 the same over co-sited
 // merged samples (radiance_merge_kernel)
 // MRGS: CALPA's steered pass over co-sited merged planes (ORDER >= 1)
 template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false,
           bool MRGS = false>
-// Tap-table order<=1 kernels are held to 80 registers: 3 CTAs per SM beat 2
-// by ~8% on cfg2; 4 (64 registers, no spills) measured ~2% slower than 3.
-__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS : (PAT ? HDR_PAT_MINBLOCKS : 2)))
+// Per-sensor tap kernels are held to 80 registers: 3 CTAs per SM beat 2 by
+// ~8% on cfg2 and 4 (64 registers) measured ~2% slower than 3.
+__global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
+                                               : (PAT >= 3 ? HDR_MRG_MINBLOCKS
+                                                           : (PAT ? HDR_PAT_MINBLOCKS : 2))))
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
                     typename std::conditional<(PAT != 0), TapParam, NoTaps>::type T) {
