@@ -66,7 +66,11 @@ __device__ __forceinline__ void accumulate_merged_taps(const DevParams &P, const
     float sabs = 0.f;
     const int n = P.pat_cnt[0][c][cls];
     const int o = P.pat_off[0][c][cls];
-#pragma unroll 4
+#ifndef HDR_MRG_UNROLL
+#define HDR_MRG_UNROLL 2
+#endif
+    constexpr int kUnroll = HDR_MRG_UNROLL;
+#pragma unroll kUnroll
     for (int t = o; t < o + n; ++t) {
         const double2 X = lds_d2(txy + 16u * (uint32_t)t);
         const uint2 Q = lds_u2(tw + 8u * (uint32_t)t);
