@@ -390,11 +390,13 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
         const int n16 = (P.tab_bytes + 15) / 16;
         for (int i = threadIdx.x; i < n16; i += NT) dst[i] = __ldg(src + i);
     }
+    __shared__ int s_next[NBUF];  // tile index the next refill of buffer b stages
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&bar_full[b], 1);
             s_done[b] = 0;
+            s_next[b] = (int)atomicAdd(P.tile_counter, 1u);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -404,10 +406,12 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
     // together.  The staging warp takes the next index, publishes it in
     // s_tile[b] and releases it with the buffer's mbarrier (a plain arrive, no
     // copies, when the counter is exhausted: s_tile = -1 ends the loop).
+    // The index a refill stages was taken from the counter one refill of this
+    // buffer earlier (s_next), so the global atomic's latency is not on the
+    // path from "buffer free" to "copy issued"; the refill takes the index for
+    // the buffer's next refill after issuing its copies.
     auto refill = [&](int b) {  // one whole warp
-        int tn = 0;
-        if ((threadIdx.x & 31) == 0) tn = (int)atomicAdd(P.tile_counter, 1u);
-        tn = __shfl_sync(0xffffffffu, tn, 0);
+        const int tn = s_next[b];
         if (tn < ntiles) {
             if ((threadIdx.x & 31) == 0) {
                 s_tile[b] = tn;
@@ -415,6 +419,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
                 s_tcol[b] = tn - s_trow[b] * P.tiles_x;
             }
             stage_tile<!PAT>(P, planes + b * P.buf_stride, tn, s_org[b], &s_cov[b], &bar_full[b]);
+            if ((threadIdx.x & 31) == 0) s_next[b] = (int)atomicAdd(P.tile_counter, 1u);
         } else if ((threadIdx.x & 31) == 0) {
             s_tile[b] = -1;
             mbar_expect_tx(&bar_full[b], 0);
