@@ -28,6 +28,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 // the phase completes instead of spinning through the issue slots of the
 // warps that compute (busy polling was ~10 % of the tap kernel's
 // instructions); the bound is 2 s of %globaltimer.
+#ifndef HDR_MBAR_SLEEP
+#define HDR_MBAR_SLEEP 0  // ns of __nanosleep between failed polls
+#endif
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -44,6 +47,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
             : "memory");
         if (done) return;
+#if HDR_MBAR_SLEEP > 0
+        __nanosleep(HDR_MBAR_SLEEP);
+#endif
         const uint64_t now = global_ns();
         if (t0 == 0) t0 = now;
         else if (now - t0 > 2000000000ull) __trap();
