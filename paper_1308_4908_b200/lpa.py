@@ -133,6 +133,8 @@ def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=
 
     ``samples`` is the RawFrameSet of :func:`frames_to_samples` (fused raw
     path) or scattered :class:`~.samples.RadianceSamples` (CSR index path)."""
+    from .engine import to_host
+
     if _is_scattered(samples):
         import torch
 
@@ -143,15 +145,15 @@ def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=
             val, gx, gy = reconstruct_channel_device(samples, out_size, params, ch, ref_size)
             planes.append(torch.clamp_min(val, 0.0).to(torch.float32))  # keeps NaN (lpa.py:428)
             if return_gradients:
-                grads[ch] = (gx.cpu().numpy(), gy.cpu().numpy())
-        img = HDRImage(torch.stack(planes, 2).cpu().numpy())
+                grads[ch] = (to_host(gx), to_host(gy))
+        img = HDRImage(to_host(torch.stack(planes, 2)))
         return (img, grads) if return_gradients else img
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=return_gradients)
-    img = HDRImage(out["rgb"].cpu().numpy())
+    img = HDRImage(to_host(out["rgb"]))
     if not return_gradients:
         return img
-    g = out["grad"].double().cpu().numpy()
+    g = to_host(out["grad"].double())
     grads = {ch: (g[int(ch), 0], g[int(ch), 1]) for ch in ColorChannel}
     return img, grads
 
@@ -160,6 +162,8 @@ def reconstruct_channel(samples, out_size, params: ReconstructionParams, channel
                         ref_size=None, steering=None):
     """(value, grad_x, grad_y) planes of one channel (reference lpa.py:379-408).
     ``value`` is unclamped like the reference's; NaN where no fit exists."""
+    from .engine import to_host
+
     if _is_scattered(samples):
         from .samples import reconstruct_channel_samples
 
@@ -170,6 +174,6 @@ def reconstruct_channel(samples, out_size, params: ReconstructionParams, channel
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=True, raw_value=True)
     c = int(channel)
-    val = out["value"][c].double().cpu().numpy()
-    g = out["grad"].double().cpu().numpy()
-    return val, g[c, 0], g[c, 1]
+    val = to_host(out["value"][c].double())
+    g = to_host(out["grad"][c].double())
+    return val, g[0], g[1]

@@ -24,6 +24,7 @@ from . import _native as N
 from .bayer import ColorChannel
 from .images import HDRImage
 from .lpa import SUPPORT_SIGMAS, ReconstructionParams, _device_rig
+from .engine import to_host
 from .validation import check_positive
 
 
@@ -132,7 +133,7 @@ def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
         fld = field_for(ColorChannel.G)
         out = rig.reconstruct_steered(out_size, base, (fld.theta, fld.sigma, fld.gamma),
                                       ref_size=ref_size)
-        img = HDRImage(out["rgb"].cpu().numpy())
+        img = HDRImage(to_host(out["rgb"]))
     else:
         out_w, out_h = out_size
         planes = np.empty((out_h, out_w, 3), np.float32)
@@ -141,7 +142,7 @@ def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
             f = field_for(ch)
             o = rig.reconstruct_steered(out_size, base, (f.theta, f.sigma, f.gamma),
                                         ref_size=ref_size)
-            planes[:, :, int(ch)] = o["rgb"][:, :, int(ch)].cpu().numpy()
+            planes[:, :, int(ch)] = to_host(o["rgb"][:, :, int(ch)])
         img = HDRImage(planes)
     if return_field:
         return img, fld

@@ -34,3 +34,11 @@ for it in range(3):
     fld, c = t(lambda: compute_steering_field((gx, gy), ap, sc))
     out, d = t(lambda: rig.reconstruct_steered((W, H), ap.base, (fld.theta, fld.sigma, fld.gamma)))
     print(f"pass1 {a:.2f} ms, scale {b:.2f} ms, field {c:.2f} ms, steered {d:.2f} ms", flush=True)
+
+# the public API end to end (device frames in, host image out)
+for it in range(3):
+    img, e = t(lambda: hl.calpa_reconstruct(rig, (W, H), ap))
+    o, f = t(lambda: rig.reconstruct_steered((W, H), ap.base, (fld.theta, fld.sigma, fld.gamma)))
+    _, g = t(lambda: o["rgb"].cpu().numpy())
+    print(f"calpa_reconstruct {e:.2f} ms; of which D2H of the RGB image (pageable) ~{g:.2f} ms",
+          flush=True)
