@@ -169,6 +169,11 @@ struct TileSweep {
             const int ihi = kin >= 0 ? R.first + R.hi[kin] : 1 << 30;
             const double dy = R.dy, dyy = dy * dy;
             pol.begin_row(dy, dyy);
+#ifndef HDR_RT_UNROLL
+#define HDR_RT_UNROLL 1
+#endif
+            constexpr int kRtUnroll = HDR_RT_UNROLL;
+#pragma unroll kRtUnroll
             for (int t = R.first + lo; t < R.first + hi; ++t) {
                 const RowTap T = taps[t];
                 const float2 e = *(const float2 *)(vb + T.off);
