@@ -362,9 +362,14 @@ template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = 
           bool MRGS = false>
 // Per-sensor tap kernels are held to 80 registers: 3 CTAs per SM beat 2 by
 // ~8% on cfg2 and 4 (64 registers) measured ~2% slower than 3.
+#ifndef HDR_STEER_MINBLOCKS
+#define HDR_STEER_MINBLOCKS 2
+#endif
 __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
                                                : (PAT >= 3 ? HDR_MRG_MINBLOCKS
-                                                           : (PAT ? HDR_PAT_MINBLOCKS : 2))))
+                                                           : (PAT ? HDR_PAT_MINBLOCKS
+                                                                  : (STEER ? HDR_STEER_MINBLOCKS
+                                                                           : 2)))))
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
                     typename std::conditional<(PAT != 0), TapParam, NoTaps>::type T) {
