@@ -417,3 +417,16 @@ def test_cosited_sigma_weights_planes_and_defects(cuda):
         p = hl.ReconstructionParams(order=1, scale=0.7, weight_mode=mode)
         got, ref, _ = _run(frames, cfgs, cals, (W, H), p)
         _check(got, ref)
+
+
+@pytest.mark.parametrize("order,J,up", [(1, 3, False), (2, 4, False), (1, 1, True), (2, 3, True)])
+def test_cosited_rig_outside_the_merged_mode(cuda, order, J, up):
+    """Co-sited sensors where the merged tap kernel does not apply (ICI
+    scales, the 2x output grid): the row-tap / sweep kernels take over."""
+    W, H = 88, 60
+    rig = _cosited_rig(W, H, seed=24, shift=(0.25, -0.5))
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    p = hl.ReconstructionParams(order=order, scale=0.7, ici_scales=J)
+    out = (2 * W, 2 * H) if up else (W, H)
+    got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), out, p, ref_size=(W, H))
+    _check(got, ref)
