@@ -44,6 +44,8 @@ from .steering import (  # noqa: E402
     gradient_field,
 )
 
+from .pipeline import FramePipeline  # noqa: E402  (streaming: pinned H2D, graphs, D2H)
+
 __all__ = [
     "BayerPattern", "CFAImage", "ColorChannel", "ConfigurationError", "FloatFrame", "HDRImage",
     "NoiseCalibration", "RawFrameSet", "ReconstructionParams", "SUPPORT_SIGMAS", "SensorConfig",
@@ -52,5 +54,5 @@ __all__ = [
     "grid_coordinates", "reconstruct_channel", "reconstruct_frame", "saturation_mask",
     "AdaptiveParams", "SteeringField", "calpa_reconstruct", "compute_steering_field",
     "gradient_field", "LocalPolynomialRegressor", "RadianceSample", "RadianceSamples",
-    "SampleIndex",
+    "SampleIndex", "FramePipeline",
 ]
