@@ -739,7 +739,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-slots", type=int, default=3,
                     help="device slots (frames in flight) of the end-to-end pipeline")
-    ap.add_argument("--lanes", type=int, default=2,
+    ap.add_argument("--lanes", type=int, default=4,
                     help="streams consecutive frames alternate between (CUDA-graph mode)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="eager launches instead of CUDA-graph replay per step")
