@@ -13,7 +13,11 @@ for r in csv.DictReader(lines):
     if r.get("Metric Name") != "gpu__time_duration.sum":
         continue
     name = r["Kernel Name"]
-    if "hdrlpa::" not in name or "fp64_probe" in name:
+    # ncu prints the namespace or not depending on the capture mode
+    ours = "hdrlpa::" in name or any(
+        k in name for k in ("lpa_", "radiance_", "table_copy", "steering_field", "sample_planes",
+                            "saturation_mask"))
+    if not ours or "fp64_probe" in name:
         continue
     us = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "")
