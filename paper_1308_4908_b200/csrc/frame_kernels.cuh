@@ -109,11 +109,86 @@ __device__ __forceinline__ void merge_scalar(const DevSensor &S, uint32_t raw, i
     o.w += iv > 0.f ? 1.f : 0.f;
 }
 
-// One thread per (phase row j, raw row 2j + r, group of 4 phase columns): the
-// raw 16-B vectors of every sensor are loaded before any conversion (the
-// loads overlap), then merged and stored as 2 x 4 float4.  Sensors with
-// scalar calibration, no defect map and 16-B rows take a branch-free path.
+// One thread per (phase row j, raw row 2j + r) and 4 phase columns i spaced
+// by a warp (i = base + lane + 32k): every store of a warp is 32 consecutive
+// float4 (512 B) and every raw load 32 consecutive 4-B pixel pairs.  The raw
+// pairs of all sensors and columns are loaded before any conversion (the loads
+// overlap).  Sensors with scalar calibration, no defect map and 16-B rows take
+// a branch-free path.  (HDR_MERGE_COALESCED 0: the previous mapping, 4
+// adjacent phase columns per thread -- each warp store then touched 32
+// half-sectors 64 B apart.)
+#ifndef HDR_MERGE_COALESCED
+#define HDR_MERGE_COALESCED 1
+#endif
 __global__ void __launch_bounds__(128) radiance_merge_kernel(const __grid_constant__ DevParams P) {
+#if HDR_MERGE_COALESCED
+    const DevSensor &S0 = P.s[0];
+    const int jr = blockIdx.y * blockDim.y + threadIdx.y;
+    const int j = jr >> 1, r = jr & 1;
+    if (j >= S0.phg) return;
+    const int y = 2 * j + r;
+    const int ib = blockIdx.x * 128 + (int)threadIdx.x;
+    float4 *planes = (float4 *)S0.phase;
+    float4 *dst0 = planes + ((size_t)(2 * r) * S0.phg + j) * S0.pwg;
+    float4 *dst1 = planes + ((size_t)(2 * r + 1) * S0.phg + j) * S0.pwg;
+    bool simple = y < S0.height;
+#pragma unroll
+    for (int s = 0; s < PAT_MAXS; ++s)
+        if (s < P.n_sensors) simple &= !P.s[s].planes && !P.s[s].defective && P.s[s].vec_raw;
+    // the scalar path per aligned group of 8 raw columns inside the width (the
+    // previous mapping's rule, so every pixel takes the same path as before)
+    if (simple && ((2 * (ib + 96)) & ~7) + 8 <= S0.width) {
+        uint32_t w[4][PAT_MAXS];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s)
+                if (s < P.n_sensors)
+                    w[k][s] = __ldg((const uint32_t *)(P.s[s].raw + (size_t)y * P.s[s].pitch +
+                                                       2 * (ib + 32 * k)));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float4 o0 = make_float4(0.f, 0.f, 0.f, 0.f), o1 = o0;
+#pragma unroll
+            for (int s = 0; s < PAT_MAXS; ++s) {
+                if (s >= P.n_sensors) break;
+                merge_scalar(P.s[s], w[k][s] & 0xffffu, P.use_sigma, o0);
+                merge_scalar(P.s[s], w[k][s] >> 16, P.use_sigma, o1);
+            }
+            dst0[ib + 32 * k] = o0;
+            dst1[ib + 32 * k] = o1;
+        }
+        return;
+    }
+    // the frame's right edge, odd widths, per-pixel calibration planes, defects
+    for (int k = 0; k < 4; ++k) {
+        const int i = ib + 32 * k;
+        if (i >= S0.pwg) break;
+        float4 o[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+        if (y < S0.height) {
+            for (int s = 0; s < PAT_MAXS; ++s) {
+                if (s >= P.n_sensors) break;
+                const DevSensor &S = P.s[s];
+                for (int d = 0; d < 2; ++d) {
+                    const int x = 2 * i + d;
+                    if (x >= S.width) continue;
+                    const int v = (int)__ldg(S.raw + (size_t)y * S.pitch + x);
+                    if (simple && (x & ~7) + 8 <= S0.width) {
+                        merge_scalar(S, (uint32_t)v, P.use_sigma, o[d]);
+                    } else {
+                        const float2 e = radiance_from_raw(S, v, x, y, P.use_sigma);
+                        o[d].x += e.y;
+                        o[d].y = fmaf(e.x, e.y, o[d].y);
+                        o[d].z = fmaf(fabsf(e.x), e.y, o[d].z);
+                        o[d].w += e.y > 0.f ? 1.f : 0.f;
+                    }
+                }
+            }
+        }
+        dst0[i] = o[0];
+        dst1[i] = o[1];
+    }
+#else
     const DevSensor &S0 = P.s[0];
     const int jr = blockIdx.y * blockDim.y + threadIdx.y;
     const int j = jr >> 1, r = jr & 1;
@@ -174,6 +249,7 @@ __global__ void __launch_bounds__(128) radiance_merge_kernel(const __grid_consta
 #pragma unroll
         for (int k = 0; k < 4; ++k) dst[k] = o[px + 2 * k];
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------
