@@ -86,3 +86,35 @@ def test_two_rank_gloo_band_split_and_frame_parallel(tmp_path):
     assert res["frames"] == [0, 1, 2, 3, 4]
     assert sorted(p.name for p in tmp_path.glob("frame_*.pfm")) == [
         f"frame_{k:06d}.pfm" for k in range(5)]
+
+
+def test_bench_gpus_n_relaunches_n_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself with one rank per
+    GPU (here: gloo, dry run -- the plumbing a SCALE run takes)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = __import__("pathlib").Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["HDR_DIST_BACKEND"] = "gloo"
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--dry-run",
+                          "--steps", "9"], env=env, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line == {"dry_run": True, "n_gpus": 2, "ranks_seen": 2, "frames_total": 9,
+                    "max_rank": 1}
+
+
+def test_bench_rejects_world_size_mismatch():
+    import os
+    import subprocess
+    import sys
+
+    root = __import__("pathlib").Path(__file__).resolve().parent.parent
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--dry-run"],
+                         env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
