@@ -42,7 +42,7 @@ extern "C" {
 
 #define HDR_LPA_MAX_SENSORS 8
 #define HDR_LPA_MAX_SCALES 8
-#define HDR_LPA_ABI_VERSION 4
+#define HDR_LPA_ABI_VERSION 5
 
 /* status codes */
 #define HDR_OK 0
@@ -51,6 +51,11 @@ extern "C" {
 #define HDR_ERR_SHAPE 3      /* inconsistent sizes            -> ShapeMismatchError  */
 #define HDR_ERR_WORKSPACE 4  /* workspace too small                                  */
 #define HDR_ERR_CUDA 5       /* CUDA launch / runtime error                          */
+#define HDR_ERR_FAULT 6      /* a kernel raised a fault bit (results incomplete)     */
+
+/* Fault bits a kernel raises in the workspace header instead of trapping
+ * (read back by hdr_lpa_workspace_status; cleared by every reconstruct call) */
+#define HDR_FAULT_MBAR_TIMEOUT 1u  /* a staging barrier wait exceeded its bound */
 
 /* Weight modes (ReconstructionParams.weight_mode, lpa.py:54-61) */
 #define HDR_WEIGHT_VARIANCE 0
@@ -237,6 +242,13 @@ int hdr_sample_planes(const HdrSensor *sensor, double *value, double *sigma, voi
 /* Number of (pixel, channel) items the last call on this workspace routed
  * through the exact slow path (device value; reads it synchronously). */
 int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream);
+
+/* Status of the last call on this workspace (synchronous read of the header):
+ * the slow-path item count and the HDR_FAULT_* bits any kernel raised.
+ * Returns HDR_ERR_FAULT when a fault bit is set (the outputs of that call are
+ * incomplete), else HDR_OK.  Either pointer may be NULL.  (ABI v5) */
+int hdr_lpa_workspace_status(const void *workspace, uint32_t *slow_items, uint32_t *fault,
+                             void *stream);
 
 /*
  * Measured float64 FMA throughput of the device (DFMA chains on every SM),

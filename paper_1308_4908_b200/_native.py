@@ -25,7 +25,9 @@ SOURCES = sorted((PKG / "csrc").glob("*.cu*")) + [ROOT / "include" / "hdr_lpa.h"
 MAX_SENSORS = 8
 MAX_SCALES = 8
 
-HDR_OK, HDR_ERR_ARG, HDR_ERR_CONFIG, HDR_ERR_SHAPE, HDR_ERR_WORKSPACE, HDR_ERR_CUDA = range(6)
+(HDR_OK, HDR_ERR_ARG, HDR_ERR_CONFIG, HDR_ERR_SHAPE, HDR_ERR_WORKSPACE, HDR_ERR_CUDA,
+ HDR_ERR_FAULT) = range(7)
+HDR_FAULT_MBAR_TIMEOUT = 1
 HDR_WEIGHT_VARIANCE, HDR_WEIGHT_SIGMA = 0, 1
 HDR_OUTCOME_NAN = 0xFF
 HDR_FLAG_FAST_ONLY = 1
@@ -41,6 +43,7 @@ EXPORTED = (
     "hdr_radiance_planes",
     "hdr_sample_planes",
     "hdr_lpa_slow_items",
+    "hdr_lpa_workspace_status",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
     "hdr_lpa_last_error",
@@ -114,12 +117,37 @@ _lock = threading.Lock()
 _lib = None
 
 
-def nvcc_command(out: Path):
-    return [
-        "nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-        "-Xcompiler", "-fPIC", "-shared", "-I", str(ROOT / "include"), "-o", str(out),
-        str(PKG / "csrc" / "hdr_lpa.cu"),
-    ]
+UNITS = ("hdr_lpa.cu", "fast_o0.cu", "fast_o1.cu", "fast_o2.cu")
+NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              "-Xcompiler", "-fPIC"]
+
+
+def compile_library(out: Path, extra_flags=(), verbose_ptxas: bool = False) -> Path:
+    """nvcc every translation unit of csrc/ for sm_100a in parallel, then link
+    the shared library ``out``."""
+    import tempfile
+
+    with tempfile.TemporaryDirectory(prefix="hdrlpa_build_") as tmp:
+        procs, objs = [], []
+        for unit in UNITS:
+            obj = Path(tmp) / (unit + ".o")
+            cmd = ["nvcc", *NVCC_FLAGS, *extra_flags, "-I", str(ROOT / "include"), "-c", "-o",
+                   str(obj), str(PKG / "csrc" / unit)]
+            if verbose_ptxas:
+                cmd[1:1] = ["-Xptxas", "-v"]
+            procs.append((unit, subprocess.Popen(cmd, stderr=subprocess.PIPE, text=True)))
+            objs.append(str(obj))
+        errs = []
+        for unit, p in procs:
+            _, err = p.communicate()
+            if p.returncode != 0:
+                errs.append(f"{unit}:\n{err}")
+            elif verbose_ptxas:
+                print(err, end="")
+        if errs:
+            raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+        subprocess.run(["nvcc", "-shared", "-o", str(out), *objs, "-lcuda"], check=True)
+    return out
 
 
 def build(force: bool = False) -> Path:
@@ -129,7 +157,7 @@ def build(force: bool = False) -> Path:
         if all(s.stat().st_mtime <= mtime for s in SOURCES):
             return LIB_PATH
     tmp = LIB_PATH.with_name(f"libhdrlpa.{os.getpid()}.tmp.so")
-    subprocess.run(nvcc_command(tmp), check=True)
+    compile_library(tmp)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -177,6 +205,8 @@ def lib():
                                             ctypes.c_void_p, ctypes.c_void_p]
             L.hdr_lpa_slow_items.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
                                              ctypes.c_void_p]
+            L.hdr_lpa_workspace_status.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
+                                                   ctypes.POINTER(ctypes.c_uint32), ctypes.c_void_p]
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
             L.hdr_lpa_status_string.restype = ctypes.c_char_p
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]
@@ -189,7 +219,7 @@ def lib():
             L.hdr_lpa_launch_count.argtypes = []
             L.hdr_lpa_kernel_timer.argtypes = [ctypes.c_int]
             L.hdr_lpa_kernel_timer_read.argtypes = [ctypes.POINTER(ctypes.c_float)]
-            if L.hdr_lpa_abi_version() != 4:
+            if L.hdr_lpa_abi_version() != 5:
                 raise RuntimeError("libhdrlpa.so ABI version mismatch")
             _lib = L
         return _lib

@@ -53,19 +53,38 @@ __device__ void ladder(const DevParams &P, int c, const Sweep &sweep, PixelResul
 // bounds; may return AMBIG) or exact.  Returns FIT_OK with R filled, FIT_FAIL
 // if scale 0 fails (the caller runs the ladder), FIT_AMBIG if a decision
 // needs the exact path.
-template <int ORDER, bool EXACT, class Sweep>
-__device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+// The running state (bounds, their error bounds, the selected estimate) lives
+// across the scale loop; the fast kernel keeps it in a per-thread shared-memory
+// slot (IciState) instead of registers, which the order-2 sweeps need.
+struct IciState {
+    double L, U;           // running intersection
+    float eL, eU;          // their error bounds (rounded up)
+    float val, gx, gy;     // estimate of the selected scale (the output is float32)
+    float tgx, tgy;        // gradient of the scale being evaluated (until it is accepted)
+    int sidx, count, precise;
+};
+struct IciRegs {  // the exact path: plain registers
+    IciState st;
+    __device__ __forceinline__ IciState &operator()() { return st; }
+};
+struct IciSmem {  // the fast path: volatile accesses keep it out of registers
+    volatile IciState *p;
+    __device__ __forceinline__ volatile IciState &operator()() { return *p; }
+};
+template <int ORDER, bool EXACT, class Sweep, class State = IciRegs>
+__device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R,
+                   State S = State()) {
     constexpr int PN = NC<ORDER>::P;
     Acc<PN> acc;
     Fit fit;
-    double L = 0.0, U = 0.0, eL = 0.0, eU = 0.0;  // running bounds and their error bounds
-    bool precise = true;
+    S().precise = 1;
     // fast row sweeps: the variance sweep of scale k and the moment sweep of
     // scale k+1 share one traversal (FusedVarMom); the moments of k+1 are
     // wasted only when the search ends at k
     constexpr bool FUSED = !EXACT && ORDER >= 1 && HasRows<Sweep>::value;
     if constexpr (FUSED) accumulate<ORDER, EXACT>(P, c, 0, P.r[c][0], P.r2[c][0], sweep, acc);
-    for (int k = 0; k < P.n_scales; ++k) {
+    int k = 0;
+    for (; k < P.n_scales; ++k) {
         if constexpr (!FUSED) accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
         R.work += acc.count;
         const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
@@ -77,6 +96,9 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         const int count_k = acc.count;
         float tk = 0.f;
         double var_k;
+        const double c0 = fit.c0;
+        S().tgx = (float)fit.c1;  // parked in the state while the next sweep runs
+        S().tgy = (float)fit.c2;
         if constexpr (FUSED) {
             RowVariance<ORDER> V{fit.g, P.hl[c][k], (bool)P.use_sigma, 0.0, 0.0, 0.0, 0.f};
             if (k + 1 < P.n_scales) {
@@ -93,31 +115,45 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
             var_k = fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk);
         }
         const double sd = sqrt(var_k);
-        const double lo = fit.c0 - P.gamma * sd, hi = fit.c0 + P.gamma * sd;
+        const double lo = c0 - P.gamma * sd, hi = c0 + P.gamma * sd;
         // fast path: error bound of lo/hi (fp32 rounding of c0: fit_precise_sharp;
         // of sd: ICI_SD_EPS relative) -- an intersection test closer than the
         // bounds is decided by the exact path, so scale indices stay exact
-        const double ek = EXACT ? 0.0 : 2.0 * FAST_EPS * (double)tk + P.gamma * sd * ICI_SD_EPS;
+        const float ek =
+            EXACT ? 0.f
+                  : __double2float_ru(2.0 * FAST_EPS * (double)tk + P.gamma * sd * ICI_SD_EPS);
         if (k == 0) {
-            L = lo;
-            U = hi;
-            eL = eU = ek;
+            S().L = lo;
+            S().U = hi;
+            S().eL = ek;
+            S().eU = ek;
         } else {
-            if (lo >= L) eL = lo > L ? ek : fmax(eL, ek);
-            if (hi <= U) eU = hi < U ? ek : fmax(eU, ek);
+            double L = S().L, U = S().U;
+            float eL = S().eL, eU = S().eU;
+            if (lo >= L) eL = lo > L ? ek : fmaxf(eL, ek);
+            if (hi <= U) eU = hi < U ? ek : fmaxf(eU, ek);
             L = fmax(L, lo);
             U = fmin(U, hi);
-            if (!EXACT && fabs(L - U) <= eL + eU) return FIT_AMBIG;
+            if (!EXACT && fabs(L - U) <= (double)eL + (double)eU) return FIT_AMBIG;
             if (L > U) break;
+            S().L = L;
+            S().U = U;
+            S().eL = eL;
+            S().eU = eU;
         }
-        R.val = fit.c0;
-        R.gx = fit.c1;
-        R.gy = fit.c2;
-        R.sidx = k;
-        R.count = count_k;
-        if constexpr (!EXACT) precise = fit_precise_sharp(fit.c0, tk, P.prec_floor);
+        S().val = (float)c0;  // write_result rounds max(val, 0) to float32 anyway
+        S().gx = S().tgx;
+        S().gy = S().tgy;
+        S().sidx = k;
+        S().count = count_k;
+        if constexpr (!EXACT) S().precise = fit_precise_sharp(c0, tk, P.prec_floor) ? 1 : 0;
     }
-    if (!precise) return FIT_PREC;  // selected estimate too close to fp32 rounding limits
+    R.val = S().val;
+    R.gx = S().gx;
+    R.gy = S().gy;
+    R.sidx = S().sidx;
+    R.count = S().count;
+    if (!S().precise) return FIT_PREC;  // selected estimate too close to fp32 rounding limits
     if (ORDER == 0) R.gx = R.gy = qnan();
     R.outcome = ORDER * 16;
     return FIT_OK;
@@ -152,7 +188,7 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
     constexpr int G = SLOW_LANES;  // lanes per work item
-    const uint32_t n = *P.work_count;
+    const uint32_t n = P.all_items ? P.all_items : *P.work_count;
     // items are fetched dynamically (their cost varies by orders of magnitude)
     const unsigned gmask = G >= 32 ? 0xffffffffu
                                    : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
@@ -162,7 +198,7 @@ __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ D
         if ((threadIdx.x & (G - 1)) == 0) i = atomicAdd(P.slow_counter, 1u);
         i = __shfl_sync(gmask, i, leader);
         if (i >= n) break;
-        const uint32_t item = P.work_items[i];
+        const uint32_t item = P.all_items ? (((i / 3u) << 6) | (i % 3u)) : P.work_items[i];
         const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
         const int kk = (int)((item >> 2) & 15);
         const int ox = pix % P.out_w, oy = pix / P.out_w;

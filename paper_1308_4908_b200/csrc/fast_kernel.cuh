@@ -205,7 +205,7 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
     }
 }
 
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER, bool MRGS>
+template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER, bool MRGS, bool ICISM>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int tcol, int trow,
                                              const int (*org)[2], bool tile_covered,
@@ -295,7 +295,15 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
                     R.outcome = ORDER * 16;  // phase 0 (anisotropic), radius step 0
                 }
             } else if constexpr (ICI) {
-                st = ici<ORDER, false>(P, c, sweep, R);
+                // ICISM: the running ICI state in a per-thread shared-memory slot
+                // (frees ~20 registers the order-2 sweeps spill without it; the
+                // host picks it when it costs no occupancy)
+                if constexpr (ICISM) {
+                    __shared__ IciState s_ici[NT];
+                    st = ici<ORDER, false>(P, c, sweep, R, IciSmem{&s_ici[threadIdx.x]});
+                } else {
+                    st = ici<ORDER, false>(P, c, sweep, R);
+                }
             } else {
                 Acc<PN> acc;
                 if constexpr (MRG)
@@ -359,7 +367,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 // merged samples (radiance_merge_kernel)
 // MRGS: CALPA's steered pass over co-sited merged planes (ORDER >= 1)
 template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false,
-          bool MRGS = false>
+          bool MRGS = false, bool ICISM = false>
 // Per-sensor tap kernels are held to 80 registers: 3 CTAs per SM beat 2 by
 // ~8% on cfg2 and 4 (64 registers) measured ~2% slower than 3.
 #ifndef HDR_STEER_MINBLOCKS
@@ -442,10 +450,10 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
     for (int i = 0;; ++i) {
         const int b = i % NBUF;
         unsigned char *pb = planes + b * P.buf_stride;
-        mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1));
+        if (!mbar_wait(&bar_full[b], (uint32_t)((i / NBUF) & 1), P.fault)) break;
         const int t = s_tile[b];
         if (t < 0) break;
-        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>(P, pb, taps, s_tcol[b], s_trow[b], s_org[b],
+        tile_compute<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS, ICISM>(P, pb, taps, s_tcol[b], s_trow[b], s_org[b],
                                                        s_cov[b] != 0, HDR_ROW_ROT ? (i & 1) : 0);
         __syncwarp();
         unsigned last = 0;

@@ -1,0 +1,8 @@
+// fast_o1.cu -- the order-1 fast tile kernels and exact path (launch_all<1>),
+// a separate translation unit so the library's kernels compile in parallel.
+#include "launch.cuh"
+
+namespace hdrlpa {
+template int launch_all<1>(const DevParams &, const DevParams &, const TapParam &, int, int, int,
+                            cudaStream_t);
+}  // namespace hdrlpa

@@ -1,6 +1,8 @@
 // hdr_lpa.cu -- host side and C ABI (include/hdr_lpa.h) of the sm_100a
-// unified HDR LPA operator.  The kernels live in the headers below (one
-// translation unit, so every template instantiation is visible here).
+// unified HDR LPA operator.  The kernels live in the headers; the per-order
+// fast/slow kernel launches (launch_all<ORDER>) are instantiated in
+// fast_o0.cu / fast_o1.cu / fast_o2.cu (separate translation units, compiled
+// in parallel), everything else here.
 //
 // Pipeline per frame (one stream, no host synchronisation):
 //   1. memset of the exact-path work counter (+ row-tap table copy, RT mode)
@@ -25,9 +27,8 @@
 #include <string.h>
 
 #include "hdr_lpa.h"
-#include "config.cuh"
+#include "launch.cuh"
 #include "frame_kernels.cuh"
-#include "fast_kernel.cuh"
 #include "calpa.cuh"
 #include "samples.cuh"
 
@@ -100,59 +101,29 @@ static int fill_sensor(const HdrSensor &h, DevSensor &d) {
     return HDR_OK;
 }
 
-static thread_local char g_last_error[256] = "";
+thread_local char g_last_error[256] = "";
 // kernel launches issued by this library since load (hdr_lpa_launch_count)
-static std::atomic<unsigned long long> g_launches{0};
-#define COUNT_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
+std::atomic<unsigned long long> g_launches{0};
 
-static int cuda_fail(const char *where) {
+int cuda_fail(const char *where) {
     const cudaError_t e = cudaGetLastError();
     snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
     return HDR_ERR_CUDA;
 }
 
-static int set_smem_attr(const void *fn, int bytes) {
+int set_smem_attr(const void *fn, int bytes) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     return e == cudaSuccess ? HDR_OK : cuda_fail("cudaFuncSetAttribute(smem)");
 }
 
 // hdr_lpa_kernel_timer: an event pair around each eager fast-kernel launch
-static thread_local bool g_timer_on = false;
-static thread_local cudaEvent_t g_timer_ev[2] = {nullptr, nullptr};
-static thread_local bool g_timer_recorded = false;
-static bool timer_active(cudaStream_t st) {
+thread_local bool g_timer_on = false;
+thread_local cudaEvent_t g_timer_ev[2] = {nullptr, nullptr};
+thread_local bool g_timer_recorded = false;
+bool timer_active(cudaStream_t st) {
     if (!g_timer_on) return false;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
-}
-
-template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false,
-          bool MRGS = false>
-static int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
-                       cudaStream_t st) {
-    const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>;
-    if (set_smem_attr(fn, smem_bytes) != HDR_OK) return HDR_ERR_CUDA;
-    int dev = 0, nsm = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem_bytes) != cudaSuccess ||
-        per_sm < 1)
-        return cuda_fail("occupancy query");
-    const int grid = min(tiles, nsm * per_sm);  // persistent: every CTA loops over tiles
-    const bool timed = timer_active(st);
-    if (timed) cudaEventRecord(g_timer_ev[0], st);
-    COUNT_LAUNCH();
-    if constexpr (PAT)
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS><<<grid, NT, smem_bytes, st>>>(P, T);
-    else
-        lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS>
-            <<<grid, NT, smem_bytes, st>>>(P, NoTaps{});
-    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_fast_kernel launch");
-    if (timed) {
-        cudaEventRecord(g_timer_ev[1], st);
-        g_timer_recorded = true;
-    }
-    return HDR_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -189,42 +160,6 @@ static bool encode_phase_map(const DevSensor &d, CUtensorMap *map, bool merged =
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Pf: the fast kernel's parameters (a one-sensor view over the merged planes
-// in co-sited mode), P: the full rig for the exact path.
-template <int ORDER>
-static int launch_all(const DevParams &Pf, const DevParams &P, const TapParam &T, int tiles,
-                      int smem_bytes, int maxc, cudaStream_t st) {
-    int rc;
-    const bool cnt = P.count || P.work;
-    if (Pf.merged)
-        rc = cnt ? launch_fast<ORDER, false, 4, 3>(Pf, T, tiles, smem_bytes, st)
-                 : launch_fast<ORDER, false, 4, 4>(Pf, T, tiles, smem_bytes, st);
-    else if (P.pat)
-        rc = cnt ? launch_fast<ORDER, false, 4, 1>(P, T, tiles, smem_bytes, st)
-                 : launch_fast<ORDER, false, 4, 2>(P, T, tiles, smem_bytes, st);
-    else if (P.rt && P.n_scales > 1)
-        rc = maxc <= 6 ? launch_fast<ORDER, true, 6, 0, true>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, true, 8, 0, true>(P, T, tiles, smem_bytes, st);
-    else if (P.rt)
-        rc = maxc <= 4 ? launch_fast<ORDER, false, 4, 0, true>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, false, 8, 0, true>(P, T, tiles, smem_bytes, st);
-    else if (P.n_scales > 1)
-        rc = maxc <= 6 ? launch_fast<ORDER, true, 6>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, true, 8>(P, T, tiles, smem_bytes, st);
-    else
-        rc = maxc <= 4 ? launch_fast<ORDER, false, 4>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, false, 8>(P, T, tiles, smem_bytes, st);
-    if (rc != HDR_OK) return rc;
-    if (P.flags & HDR_FLAG_FAST_ONLY) return HDR_OK;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    COUNT_LAUNCH();
-    lpa_slow_kernel<ORDER><<<nsm * 4, 128, 0, st>>>(P);
-    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_slow_kernel launch");
-    return HDR_OK;
-}
-
 // Pre-computed-weight mode: applies when the output grid is the
 // reference grid and every sensor is translation-only.  Then, for an output
 // pixel q = (j, i), sensor pixel x = j + k maps to X = fl(x + T02) and
@@ -249,7 +184,7 @@ static bool build_rowtaps(DevParams &P, std::vector<unsigned char> &table) {
         shift = 1;  // 2x output grid: classes repeat every 4 output pixels
     else
         return false;
-    const int period = 2 << shift;
+    const int period = 2 << shift, ncls = period * period, nj = P.n_scales;
     bool any = false;
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
@@ -260,9 +195,9 @@ static bool build_rowtaps(DevParams &P, std::vector<unsigned char> &table) {
         any = true;
     }
     if (!any) return false;
-    RtHeader hd;
-    memset(&hd, 0, sizeof(hd));
-    std::vector<TapRow> rows;
+    std::vector<int> hdr((size_t)P.n_sensors * 3 * ncls * nj * 2, 0);  // int2 {row0, nrow}
+    std::vector<double> row_dy;
+    std::vector<uint32_t> row_fn;
     std::vector<RowTap> taps;
     for (int s = 0; s < P.n_sensors; ++s) {
         const DevSensor &S = P.s[s];
@@ -272,78 +207,102 @@ static bool build_rowtaps(DevParams &P, std::vector<unsigned char> &table) {
             for (int c = 0; c < 3; ++c)
                 if ((S.phmask[c] >> ph) & 1) tile[ph] = c;
         const int pw = S.rw >> 1, plane = pw * (S.rh >> 1);
+        if (4 * plane * (int)sizeof(float2) >= (1 << 23)) return false;  // 24-bit offsets
         for (int c = 0; c < 3; ++c) {
             double rmax2 = 0.0, rmax = 0.0;
-            for (int k = 0; k < P.n_scales; ++k) {
+            for (int k = 0; k < nj; ++k) {
                 rmax2 = fmax(rmax2, P.r2[c][k]);
                 rmax = fmax(rmax, P.r[c][k]);
             }
             const int R = (int)ceil(rmax + fabs(S.T[2]) + fabs(S.T[5])) + 2;
-            for (int cl = 0; cl < period * period; ++cl) {
+            for (int cl = 0; cl < ncls; ++cl) {
                 // representative output pixel of the class and its anchor
                 const int j = 128 + cl % period, i = 128 + cl / period;
                 const double qx = ((double)j + 0.5) * P.sx + -0.5;  // qcoord (lpa.py:222-223)
                 const double qy = ((double)i + 0.5) * P.sy + -0.5;
                 const int ax = j >> shift, ay = i >> shift;
-                hd.row0[s][c][cl] = (int)rows.size();
+                std::vector<double> kdy[MAXJ];
+                std::vector<uint32_t> kfn[MAXJ];
                 for (int m = -R; m <= R; ++m) {
                     const int y = ay + m;
-                    TapRow row;
-                    memset(&row, 0, sizeof(row));
-                    row.first = (int)taps.size();
+                    const int first = (int)taps.size();
                     std::vector<double> d2s;
+                    double dy = 0.0;
                     for (int k2 = -R; k2 <= R; ++k2) {
                         const int x = ax + k2;
                         if (tile[((y & 1) << 1) | (x & 1)] != c) continue;
+                        // the reference's arithmetic: apply_transform (radiometry.py:84),
+                        // d = X - q and |d|^2 (_kernels.py:160-162)
                         const double X = (1.0 * (double)x + 0.0 * (double)y) + S.T[2];
                         const double Y = (0.0 * (double)x + 1.0 * (double)y) + S.T[5];
-                        const double dx = X - qx, dy = Y - qy;
+                        const double dx = X - qx;
+                        dy = Y - qy;
                         const double d2 = dx * dx + dy * dy;
-                        for (int k = 0; k < P.n_scales; ++k)
+                        for (int k = 0; k < nj; ++k)
                             if (fabs(d2 - P.r2[c][k]) <= 1e-9 * P.r2[c][k]) return false;
                         if (d2 > rmax2) continue;
+                        int kmin = nj;
+                        for (int k = nj - 1; k >= 0; --k)
+                            if (d2 <= P.r2[c][k]) kmin = k;
+                        const int ph = ((y & 1) << 1) | (x & 1);
+                        const int off = (int)sizeof(float2) *
+                                        (ph * plane + ((y >> 1) - (ay >> 1)) * pw + ((x >> 1) - (ax >> 1)));
                         RowTap t;
                         t.dx = dx;
                         t.d2f = (float)d2;
-                        const int ph = ((y & 1) << 1) | (x & 1);
-                        t.off = (int)sizeof(float2) *
-                                (ph * plane + ((y >> 1) - (ay >> 1)) * pw + ((x >> 1) - (ax >> 1)));
+                        t.off = rt_pack(off, kmin);
                         taps.push_back(t);
                         d2s.push_back(d2);
-                        row.dy = dy;
                     }
                     const int n = (int)d2s.size();
-                    if (!n) continue;
-                    if (n > 255) return false;
-                    for (int k = 0; k < P.n_scales; ++k) {
+                    for (int k = 0; k < nj; ++k) {
                         int lo = n, hi = 0;
                         for (int u = 0; u < n; ++u)
                             if (d2s[u] <= P.r2[c][k]) {
                                 lo = std::min(lo, u);
                                 hi = u + 1;
                             }
-                        if (lo >= hi) lo = hi = 0;
-                        row.lo[k] = (unsigned char)lo;
-                        row.hi[k] = (unsigned char)hi;
+                        if (lo >= hi) continue;
+                        for (int u = lo; u < hi; ++u)  // convexity: the run has no holes
+                            if (!(d2s[u] <= P.r2[c][k])) return false;
+                        if (hi - lo >= (1 << (32 - RT_ROW_N_SHIFT))) return false;
+                        kdy[k].push_back(dy);
+                        kfn[k].push_back((uint32_t)(first + lo) | ((uint32_t)(hi - lo) << RT_ROW_N_SHIFT));
                     }
-                    rows.push_back(row);
                 }
-                hd.nrow[s][c][cl] = (int)rows.size() - hd.row0[s][c][cl];
+                for (int k = 0; k < nj; ++k) {
+                    const size_t h = 2 * ((((size_t)s * 3 + c) * ncls + cl) * nj + k);
+                    hdr[h] = (int)row_dy.size();
+                    hdr[h + 1] = (int)kdy[k].size();
+                    row_dy.insert(row_dy.end(), kdy[k].begin(), kdy[k].end());
+                    row_fn.insert(row_fn.end(), kfn[k].begin(), kfn[k].end());
+                }
             }
         }
     }
-    hd.n_rows = (int)rows.size();
-    const size_t bytes =
-        sizeof(RtHeader) + rows.size() * sizeof(TapRow) + taps.size() * sizeof(RowTap);
+    if (taps.size() >= (1u << RT_ROW_N_SHIFT)) return false;
+    const size_t a16 = 15;
+    const size_t hbytes = (hdr.size() * sizeof(int) + a16) & ~a16;
+    const size_t dybytes = (row_dy.size() * sizeof(double) + a16) & ~a16;
+    const size_t fnbytes = (row_fn.size() * sizeof(uint32_t) + a16) & ~a16;
+    const size_t bytes = hbytes + dybytes + fnbytes + taps.size() * sizeof(RowTap);
     if (bytes > RT_TABLE_BYTES) return false;
-    table.resize(bytes);
-    memcpy(table.data(), &hd, sizeof(hd));
-    memcpy(table.data() + sizeof(hd), rows.data(), rows.size() * sizeof(TapRow));
-    memcpy(table.data() + sizeof(hd) + rows.size() * sizeof(TapRow), taps.data(),
-           taps.size() * sizeof(RowTap));
+    table.assign(bytes, 0);
+    memcpy(table.data(), hdr.data(), hdr.size() * sizeof(int));
+    memcpy(table.data() + hbytes, row_dy.data(), row_dy.size() * sizeof(double));
+    memcpy(table.data() + hbytes + dybytes, row_fn.data(), row_fn.size() * sizeof(uint32_t));
+    memcpy(table.data() + hbytes + dybytes + fnbytes, taps.data(), taps.size() * sizeof(RowTap));
     P.rt_period = period;
     P.rt_shift = shift;
+    P.rt_ncls = ncls;
+    P.rt_nj = nj;
+    P.rt_dy_off = (int)hbytes;
+    P.rt_fn_off = (int)(hbytes + dybytes);
+    P.rt_taps_off = (int)(hbytes + dybytes + fnbytes);
     P.tab_bytes = (int)bytes;
+    if (getenv("HDR_DEBUG_RT"))
+        fprintf(stderr, "row-tap table: %zu taps, %zu rows, %zu bytes\n", taps.size(),
+                row_dy.size(), bytes);
     return true;
 }
 
@@ -476,6 +435,7 @@ const char *hdr_lpa_status_string(int status) {
         case HDR_ERR_SHAPE: return "dimension mismatch";
         case HDR_ERR_WORKSPACE: return "workspace too small";
         case HDR_ERR_CUDA: return "CUDA error";
+        case HDR_ERR_FAULT: return "kernel fault";
         default: return "unknown status";
     }
 }
@@ -583,6 +543,7 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.work_count = (uint32_t *)workspace;
     P.tile_counter = (uint32_t *)workspace + 1;
     P.slow_counter = (uint32_t *)workspace + 2;
+    P.fault = (uint32_t *)workspace + 3;
     P.rt_global = (const unsigned char *)workspace + WS_HEADER;
     char *wsp = (char *)workspace + WS_HEADER + RT_TABLE_BYTES;
     for (int s = 0; s < n_sensors; ++s) {
@@ -649,6 +610,7 @@ static bool cosited(const DevParams &P) {
 
 // Staged-region geometry, shared-memory layout, tap tables (when allowed) and
 // TMA descriptors of the fast kernels, for windows up to radius fastR.
+constexpr int STAGING_TOO_LARGE = -1;  // setup_staging: the tiles do not fit shared memory
 static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_taps, TapParam &T,
                          std::vector<unsigned char> &rt_table, int &smem_bytes, int &maxc) {
     // Staged region per sensor: tile extent in sensor space + 2 x window
@@ -710,7 +672,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
     }
     P.buf_stride = smem;
     smem_bytes = P.plane_base + nbuf_for(P.pat) * P.buf_stride;
-    if (smem_bytes > 200 * 1024) return HDR_ERR_ARG;  // window too large for the staged path
+    if (smem_bytes > 200 * 1024) return STAGING_TOO_LARGE;  // windows too large to stage
     for (int s = 0; s < n_sensors; ++s)
         if (!encode_phase_map(P.s[s], &P.tmap[s], P.merged != 0)) {
             snprintf(g_last_error, sizeof(g_last_error), "cuTensorMapEncodeTiled failed (sensor %d)", s);
@@ -747,7 +709,15 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
     }
     if (!merged) {
         const int rc = setup_staging(P, n_sensors, fastR, true, T, rt_table, smem_bytes, maxc);
-        if (rc != HDR_OK) return rc;
+        if (rc == STAGING_TOO_LARGE) {
+            // the staged tiles of this rig (many sensors, large windows or ICI
+            // scales) do not fit shared memory: every (pixel, channel) goes
+            // through the exact path, which reads the raw frames directly
+            P.rt = 0;
+            P.all_items = (uint32_t)((row_end - row_begin) * out_w * 3);
+        } else if (rc != HDR_OK) {
+            return rc;
+        }
     }
     cudaStream_t st = (cudaStream_t)stream;
     P.tiles_y = (row_end - row_begin + TH - 1) / TH;
@@ -987,6 +957,25 @@ int hdr_fp64_peak_probe(double *flops_per_s, void *stream) {
     cudaFree(sink);
     if (cudaGetLastError() != cudaSuccess) return HDR_ERR_CUDA;
     *flops_per_s = (double)blocks * 256 * iters * 8 * 2 / (best * 1e-3);
+    return HDR_OK;
+}
+
+int hdr_lpa_workspace_status(const void *workspace, uint32_t *slow_items, uint32_t *fault,
+                             void *stream) {
+    if (!workspace) return HDR_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t hdr[4];
+    if (cudaMemcpyAsync(hdr, workspace, sizeof(hdr), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return cuda_fail("workspace status copy");
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("workspace status sync");
+    if (slow_items) *slow_items = hdr[0];
+    if (fault) *fault = hdr[3];
+    if (hdr[3]) {
+        snprintf(g_last_error, sizeof(g_last_error),
+                 "kernel fault 0x%x (staging barrier timed out: the tile results are incomplete)",
+                 hdr[3]);
+        return HDR_ERR_FAULT;
+    }
     return HDR_OK;
 }
 

@@ -83,27 +83,28 @@ struct __align__(16) TapParam {
 };
 struct NoTaps {};
 // Row taps (RT mode): per (translation-only sensor, channel, parity class) the
-// sensor rows of the largest ICI window, each with its exact dy and its taps
-// (exact dx, |d|^2, sample offset) in column order; per scale k the taps
-// [lo[k], hi[k]) of a row are the ones inside r_k (a contiguous run).
+// taps of the largest ICI window in (sensor row, column) order, each with its
+// exact offset dx, |d|^2 (fp32, for the window weight), its byte offset in the
+// staged phase planes and the smallest scale whose disk contains it.  Per
+// scale k a list of rows {exact dy, the run of taps inside r_k}: |d|^2 is
+// convex along a row, so each scale's members are one contiguous run.  A
+// traversal of scale k reads only its own rows and taps -- no membership
+// test, no empty rows -- and the fused ICI traversal tells the inner scale's
+// members by kmin <= kin.
+constexpr int RT_CLASSES = 16;  // (out x mod period) + period * (out y mod period), period <= 4
 struct __align__(16) RowTap {
     double dx;
     float d2f;
-    int off;  // byte offset of the sample from the pixel's own phase-plane position
+    int off;  // bits 0-23: byte offset of the sample from the pixel's phase-plane position
+              // (signed, 24 bits); bits 24-31: smallest scale index whose disk holds the tap
 };
-// RT table layout: RtHeader, then TapRow[n_rows], then RowTap[n_taps].
-constexpr int RT_CLASSES = 16;  // (out x mod period) + period * (out y mod period), period <= 4
-struct RtHeader {
-    int row0[MAXS][3][RT_CLASSES];
-    int nrow[MAXS][3][RT_CLASSES];
-    int n_rows, pad[3];
-};
-struct __align__(16) TapRow {
-    double dy;
-    int first;  // index of the row's first RowTap
-    int pad;
-    unsigned char lo[8], hi[8];
-};
+__host__ __device__ constexpr int rt_pack(int off, int kmin) { return (off & 0xffffff) | (kmin << 24); }
+__device__ __forceinline__ int rt_off(int v) { return (v << 8) >> 8; }
+__device__ __forceinline__ int rt_kmin(int v) { return (int)((unsigned)v >> 24); }
+// Table layout: int2 {first row, row count} per (sensor, channel, class, scale)
+// (index ((s * 3 + c) * rt_ncls + cls) * rt_nj + k), then the rows as two
+// arrays (dy: double[n_rows], first | n << 20: uint32[n_rows]), then RowTap[].
+constexpr int RT_ROW_N_SHIFT = 20;
 
 struct DevParams {
     CUtensorMap tmap[MAXS];   // per-sensor 3-D maps over the phase planes (box = staged region)
@@ -136,6 +137,8 @@ struct DevParams {
     int pat, n_taps, off_taps, tab_bytes;  // tab_bytes: kernel-parameter table size (PAT or RT)
     int rt;                         // row-tap mode (ICI / order 2 with translation-only sensors)
     int rt_period, rt_shift;        // RT: class period (2 / 4) and anchor shift (0 / 1) for sx 1 / 0.5
+    int rt_ncls, rt_nj;             // RT: classes (period^2) and scales of the table
+    int rt_dy_off, rt_fn_off, rt_taps_off;  // RT: byte offsets of the row arrays and RowTap[]
     const unsigned char *rt_global; // RT: the table in the workspace (copied to shared memory)
     int plane_base, buf_stride;     // shared memory: plane buffer b at plane_base + b*buf_stride
     int pat_off[MAXS][3][4];        // first tap of (sensor, channel, class = (y&1)*2 + (x&1))
@@ -143,6 +146,9 @@ struct DevParams {
     uint32_t *work_count;
     uint32_t *tile_counter;          // fast kernel: next tile to hand out (workspace header)
     uint32_t *slow_counter;          // exact path: next work item to evaluate
+    uint32_t *fault;                 // HDR_FAULT_* bits raised by a kernel (workspace header)
+    uint32_t all_items;              // > 0: no fast kernel; the exact path evaluates every
+                                     // (pixel, channel) of the band (item i: pixel i / 3, channel i % 3)
     uint32_t *work_items;
     // CALPA steered pass: per output pixel steering field (theta, sigma, gamma)
     const double *st_theta, *st_sigma, *st_gamma;
@@ -669,7 +675,7 @@ __device__ __forceinline__ void eig_range3(const double *A, double &lmin, double
 }
 
 // p == 6: cyclic Jacobi (the reference calls LAPACK dsyevd, _kernels.py:72)
-__device__ __noinline__ void eig_range6(const double *A, double &lmin, double &lmax) {
+static __device__ __noinline__ void eig_range6(const double *A, double &lmin, double &lmax) {
     double M[6][6];
 #pragma unroll
     for (int i = 0; i < 6; ++i)

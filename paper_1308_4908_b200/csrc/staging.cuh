@@ -23,20 +23,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
         : "memory");
 }
 // Bounded wait: a barrier that never completes (a lost TMA transaction)
-// traps -- the launch fails with an error -- instead of hanging the GPU.
-// try_wait carries a suspend-time hint, so a waiting warp is parked until
-// the phase completes instead of spinning through the issue slots of the
-// warps that compute (busy polling was ~10 % of the tap kernel's
-// instructions); the bound is 2 s of %globaltimer.
+// must not hang the GPU.  try_wait carries a suspend-time hint, so a waiting
+// warp is parked until the phase completes instead of spinning through the
+// issue slots of the warps that compute (busy polling was ~10 % of the tap
+// kernel's instructions).  After HDR_MBAR_TIMEOUT_NS of %globaltimer the wait
+// gives up: it raises HDR_FAULT_MBAR_TIMEOUT in the workspace header's fault
+// word (read back by hdr_lpa_workspace_status) and returns false, and the
+// caller's warp leaves the kernel.  No __trap: preemption, time-slicing or a
+// debugger can stretch a healthy wait, and a trap kills the whole context.
 #ifndef HDR_MBAR_SLEEP
 #define HDR_MBAR_SLEEP 0  // ns of __nanosleep between failed polls
+#endif
+#ifndef HDR_MBAR_TIMEOUT_NS
+#define HDR_MBAR_TIMEOUT_NS 20000000000ull  // 20 s
 #endif
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_wait(uint64_t *bar, uint32_t parity, uint32_t *fault) {
     uint32_t done = 0;
     uint64_t t0 = 0;
     for (;;) {
@@ -46,13 +52,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "=r"(done)
             : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
             : "memory");
-        if (done) return;
+        if (done) return true;
 #if HDR_MBAR_SLEEP > 0
         __nanosleep(HDR_MBAR_SLEEP);
 #endif
         const uint64_t now = global_ns();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > 2000000000ull) __trap();
+        if (t0 == 0) {
+            t0 = now;
+        } else if (now - t0 > HDR_MBAR_TIMEOUT_NS) {
+            atomicOr(fault, (uint32_t)HDR_FAULT_MBAR_TIMEOUT);
+            return false;
+        }
     }
 }
 __device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParams &P, int tx0,

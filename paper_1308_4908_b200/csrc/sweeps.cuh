@@ -142,43 +142,39 @@ struct TileSweep {
     }
 
     // RT: the pre-computed rows of a translation-only sensor at scale k (all
-    // taps inside r_k by construction; masked samples contribute weight 0).
-    // kin >= 0: each sample also carries `inner` = inside the window of scale
-    // kin <= k (a fused traversal: variance at kin, moments at k)
+    // taps inside r_k by construction; masked samples carry 1/den = 0).
+    // kin >= 0: each sample also carries the inner scale's window weight
+    // W[kin] (0 outside r_kin): a fused traversal, variance at kin, moments at k.
     template <class Pol>
     __device__ __forceinline__ void tap_rows(int s, int c, int k, Pol &pol, int kin = -1) const {
         const DevSensor &S = P.s[s];
         const int pm = P.rt_period - 1;
         const int cls = (py & pm) * P.rt_period + (px & pm);
-        const RtHeader &hd = *(const RtHeader *)rt;
-        const int r0 = hd.row0[s][c][cls], nr = hd.nrow[s][c][cls];
-        const TapRow *rows = (const TapRow *)(rt + sizeof(RtHeader));
-        const RowTap *taps =
-            (const RowTap *)(rt + sizeof(RtHeader) + (size_t)hd.n_rows * sizeof(TapRow));
+        const int2 rr = ((const int2 *)rt)[((s * 3 + c) * P.rt_ncls + cls) * P.rt_nj + k];
+        const double *rdy = (const double *)(rt + P.rt_dy_off);
+        const uint32_t *rfn = (const uint32_t *)(rt + P.rt_fn_off);
+        const RowTap *taps = (const RowTap *)(rt + P.rt_taps_off);
         const int pw = S.rw >> 1;
         // the pixel's anchor: its own sensor pixel (sx = 1) or cell (sx = 1/2)
         const int ax = px >> P.rt_shift, ay = py >> P.rt_shift;
         const unsigned char *vb = sm + S.off_vi +
                                   8 * (((ay - org[s][1]) >> 1) * pw + ((ax - org[s][0]) >> 1));
-        for (int ri = r0; ri < r0 + nr; ++ri) {
-            const TapRow &R = rows[ri];
-            const int lo = R.lo[k], hi = R.hi[k];
-            if (lo >= hi) continue;
-            // the inner scale's run [ilo, ihi) lies inside [lo, hi) (nested disks)
-            const int ilo = kin >= 0 ? R.first + R.lo[kin] : 0;
-            const int ihi = kin >= 0 ? R.first + R.hi[kin] : 1 << 30;
-            const double dy = R.dy, dyy = dy * dy;
+        for (int ri = rr.x; ri < rr.x + rr.y; ++ri) {
+            const double dy = rdy[ri], dyy = dy * dy;
+            const uint32_t fn = rfn[ri];
             pol.begin_row(dy, dyy);
+            const RowTap *t = taps + (fn & ((1u << RT_ROW_N_SHIFT) - 1));
+            const RowTap *te = t + (fn >> RT_ROW_N_SHIFT);
 #ifndef HDR_RT_UNROLL
 #define HDR_RT_UNROLL 1
 #endif
             constexpr int kRtUnroll = HDR_RT_UNROLL;
 #pragma unroll kRtUnroll
-            for (int t = R.first + lo; t < R.first + hi; ++t) {
-                const RowTap T = taps[t];
-                const float2 e = *(const float2 *)(vb + T.off);
+            for (; t < te; ++t) {
+                const RowTap T = *t;
+                const float2 e = *(const float2 *)(vb + rt_off(T.off));
                 pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f,
-                           t >= ilo && t < ihi);
+                           rt_kmin(T.off) <= kin);
             }
             pol.end_row(dy, dyy);
         }

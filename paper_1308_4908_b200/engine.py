@@ -335,12 +335,19 @@ class DeviceRig:
         return CapturedReconstruction(graph, out, n_kernels, list(self.raws))
 
     def slow_items(self, out_size) -> int:
-        """Work items the last reconstruct on this output size sent to the slow path."""
+        """Work items the last reconstruct on this output size sent to the slow
+        path (raises RuntimeError if that call's kernels raised a fault)."""
+        return self.status(out_size)
+
+    def status(self, out_size, stream=None) -> int:
+        """Synchronous check of the last reconstruct on this output size: the
+        slow-path item count; RuntimeError if a kernel raised a fault bit
+        (e.g. a staging-barrier timeout -- the outputs are incomplete)."""
         ws = self.workspace(int(out_size[0]), int(out_size[1]))
-        n = ctypes.c_uint32()
-        st = torch.cuda.current_stream(self.device)
-        N.check(N.lib().hdr_lpa_slow_items(ws.data_ptr(), ctypes.byref(n), st.cuda_stream),
-                "hdr_lpa_slow_items")
+        n, f = ctypes.c_uint32(), ctypes.c_uint32()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        N.check(N.lib().hdr_lpa_workspace_status(ws.data_ptr(), ctypes.byref(n), ctypes.byref(f),
+                                                 st.cuda_stream), "hdr_lpa_workspace_status")
         return int(n.value)
 
     # -- auxiliary outputs ---------------------------------------------------
@@ -406,7 +413,8 @@ class DeviceRig:
             tile = torch.as_tensor(np.asarray(cfg.pattern.flat_tile(), np.uint8), device=self.device)
             ch = tile[(ys % 2) * 2 + xs % 2]
             cols.append((torch.stack([X, Y], 1), ch, v.reshape(-1)[idx], s.reshape(-1)[idx],
-                         torch.full((len(idx),), k, dtype=torch.int32, device=self.device)))
+                         torch.full((len(idx),), int(cfg.sensor_id), dtype=torch.int32,
+                                    device=self.device)))  # radiometry.py:335
         return tuple(torch.cat([c[i] for c in cols]) for i in range(5))
 
 

@@ -151,6 +151,7 @@ def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=return_gradients)
     img = HDRImage(to_host(out["rgb"]))
+    rig.status(out_size)  # synchronous API: surface a kernel fault (after the sync above)
     if not return_gradients:
         return img
     g = to_host(out["grad"].double())

@@ -1,5 +1,10 @@
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
-for i in 1 2; do for lib in exp/lib_base.so exp/lib_sharp.so; do
-  HDR_LPA_LIB=$lib timeout 300 python bench.py --steps 50 --warmup 5 --workload cfg2 --no-cpu-baseline > gpurun_out/exp_$(basename $lib .so)_$i.json 2>/dev/null
-  echo "$lib: $(python scripts/bench_summary.py gpurun_out/exp_$(basename $lib .so)_$i.json | cut -c1-140)"
-done; done
+#!/bin/bash
+# A/B of exp/lib_*.so on workloads (bench lines), optional parity tests with the first lib
+TAG=${1:-ab}; shift
+for W in "$@"; do
+  for lib in exp/lib_*.so; do
+    n=$(basename $lib .so)
+    HDR_DEBUG_RT=1 HDR_LPA_LIB=$lib timeout 300 python bench.py --steps 10 --warmup 3 --workload $W --no-cpu-baseline --no-api-e2e > gpurun_out/${TAG}_${n}_$W.json 2>gpurun_out/${TAG}_${n}_$W.err
+    echo "$n $W: $(python scripts/bench_summary.py gpurun_out/${TAG}_${n}_$W.json | cut -c1-150) | $(grep -m1 row-tap gpurun_out/${TAG}_${n}_$W.err)"
+  done
+done

@@ -430,3 +430,28 @@ def test_cosited_rig_outside_the_merged_mode(cuda, order, J, up):
     out = (2 * W, 2 * H) if up else (W, H)
     got, ref, _ = _run(frames, list(rig.sensors), rig.calibrations(), out, p, ref_size=(W, H))
     _check(got, ref)
+
+
+@pytest.mark.parametrize("n_sensors,scale,J", [(8, 2.0, 4), (4, 30.0, 1), (3, 45.0, 1)])
+def test_windows_too_large_to_stage(cuda, n_sensors, scale, J):
+    """Rigs whose staged tiles exceed shared memory (many sensors x large
+    windows / ICI scales) run every (pixel, channel) through the exact path
+    instead of failing (hdr_lpa.cu setup_staging -> all_items)."""
+    import dataclasses
+
+    W, H = 48, 40
+    gt = sim.hdr_chart(W, H)
+    base = sim.baseline_rig("misaligned", W, H, seed=41, n_sensors=4)
+    sensors, noise = [], []
+    for i in range(n_sensors):
+        src = base.sensors[i % 4]
+        T = np.array(src.transform, dtype=float)
+        T[:, 2] += (0.11 * (i // 4), -0.05 * (i // 4))
+        sensors.append(dataclasses.replace(src, sensor_id=i, transform=T,
+                                           exposure_scaling=2.0 ** -(i % 6)))
+        noise.append(base.noise[i % 4])
+    rig = sim.RigSpec(sensors=sensors, noise=noise, sensor_sizes=[(W, H)] * n_sensors, seed=4)
+    frames = sim.simulate_rig(gt, rig)
+    p = hl.ReconstructionParams(order=1, scale=scale, ici_scales=J)
+    got, ref, _ = _run(frames, sensors, rig.calibrations(), (W, H), p)
+    _check(got, ref)

@@ -59,9 +59,10 @@ def test_struct_layouts_match_the_header(tmp_path):
 
 def test_abi_version_and_status_strings():
     L = N.lib()
-    assert L.hdr_lpa_abi_version() == 4
+    assert L.hdr_lpa_abi_version() == 5
     for code, text in ((0, "ok"), (1, "invalid argument"), (2, "invalid sensor configuration"),
-                       (3, "dimension mismatch"), (4, "workspace too small"), (5, "CUDA error")):
+                       (3, "dimension mismatch"), (4, "workspace too small"), (5, "CUDA error"),
+                       (6, "kernel fault")):
         assert L.hdr_lpa_status_string(code).decode() == text
 
 
