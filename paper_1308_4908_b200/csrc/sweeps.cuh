@@ -95,7 +95,10 @@ struct GlobalSweep {
 template <class Body>
 struct PerSample {
     Body &body;
-    __device__ __forceinline__ void begin_row(double, double) {}
+    __device__ __forceinline__ void begin_row(double dy, double dyy) {
+        dy_ = dy;
+        dyy_ = dyy;
+    }
     __device__ __forceinline__ void end_row(double, double) {}
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
                                            double dxx, double dyy, float d2f, bool = true) {
@@ -104,6 +107,11 @@ struct PerSample {
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    double dy_, dyy_;  // the row's offset (row taps pass it to begin_row)
+    __device__ __forceinline__ void sample_rt(float2 e, double dx, double dxx, float d2f,
+                                              bool = true) {
+        body(e.y > 0.f, (double)e.x, e.y, dx, dy_, dxx, dyy_, d2f);
     }
 };
 
@@ -173,8 +181,7 @@ struct TileSweep {
             for (; t < te; ++t) {
                 const RowTap T = *t;
                 const float2 e = *(const float2 *)(vb + rt_off(T.off));
-                pol.sample(e.y > 0.f, (double)e.x, e.y, T.dx, dy, T.dx * T.dx, dyy, T.d2f,
-                           rt_kmin(T.off) <= kin);
+                pol.sample_rt(e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
             }
             pol.end_row(dy, dyy);
         }
@@ -295,18 +302,19 @@ struct TileSweep {
                         const int ly = y - oy;
                         const double t1y = ty1[ly], t4y = ty4[ly];
                         const int rb = ph * plane + (ly >> 1) * pw - (ox >> 1);
+                        // straight-line body (the chord pre-test leaves few candidates
+                        // outside the disk): masked and outside samples take weight 0
                         for (int x = x0; x <= x1; x += 2) {
                             const int k = rb + (x >> 1);
                             const float2 e = vi[k];
-                            if (!(e.y > 0.f)) continue;
                             const int lx = x - ox;
                             const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
                             const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
                             const double dx = __dsub_rn(X, qx()), dy = __dsub_rn(Y, qy());
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
-                            const double d2 = __dadd_rn(dxx, dyy);
-                            if (d2 > r2) continue;
-                            pol.general(true, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2,
+                            const double d2 = __dadd_rn(dxx, dyy);  // _kernels.py:160-162
+                            const bool ok = (e.y > 0.f) && !(d2 > r2);
+                            pol.general(ok, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2,
                                         d2 <= r2in);
                         }
                     }
@@ -358,6 +366,29 @@ struct RowMoments {
 #pragma unroll
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
         cnt += ok ? 1 : 0;
+    }
+    // row tap (RT): every tap lies inside the disk and a masked sample is
+    // staged as (0, 0), so no select is needed (its weight and value are 0)
+    __device__ __forceinline__ void sample_rt(float2 e, double dx, double dxx, float d2f,
+                                              bool = true) {
+        const float w32 = ex2_approx(-hl * d2f) * e.y;
+        const double w = (double)w32, y = (double)e.x;
+        acc.sabs = fmaf(w32, fabsf(e.x), acc.sabs);
+        double px[5];
+        px[1] = dx;
+        px[2] = dxx;
+        if (ORDER >= 2) {
+            px[3] = dx * dxx;
+            px[4] = dxx * dxx;
+        }
+        S[0] += w;
+#pragma unroll
+        for (int n = 1; n <= 2 * ORDER; ++n) S[n] = fma(w, px[n], S[n]);
+        const double wy = w * y;
+        T[0] += wy;
+#pragma unroll
+        for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
+        cnt += e.y > 0.f ? 1 : 0;
     }
     // co-sited merged sample: w = W sum 1/den, wy = W sum f_hat/den (fp32),
     // the bound's sum w |y| from W sum |f_hat|/den, count = the sensors' samples
@@ -459,6 +490,18 @@ struct RowVariance {
             T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
         }
     }
+    __device__ __forceinline__ void sample_rt(float2 e, double dx, double, float d2f,
+                                              bool = true) {
+        const float W = ex2_approx(-hl * d2f);
+        // masked samples: 1/den = 0 (variance weights W^2/den vanish; sigma
+        // weights W^2 need the mask)
+        const float t32 = sig ? (e.y > 0.f ? W * W : 0.f) : W * W * e.y;
+        double pg = c0;
+        if (ORDER == 1) pg = fma(dx, c1, c0);
+        if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
+        v = fma((double)t32, pg * pg, v);
+        T = fmaf(W * e.y, fabsf((float)pg) * fabsf(e.x), T);
+    }
     __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
@@ -466,10 +509,9 @@ struct RowVariance {
         double pg = g[0];
         if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
         if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
-        if (ok) {
-            v = fma(t, pg * pg, v);
-            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
-        }
+        // W = 0 when !ok: both sums take zero contributions (no branch)
+        v = fma(t, pg * pg, v);
+        T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
     }
 };
 
@@ -493,10 +535,18 @@ struct FusedVarMom {
         M.sample(ok, v, iv, dx, dy, dxx, dyy, d2f);
         if (inner) V.sample(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
+    // rotated sensors: inner differs between the lanes of a warp, so both
+    // halves run unconditionally (the variance with weight 0 outside r_kin)
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool inner) {
         M.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
-        if (inner) V.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
+        V.general(ok && inner, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    // row taps: inner is uniform across the warp (class-uniform tap lists)
+    __device__ __forceinline__ void sample_rt(float2 e, double dx, double dxx, float d2f,
+                                              bool inner) {
+        M.sample_rt(e, dx, dxx, d2f);
+        if (inner) V.sample_rt(e, dx, dxx, d2f);
     }
 };
 

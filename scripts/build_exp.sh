@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 while [ $# -ge 2 ]; do
   n=$1; f=$2; shift 2
-  python - "$n" "$f" <<'PY' > exp/ptxas_$1.log 2>&1 || echo "build $1 failed"
+  python - "$n" "$f" <<'PY' > exp/ptxas_$n.log 2>&1 || echo "build $n failed"
 import sys
 from pathlib import Path
 sys.path.insert(0, ".")
