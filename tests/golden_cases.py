@@ -25,10 +25,21 @@ def calpa_names():
     return sorted(manifest().get("calpa_cases", {}))
 
 
+def ici_manifest():
+    return json.loads((GOLDEN / "ici_golden.json").read_text())
+
+
+def ici_names():
+    return sorted(ici_manifest()["cases"])
+
+
 def load(name):
     """(frames, configs, cals, out_size, params, ref_size, case_json, arrays)."""
     m = manifest()
-    case = m["cases"][name] if name in m["cases"] else m["calpa_cases"][name]
+    if name.startswith("ici_"):
+        case = ici_manifest()["cases"][name]
+    else:
+        case = m["cases"][name] if name in m["cases"] else m["calpa_cases"][name]
     arrays = dict(np.load(GOLDEN / f"{name}.npz"))
     frames, configs, cals = [], [], []
     for k, s in enumerate(case["sensors"]):
@@ -55,6 +66,9 @@ def load(name):
                                      per_channel_scale=p["per_channel_scale"],
                                      max_support_radius=p["max_support_radius"],
                                      cond_threshold=p["cond_threshold"],
-                                     weight_mode=p["weight_mode"])
+                                     weight_mode=p["weight_mode"],
+                                     **({"ici_scales": case["ici"]["scales"],
+                                         "ici_ratio": case["ici"]["ratio"],
+                                         "ici_gamma": case["ici"]["gamma"]} if "ici" in case else {}))
     ref_size = tuple(case["ref_size"]) if case["ref_size"] else None
     return frames, configs, cals, tuple(case["out_size"]), params, ref_size, case, arrays

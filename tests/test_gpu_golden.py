@@ -32,3 +32,19 @@ def test_gpu_matches_reference_golden(cuda, name):
     g = out["grad"].cpu().numpy()
     sg = compare.summary(g[:, 0], ref["gx"], floor=1e3)
     assert sg["nan_map_equal"] and sg["p99"] < 1e-3
+
+
+@pytest.mark.parametrize("name", __import__("golden_cases").ici_names())
+def test_gpu_ici_matches_reference_fits(cuda, name):
+    """ICI on the GPU against the goldens built from the reference's own
+    per-scale gather + wls_fit (oracle/gen_ici_golden.py): scale indices
+    bit-exact, radiance within 1e-4 on every pixel."""
+    frames, cfgs, cals, out_size, params, ref_size, case, arrays = load(name)
+    raw = hl.frames_to_samples(frames, cfgs, cals)
+    out = raw.device().reconstruct(out_size, params, want_scale_idx=True)
+    sidx = out["scale_idx"].cpu().numpy()
+    mism = int((sidx != arrays["scale_idx"]).sum())
+    assert mism == 0, f"{mism} scale-index mismatches"
+    s = compare.summary(out["rgb"].cpu().numpy(), arrays["rgb"])
+    print(name, s)
+    assert s["nan_map_equal"] and s["frac_over"] == 0 and s["max"] <= 1e-4, s
