@@ -41,3 +41,23 @@ def summary(gpu, ref, floor=FLOOR):
         "p99": float(np.quantile(e, 0.99)),
         "p999": float(np.quantile(e, 0.999)),
     }
+
+
+def grad_summary(gpu, ref, val_ref, floor=FLOOR):
+    """Gradient parity: |gpu - ref| <= 1e-4 * max(|ref|, |value|, FLOOR) (per
+    pixel; gradients in e/s per pixel, scaled against the pixel's own radiance
+    where the gradient is small -- a flat region's gradient has no relative
+    precision of its own).  Same dict as summary()."""
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    v = np.abs(np.asarray(val_ref, dtype=np.float64))
+    nan_eq = bool(np.array_equal(np.isnan(gpu), np.isnan(ref)))
+    both = np.isfinite(gpu) & np.isfinite(ref) & np.isfinite(v)
+    den = np.maximum(np.maximum(np.abs(ref), v), floor)
+    e = (np.abs(gpu - ref) / den)[both]
+    if e.size == 0:
+        return {"nan_map_equal": nan_eq, "n": 0, "frac_over": 0.0, "max": 0.0,
+                "p99": 0.0, "p999": 0.0}
+    return {"nan_map_equal": nan_eq, "n": int(e.size), "frac_over": float((e > REL_TOL).mean()),
+            "max": float(e.max()), "p99": float(np.quantile(e, 0.99)),
+            "p999": float(np.quantile(e, 0.999))}

@@ -30,8 +30,13 @@ def test_gpu_matches_reference_golden(cuda, name):
         s2 = compare.summary(rgb, arrays["rgb"])
         assert s2["nan_map_equal"] and s2["frac_over"] == 0 and s2["max"] <= 1e-4
     g = out["grad"].cpu().numpy()
-    sg = compare.summary(g[:, 0], ref["gx"], floor=1e3)
-    assert sg["nan_map_equal"] and sg["p99"] < 1e-3
+    for j, key in enumerate(("gx", "gy")):  # every pixel, 1e-4 (compare.grad_summary)
+        sg = compare.grad_summary(g[:, j], ref[key], ref["val"])
+        assert sg["nan_map_equal"] and sg["frac_over"] == 0 and sg["max"] <= 1e-4, sg
+    if "grad" in arrays:  # the reference's own float64 gradients
+        for j in range(2):
+            sg = compare.grad_summary(g[:, j], arrays["grad"][:, j], ref["val"])
+            assert sg["nan_map_equal"] and sg["frac_over"] == 0 and sg["max"] <= 1e-4, sg
 
 
 @pytest.mark.parametrize("name", __import__("golden_cases").ici_names())
