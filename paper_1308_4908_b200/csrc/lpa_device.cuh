@@ -509,35 +509,40 @@ __device__ __forceinline__ void chol_finish(const double *A, const double *b, co
     fit.c0 = c[0];
     fit.c1 = (P >= 3) ? c[1] : 0.0;
     fit.c2 = (P >= 3) ? c[2] : 0.0;
-    // Linv, lower triangular, packed
-    double Li[P * (P + 1) / 2];
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-        Li[i * (i + 1) / 2 + i] = inv[i];
-#pragma unroll
-        for (int j = 0; j < i; ++j) {
-            double s = 0.0;
-#pragma unroll
-            for (int k = j; k < i; ++k) s += L[i * (i + 1) / 2 + k] * Li[k * (k + 1) / 2 + j];
-            Li[i * (i + 1) / 2 + j] = -s * inv[i];
-        }
-    }
+    // L^{-1} one column at a time (x = L^{-1} e_j, x_i = 0 for i < j):
+    // (A^{-1})_jj = |x|^2, and column 0 gives g = A^{-1} e1 = L^{-T} x by
+    // back substitution -- at most one column live, not the whole inverse
     double trA = 0.0, mA = 0.0, trI = 0.0, mI = 0.0;
+    double x0[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
         const double ajj = A[uidx<P>(j, j)];
         trA += ajj;
         mA = fmax(mA, ajj);
-        double dj = 0.0, gj = 0.0;
+        double x[P];
+        x[j] = inv[j];
+        double dj = x[j] * x[j];
 #pragma unroll
-        for (int i = j; i < P; ++i) {
-            const double lij = Li[i * (i + 1) / 2 + j];
-            dj += lij * lij;
-            gj += lij * Li[i * (i + 1) / 2 + 0];
+        for (int i = j + 1; i < P; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = j; k < i; ++k) s += L[i * (i + 1) / 2 + k] * x[k];
+            x[i] = -s * inv[i];
+            dj += x[i] * x[i];
+        }
+        if (j == 0) {
+#pragma unroll
+            for (int i = 0; i < P; ++i) x0[i] = x[i];
         }
         trI += dj;
         mI = fmax(mI, dj);
-        fit.g[j] = gj;
+    }
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+        double s = x0[i];
+#pragma unroll
+        for (int k = i + 1; k < P; ++k) s -= L[k * (k + 1) / 2 + i] * fit.g[k];
+        fit.g[i] = s * inv[i];
     }
     cu = trA * trI;
     cl = mA * mI;

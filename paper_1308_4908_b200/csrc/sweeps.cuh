@@ -109,6 +109,11 @@ struct PerSample {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
     double dy_, dyy_;  // the row's offset (row taps pass it to begin_row)
+    __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx, double dxx,
+                                             float d2f, bool inner = true) {
+        begin_row(dy, dyy);
+        sample_rt(e, dx, dxx, d2f, inner);
+    }
     __device__ __forceinline__ void sample_rt(float2 e, double dx, double dxx, float d2f,
                                               bool = true) {
         body(e.y > 0.f, (double)e.x, e.y, dx, dy_, dxx, dyy_, d2f);
@@ -170,15 +175,19 @@ struct TileSweep {
         for (int ri = rr.x; ri < rr.x + rr.y; ++ri) {
             const double dy = rdy[ri], dyy = dy * dy;
             const uint32_t fn = rfn[ri];
-            pol.begin_row(dy, dyy);
             const RowTap *t = taps + (fn & ((1u << RT_ROW_N_SHIFT) - 1));
             const RowTap *te = t + (fn >> RT_ROW_N_SHIFT);
+            {  // every row run holds >= 1 tap: the first one opens the row's sums
+                const RowTap T = *t;
+                const float2 e = *(const float2 *)(vb + rt_off(T.off));
+                pol.first_rt(dy, dyy, e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
+            }
 #ifndef HDR_RT_UNROLL
 #define HDR_RT_UNROLL 1
 #endif
             constexpr int kRtUnroll = HDR_RT_UNROLL;
 #pragma unroll kRtUnroll
-            for (; t < te; ++t) {
+            for (++t; t < te; ++t) {
                 const RowTap T = *t;
                 const float2 e = *(const float2 *)(vb + rt_off(T.off));
                 pol.sample_rt(e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
@@ -390,6 +399,28 @@ struct RowMoments {
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
         cnt += e.y > 0.f ? 1 : 0;
     }
+    // the first tap of a row run: opens the row sums (no zeroing)
+    __device__ __forceinline__ void first_rt(double, double, float2 e, double dx, double dxx,
+                                             float d2f, bool = true) {
+        const float w32 = ex2_approx(-hl * d2f) * e.y;
+        const double w = (double)w32, y = (double)e.x;
+        acc.sabs = fmaf(w32, fabsf(e.x), acc.sabs);
+        double px[5];
+        px[1] = dx;
+        px[2] = dxx;
+        if (ORDER >= 2) {
+            px[3] = dx * dxx;
+            px[4] = dxx * dxx;
+        }
+        S[0] = w;
+#pragma unroll
+        for (int n = 1; n <= 2 * ORDER; ++n) S[n] = w * px[n];
+        const double wy = w * y;
+        T[0] = wy;
+#pragma unroll
+        for (int n = 1; n <= ORDER; ++n) T[n] = wy * px[n];
+        cnt = e.y > 0.f ? 1 : 0;
+    }
     // co-sited merged sample: w = W sum 1/den, wy = W sum f_hat/den (fp32),
     // the bound's sum w |y| from W sum |f_hat|/den, count = the sensors' samples
     __device__ __forceinline__ void sample4(bool ok, float4 e, double dx, double dxx, float W) {
@@ -490,6 +521,11 @@ struct RowVariance {
             T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
         }
     }
+    __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx,
+                                             double dxx, float d2f, bool = true) {
+        begin_row(dy, dyy);
+        sample_rt(e, dx, dxx, d2f);
+    }
     __device__ __forceinline__ void sample_rt(float2 e, double dx, double, float d2f,
                                               bool = true) {
         const float W = ex2_approx(-hl * d2f);
@@ -541,6 +577,12 @@ struct FusedVarMom {
                                             double dxx, double dyy, float d2f, bool inner) {
         M.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
         V.general(ok && inner, v, iv, dx, dy, dxx, dyy, d2f);
+    }
+    __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx,
+                                             double dxx, float d2f, bool inner) {
+        V.begin_row(dy, dyy);
+        M.first_rt(dy, dyy, e, dx, dxx, d2f);
+        if (inner) V.sample_rt(e, dx, dxx, d2f);
     }
     // row taps: inner is uniform across the warp (class-uniform tap lists)
     __device__ __forceinline__ void sample_rt(float2 e, double dx, double dxx, float d2f,
