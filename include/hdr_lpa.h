@@ -56,6 +56,7 @@ extern "C" {
 /* Fault bits a kernel raises in the workspace header instead of trapping
  * (read back by hdr_lpa_workspace_status; cleared by every reconstruct call) */
 #define HDR_FAULT_MBAR_TIMEOUT 1u  /* a staging barrier wait exceeded its bound */
+#define HDR_FAULT_BOUNDS 2u        /* debug builds: a staged read out of range   */
 
 /* Weight modes (ReconstructionParams.weight_mode, lpa.py:54-61) */
 #define HDR_WEIGHT_VARIANCE 0

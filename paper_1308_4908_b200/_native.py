@@ -28,6 +28,7 @@ MAX_SCALES = 8
 (HDR_OK, HDR_ERR_ARG, HDR_ERR_CONFIG, HDR_ERR_SHAPE, HDR_ERR_WORKSPACE, HDR_ERR_CUDA,
  HDR_ERR_FAULT) = range(7)
 HDR_FAULT_MBAR_TIMEOUT = 1
+HDR_FAULT_BOUNDS = 2
 HDR_WEIGHT_VARIANCE, HDR_WEIGHT_SIGMA = 0, 1
 HDR_OUTCOME_NAN = 0xFF
 HDR_FLAG_FAST_ONLY = 1
@@ -146,7 +147,8 @@ def compile_library(out: Path, extra_flags=(), verbose_ptxas: bool = False) -> P
                 print(err, end="")
         if errs:
             raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
-        subprocess.run(["nvcc", "-shared", "-o", str(out), *objs, "-lcuda"], check=True)
+        subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
+                        str(out), *objs, "-lcuda"], check=True)
     return out
 
 

@@ -11,6 +11,21 @@
 
 namespace hdrlpa {
 
+// Debug builds (-DHDR_DEBUG_BOUNDS=1, scripts/gpu_bounds.sh): every staged
+// shared-memory read of the tile sweeps is range-checked; a violation raises
+// HDR_FAULT_BOUNDS in the workspace header (hdr_lpa_workspace_status) instead
+// of reading out of range.  compute-sanitizer is not available on the
+// measurement pool, so this is the memory-safety check the tests run.
+#ifndef HDR_DEBUG_BOUNDS
+#define HDR_DEBUG_BOUNDS 0
+#endif
+#if HDR_DEBUG_BOUNDS
+#define HDR_BOUNDS(P, cond) \
+    do { if (!(cond)) atomicOr((P).fault, (uint32_t)HDR_FAULT_BOUNDS); } while (0)
+#else
+#define HDR_BOUNDS(P, cond) do { } while (0)
+#endif
+
 constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per tile pixel
 
 // workspace layout: [header: work counter][pre-computed taps][work items]

@@ -179,6 +179,8 @@ struct TileSweep {
             const RowTap *te = t + (fn >> RT_ROW_N_SHIFT);
             {  // every row run holds >= 1 tap: the first one opens the row's sums
                 const RowTap T = *t;
+                HDR_BOUNDS(P, vb + rt_off(T.off) >= sm + S.off_vi &&
+                                  vb + rt_off(T.off) + 8 <= sm + S.off_vi + S.rw * S.rh * 8);
                 const float2 e = *(const float2 *)(vb + rt_off(T.off));
                 pol.first_rt(dy, dyy, e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
             }
@@ -189,6 +191,8 @@ struct TileSweep {
 #pragma unroll kRtUnroll
             for (++t; t < te; ++t) {
                 const RowTap T = *t;
+                HDR_BOUNDS(P, vb + rt_off(T.off) >= sm + S.off_vi &&
+                                  vb + rt_off(T.off) + 8 <= sm + S.off_vi + S.rw * S.rh * 8);
                 const float2 e = *(const float2 *)(vb + rt_off(T.off));
                 pol.sample_rt(e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
             }
@@ -234,6 +238,7 @@ struct TileSweep {
 #pragma unroll
                         for (int i = 0; i < MAXC; ++i) {
                             if (c0 + i < nc) {
+                                HDR_BOUNDS(P, xs + 2 * i - ox >= 0 && xs + 2 * i - ox < S.rw);
                                 cdx[i] = __dsub_rn(tx0[xs + 2 * i - ox], qx());  // X(x) - qx
                                 cdxx[i] = __dmul_rn(cdx[i], cdx[i]);
                             } else {
@@ -245,10 +250,14 @@ struct TileSweep {
                         const int colbase = ph * plane + ((xs - ox) >> 1);
                         for (int y = ys; y <= yhi; y += 2) {
                             const int ly = y - oy;
+                            HDR_BOUNDS(P, ly >= 0 && ly < S.rh);
                             const double dy = __dsub_rn(ty4[ly], qy());  // Y(y) - qy
                             const double dyy = __dmul_rn(dy, dy);
                             if (dyy > r2) continue;
                             const int rb = colbase + (ly >> 1) * pw;
+                            // the row's real columns (the padded tail reads the take() slack)
+                            HDR_BOUNDS(P, rb >= 0 &&
+                                              rb + (nc - c0 < MAXC ? nc - c0 : MAXC) <= 4 * plane);
                             pol.begin_row(dy, dyy);
                             // orders 0-1: branch-free over the row (candidates outside the
                             // disk or without a sample contribute with weight 0); order 2
@@ -315,8 +324,10 @@ struct TileSweep {
                         // outside the disk): masked and outside samples take weight 0
                         for (int x = x0; x <= x1; x += 2) {
                             const int k = rb + (x >> 1);
-                            const float2 e = vi[k];
                             const int lx = x - ox;
+                            HDR_BOUNDS(P, k >= 0 && k < 4 * plane && lx >= 0 && lx < S.rw &&
+                                              ly >= 0 && ly < S.rh);
+                            const float2 e = vi[k];
                             const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
                             const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
                             const double dx = __dsub_rn(X, qx()), dy = __dsub_rn(Y, qy());
