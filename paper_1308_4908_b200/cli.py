@@ -114,22 +114,49 @@ def main():
 
 
 @main.command("reconstruct")
-@click.option("--rig", "rig_config", type=click.Path(path_type=Path), required=True)
-@click.option("--out", type=click.Path(path_type=Path), required=True)
-@click.argument("frames", nargs=-1, type=click.Path(path_type=Path))
+@click.argument("args", nargs=-1, type=click.Path(path_type=Path))
+@click.option("--rig", "rig_opt", type=click.Path(path_type=Path), default=None,
+              help="rig JSON (alternative to the positional RIG_CONFIG)")
+@click.option("--out", "-o", type=click.Path(path_type=Path), required=True, help="Output PFM.")
 @_with(recon_options)
+@click.option("--calpa", is_flag=True, help="Structure-adaptive second pass (steering.py).")
+@click.option("--alpha", type=float, default=None, help="Structure sensitivity (CALPA).")
+@click.option("--grad-window", type=int, default=None, help="Gradient analysis window (odd).")
+@click.option("--threads", type=int, default=None,
+              help="accepted for compatibility (host threads do not drive the GPU path)")
+@click.option("--preview", type=click.Path(path_type=Path), default=None,
+              help="Also write an 8-bit gamma preview PNG.")
 @_exit_codes
-def cmd_reconstruct(rig_config, out, frames, order, scale, max_radius, cond_threshold,
-                    ici_scales, ici_gamma, width, height):
-    """Reconstruct an HDR PFM from per-sensor raw PGM frames."""
+def cmd_reconstruct(args, rig_opt, out, order, scale, max_radius, cond_threshold, ici_scales,
+                    ici_gamma, width, height, calpa, alpha, grad_window, threads, preview):
+    """reconstruct RIG_CONFIG FRAMES... -o OUT.pfm (reference cli.py:156-238):
+    an HDR PFM from per-sensor raw PGM frames."""
+    from .steering import AdaptiveParams, calpa_reconstruct
+
+    args = list(args)
+    if rig_opt is None:
+        if not args:
+            raise click.UsageError("missing RIG_CONFIG")
+        rig_config, frames = args[0], args[1:]
+    else:
+        rig_config, frames = rig_opt, args
+    if not frames:
+        raise click.UsageError("missing FRAMES")
     rig = load_rig(rig_config)
     raws, cals = _load_frames(rig, list(frames))
     params = _params(rig, order, scale, max_radius, cond_threshold, ici_scales, ici_gamma)
+    defaults = dict(getattr(rig, "reconstruction", {}) or {})
+    alpha = alpha if alpha is not None else float(defaults.get("alpha", 0.005))
+    grad_window = grad_window if grad_window is not None else int(defaults.get("grad_window", 9))
     ref_size = (raws[0].width, raws[0].height)            # reference cli.py:199
     out_size = (width or ref_size[0], height or ref_size[1])
     t0 = time.perf_counter()
     samples = frames_to_samples(raws, rig.configs, cals)
-    hdr = reconstruct_frame(samples, out_size, params, ref_size=ref_size)
+    if calpa:
+        adaptive = AdaptiveParams(alpha=alpha, gradient_window=grad_window, base=params)
+        hdr = calpa_reconstruct(samples, out_size, adaptive, ref_size=ref_size)
+    else:
+        hdr = reconstruct_frame(samples, out_size, params, ref_size=ref_size)
     elapsed = time.perf_counter() - t0
     out.parent.mkdir(parents=True, exist_ok=True)
     write_pfm(hdr, out)
@@ -138,14 +165,35 @@ def cmd_reconstruct(rig_config, out, frames, order, scale, max_radius, cond_thre
         "frames": [{"path": str(p), "sha256": _sha256(p)} for p in frames],
         "parameters": {"order": params.order, "scale": params.scale,
                        "max_radius": params.max_support_radius,
-                       "cond_threshold": params.cond_threshold, "ici_scales": params.ici_scales,
-                       "ici_ratio": params.ici_ratio, "ici_gamma": params.ici_gamma,
-                       "width": out_size[0], "height": out_size[1]},
-        "device": _device_name(), "seconds": elapsed,
+                       "cond_threshold": params.cond_threshold, "calpa": bool(calpa),
+                       "alpha": alpha, "grad_window": grad_window,
+                       "ici_scales": params.ici_scales, "ici_ratio": params.ici_ratio,
+                       "ici_gamma": params.ici_gamma, "width": out_size[0],
+                       "height": out_size[1]},
+        "threads": threads, "device": _device_name(), "seconds": elapsed,
         "nan_fraction": float(np.isnan(hdr.data).mean()),
     }
     Path(str(out) + ".manifest.json").write_text(json.dumps(manifest, indent=2) + "\n")
     click.echo(f"wrote {out} ({elapsed:.3f} s)")
+    if preview is not None:
+        _write_preview(hdr, rig, preview)
+        click.echo(f"wrote {preview}")
+
+
+def _write_preview(hdr, rig, path: Path) -> None:
+    """Gamma-2.2 8-bit preview (reference cli.py:241-255): NaNs take the least
+    sensitive sensor's saturation radiance, scaled by the 99th percentile."""
+    from PIL import Image
+
+    data = hdr.data.astype(np.float64).copy()
+    sat = [(c.saturation_level - c.black_level) / (c.gain * c.exposure_time * c.exposure_scaling)
+           for c in rig.configs]
+    data[~np.isfinite(data)] = max(sat)
+    finite = data[np.isfinite(data)]
+    top = np.percentile(finite, 99.0) if finite.size else 1.0
+    norm = np.clip(data / max(top, 1e-30), 0.0, 1.0) ** (1.0 / 2.2)
+    Path(path).parent.mkdir(parents=True, exist_ok=True)
+    Image.fromarray((norm * 255.0 + 0.5).astype(np.uint8)).save(path)
 
 
 @main.command("video")
