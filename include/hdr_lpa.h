@@ -240,6 +240,43 @@ int hdr_radiance_planes(const HdrSensor *sensor, int weight_mode, float *value, 
  */
 int hdr_sample_planes(const HdrSensor *sensor, double *value, double *sigma, void *stream);
 
+/*
+ * RadianceSamples columns from the sample planes, on the device, order
+ * preserving (frames_to_samples, radiometry.py:303-349; replaces the
+ * reference's per-frame numpy compaction): hdr_sample_count counts the kept
+ * pixels (sigma > 0) of one sensor and leaves per-row offsets in `workspace`
+ * (hdr_sample_count_workspace_bytes(height)); synchronous.  hdr_compact_samples
+ * then writes them, raster order, at `offset` of the columns: positions
+ * (n, 2) f64 = apply_transform (radiometry.py:84, no contraction), channels
+ * u8 (bayer.py:54-59), values / sigmas f64, sensor_ids i32.  (ABI v5)
+ */
+int hdr_sample_count_workspace_bytes(int height, size_t *bytes);
+int hdr_sample_count(const HdrSensor *sensor, const double *sigma, long long *count,
+                     void *workspace, void *stream);
+int hdr_compact_samples(const HdrSensor *sensor, int sensor_id, const double *value,
+                        const double *sigma, long long offset, double *positions,
+                        uint8_t *channels, double *values, double *sigmas, int *sensor_ids,
+                        const void *workspace, void *stream);
+
+/*
+ * SampleIndex on the device (radiometry.py:208-242), a stable counting sort
+ * by unit cell -- no library sort: hdr_sample_index_bbox returns the channel's
+ * sample count and cell grid (x0, y0 = floor of the minima, nx, ny; one cell
+ * for an empty channel; synchronous); hdr_sample_index_build fills
+ * cell_start[nx*ny+1] (int64 CSR) and packed[count][4] = [x, y, value,
+ * sigma^2] in cell order, ties in original sample order, exactly as
+ * np.argsort(cell, kind="stable").  Workspace: hdr_sample_index_workspace_bytes
+ * (its first 64 bytes also serve hdr_sample_index_bbox).  (ABI v5)
+ */
+int hdr_sample_index_workspace_bytes(long long n, long long ncells, size_t *bytes);
+int hdr_sample_index_bbox(const double *positions, const uint8_t *channels, long long n,
+                          int channel, long long *count, int *x0, int *y0, int *nx, int *ny,
+                          void *workspace, void *stream);
+int hdr_sample_index_build(const double *positions, const uint8_t *channels, const double *values,
+                           const double *sigmas, long long n, int channel, int x0, int y0, int nx,
+                           int ny, long long *cell_start, double *packed, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* Number of (pixel, channel) items the last call on this workspace routed
  * through the exact slow path (device value; reads it synchronously). */
 int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream);

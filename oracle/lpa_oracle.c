@@ -68,6 +68,7 @@ typedef struct {
     const double *nonuni;
     double bias_s, readvar_s, nonuni_s;
     const uint8_t *defective;    /* nullable, 1 = discard (radiometry.py:316-317) */
+    int sensor_id;               /* SensorConfig.sensor_id (radiometry.py:335) */
 } OSensor;
 
 typedef struct {
@@ -131,7 +132,7 @@ int64_t oracle_frames_to_samples(const OSensor *sensors, int n_sensors,
             chan[k] = (uint8_t)c;
             val[k] = v;
             sig[k] = sg;
-            sid[k] = si;
+            sid[k] = sensors[si].sensor_id;  /* radiometry.py:335 */
             ++k;
         }
     }

@@ -64,6 +64,7 @@ class OSensor(ctypes.Structure):
         ("readvar_s", ctypes.c_double),
         ("nonuni_s", ctypes.c_double),
         ("defective", ctypes.c_void_p),
+        ("sensor_id", ctypes.c_int),
     ]
 
 
@@ -174,6 +175,7 @@ def make_sensors(frames, configs, cals):
         s.width, s.height = w, h
         s.raw = raw.ctypes.data
         s.saturation_level = int(cfg.saturation_level)
+        s.sensor_id = int(getattr(cfg, "sensor_id", k))
         s.exposure_time = float(cfg.exposure_time)
         s.gain = float(cfg.gain)
         s.exposure_scaling = float(cfg.exposure_scaling)

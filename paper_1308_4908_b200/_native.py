@@ -45,6 +45,12 @@ EXPORTED = (
     "hdr_sample_planes",
     "hdr_lpa_slow_items",
     "hdr_lpa_workspace_status",
+    "hdr_sample_count_workspace_bytes",
+    "hdr_sample_count",
+    "hdr_compact_samples",
+    "hdr_sample_index_workspace_bytes",
+    "hdr_sample_index_bbox",
+    "hdr_sample_index_build",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
     "hdr_lpa_last_error",
@@ -209,6 +215,20 @@ def lib():
                                              ctypes.c_void_p]
             L.hdr_lpa_workspace_status.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
                                                    ctypes.POINTER(ctypes.c_uint32), ctypes.c_void_p]
+            i64, vp, P64 = ctypes.c_longlong, ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)
+            L.hdr_sample_count_workspace_bytes.argtypes = [ctypes.c_int,
+                                                           ctypes.POINTER(ctypes.c_size_t)]
+            L.hdr_sample_count.argtypes = [ctypes.POINTER(HdrSensor), vp, P64, vp, vp]
+            L.hdr_compact_samples.argtypes = [ctypes.POINTER(HdrSensor), ctypes.c_int, vp, vp, i64,
+                                              vp, vp, vp, vp, vp, vp, vp]
+            L.hdr_sample_index_workspace_bytes.argtypes = [i64, i64,
+                                                           ctypes.POINTER(ctypes.c_size_t)]
+            PI = ctypes.POINTER(ctypes.c_int)
+            L.hdr_sample_index_bbox.argtypes = [vp, vp, i64, ctypes.c_int, P64, PI, PI, PI, PI, vp,
+                                                vp]
+            L.hdr_sample_index_build.argtypes = [vp, vp, vp, vp, i64, ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp,
+                                                 vp, ctypes.c_size_t, vp]
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
             L.hdr_lpa_status_string.restype = ctypes.c_char_p
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]

@@ -31,6 +31,7 @@
 #include "frame_kernels.cuh"
 #include "calpa.cuh"
 #include "samples.cuh"
+#include "sample_index.cuh"
 
 namespace hdrlpa {
 
@@ -925,6 +926,164 @@ int hdr_sample_planes(const HdrSensor *sensor, double *value, double *sigma, voi
     COUNT_LAUNCH();
     sample_planes_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d, value, sigma);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+}
+
+// exclusive scan of n int64 in place-capable buffers, scratch >= scan_scratch(n)
+static size_t scan_scratch(long long n) {
+    size_t total = 0;
+    while (n > SCAN_BLOCK) {
+        n = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+        total += 2 * (size_t)n;
+    }
+    return total;
+}
+static int device_scan(const long long *in, long long *out, long long n, long long *scratch,
+                       cudaStream_t st) {
+    const long long nb = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    COUNT_LAUNCH();
+    scan_block_kernel<<<(unsigned)nb, SCAN_BLOCK, 0, st>>>(in, out, n, nb > 1 ? scratch : nullptr);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("scan_block_kernel");
+    if (nb > 1) {
+        long long *sums = scratch, *offs = scratch + nb;
+        const int rc = device_scan(sums, offs, nb, scratch + 2 * nb, st);
+        if (rc != HDR_OK) return rc;
+        COUNT_LAUNCH();
+        scan_add_kernel<<<(unsigned)nb, SCAN_BLOCK, 0, st>>>(out, n, offs);
+        if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("scan_add_kernel");
+    }
+    return HDR_OK;
+}
+
+int hdr_sample_index_workspace_bytes(long long n, long long ncells, size_t *bytes) {
+    if (!bytes || n < 0 || ncells < 1) return HDR_ERR_ARG;
+    // bbox (8 x int64) | counts (ncells + 1) | fill (ncells) | perm (n) | scan scratch
+    *bytes = 8 * sizeof(long long) + (size_t)(2 * ncells + 1 + n) * sizeof(long long) +
+             scan_scratch(ncells + 1) * sizeof(long long);
+    return HDR_OK;
+}
+
+int hdr_sample_index_bbox(const double *positions, const uint8_t *channels, long long n,
+                          int channel, long long *count, int *x0, int *y0, int *nx, int *ny,
+                          void *workspace, void *stream) {
+    if (!positions || !channels || n < 0 || !count || !x0 || !y0 || !nx || !ny || !workspace)
+        return HDR_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    long long *bbox = (long long *)workspace;
+    COUNT_LAUNCH();
+    sample_bbox_init_kernel<<<1, 1, 0, st>>>(bbox);
+    if (n > 0) {
+        COUNT_LAUNCH();
+        const long long blocks = std::min<long long>((n + 255) / 256, 148 * 8);
+        sample_bbox_kernel<<<(unsigned)blocks, 256, 0, st>>>((const double2 *)positions, channels,
+                                                             n, channel, bbox);
+    }
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("sample_bbox_kernel");
+    long long h[5];
+    if (cudaMemcpyAsync(h, bbox, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return cuda_fail("sample bbox read-back");
+    *count = h[0];
+    if (h[0] == 0) {  // empty index: one cell (radiometry.py: empty bbox)
+        *x0 = *y0 = 0;
+        *nx = *ny = 1;
+        return HDR_OK;
+    }
+    const long long w = h[3] - h[1] + 1, hh = h[4] - h[2] + 1;
+    if (h[1] < INT_MIN / 2 || h[2] < INT_MIN / 2 || w > (1 << 20) || hh > (1 << 20) ||
+        w * hh > (1ll << 31)) {
+        snprintf(g_last_error, sizeof(g_last_error), "sample bbox too large (%lld x %lld cells)",
+                 w, hh);
+        return HDR_ERR_ARG;
+    }
+    *x0 = (int)h[1];
+    *y0 = (int)h[2];
+    *nx = (int)w;
+    *ny = (int)hh;
+    return HDR_OK;
+}
+
+int hdr_sample_index_build(const double *positions, const uint8_t *channels, const double *values,
+                           const double *sigmas, long long n, int channel, int x0, int y0, int nx,
+                           int ny, long long *cell_start, double *packed, void *workspace,
+                           size_t workspace_bytes, void *stream) {
+    if (!positions || !channels || !values || !sigmas || !cell_start || !workspace || nx < 1 ||
+        ny < 1 || n < 0)
+        return HDR_ERR_ARG;
+    const long long ncells = (long long)nx * ny;
+    size_t need = 0;
+    hdr_sample_index_workspace_bytes(n, ncells, &need);
+    if (workspace_bytes < need) return HDR_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    long long *counts = (long long *)workspace + 8;
+    unsigned long long *fill = (unsigned long long *)(counts + ncells + 1);
+    long long *perm = (long long *)(fill + ncells);
+    long long *scratch = perm + n;
+    if (cudaMemsetAsync(counts, 0, (size_t)(2 * ncells + 1) * sizeof(long long), st) != cudaSuccess)
+        return cuda_fail("sample index memset");
+    const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+    const double2 *pos = (const double2 *)positions;
+    COUNT_LAUNCH();
+    cell_count_kernel<<<blocks, 256, 0, st>>>(pos, channels, n, channel, x0, y0, nx, counts);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("cell_count_kernel");
+    const int rc = device_scan(counts, cell_start, ncells + 1, scratch, st);
+    if (rc != HDR_OK) return rc;
+    COUNT_LAUNCH();
+    cell_scatter_kernel<<<blocks, 256, 0, st>>>(pos, channels, n, channel, x0, y0, nx, cell_start,
+                                                fill, perm);
+    const unsigned cblocks = (unsigned)std::min<long long>((ncells + 255) / 256, 148 * 16);
+    COUNT_LAUNCH();
+    cell_order_kernel<<<cblocks, 256, 0, st>>>(pos, values, sigmas, ncells, cell_start, perm,
+                                               (double4 *)packed);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("cell_order_kernel");
+}
+
+int hdr_sample_count(const HdrSensor *sensor, const double *sigma, long long *count,
+                     void *workspace, void *stream) {
+    if (!sensor || !sigma || !count || !workspace) return HDR_ERR_ARG;
+    DevSensor d;
+    const int rc = fill_sensor(*sensor, d);
+    if (rc != HDR_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    // workspace: rows[h + 1] | start[h + 1] | scan scratch
+    long long *rows = (long long *)workspace, *start = rows + d.height + 1;
+    COUNT_LAUNCH();
+    row_count_kernel<<<d.height, 256, 0, st>>>(sigma, d.width, d.height, rows);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("row_count_kernel");
+    long long *scratch = start + d.height + 1;
+    // start[y] = kept pixels before row y; start[h] = total
+    if (cudaMemsetAsync(rows + d.height, 0, sizeof(long long), st) != cudaSuccess)
+        return cuda_fail("sample count memset");
+    const int rc2 = device_scan(rows, start, d.height + 1, scratch, st);
+    if (rc2 != HDR_OK) return rc2;
+    if (cudaMemcpyAsync(count, start + d.height, sizeof(long long), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return cuda_fail("sample count read-back");
+    return HDR_OK;
+}
+
+int hdr_compact_samples(const HdrSensor *sensor, int sensor_id, const double *value,
+                        const double *sigma, long long offset, double *positions,
+                        uint8_t *channels, double *values, double *sigmas, int *sensor_ids,
+                        const void *workspace, void *stream) {
+    if (!sensor || !value || !sigma || !positions || !channels || !values || !sigmas ||
+        !sensor_ids || !workspace || offset < 0)
+        return HDR_ERR_ARG;
+    DevSensor d;
+    const int rc = fill_sensor(*sensor, d);
+    if (rc != HDR_OK) return rc;
+    const long long *start = (const long long *)workspace + d.height + 1;
+    COUNT_LAUNCH();
+    row_compact_kernel<<<d.height, 256, 0, (cudaStream_t)stream>>>(
+        d, sensor_id, value, sigma, d.width, d.height, start, offset, (double2 *)positions,
+        channels, values, sigmas, sensor_ids);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("row_compact_kernel");
+}
+
+int hdr_sample_count_workspace_bytes(int height, size_t *bytes) {
+    if (!bytes || height < 1) return HDR_ERR_ARG;
+    *bytes = (size_t)(2 * ((long long)height + 1) + scan_scratch(height + 1)) * sizeof(long long);
+    return HDR_OK;
 }
 
 int hdr_fp64_peak_probe(double *flops_per_s, void *stream) {

@@ -396,26 +396,45 @@ class DeviceRig:
 
     def materialize_samples(self):
         """Sample columns in the reference's order (sensor-major, raster;
-        radiometry.py:303-349), compacted on the device: positions (n, 2) f64,
+        radiometry.py:303-349), compacted on the device by the library
+        (hdr_sample_count / hdr_compact_samples): positions (n, 2) f64,
         channels u8, values f64, sigmas f64, sensor ids i32 as device tensors.
         Values and sigmas are bit-identical to the reference's; positions use
         apply_transform's operation order (T00*x + T01*y + T02)."""
-        cols = []
-        for k, (v, s) in enumerate(self.sample_planes()):
-            cfg = self.configs[k]
-            w = int(self.raws[k].shape[1])
-            idx = torch.nonzero(s.reshape(-1) > 0).squeeze(1)  # ascending = raster order
-            ys, xs = idx // w, idx % w
-            T = np.asarray(cfg.transform, dtype=np.float64)
-            xd, yd = xs.to(torch.float64), ys.to(torch.float64)
-            X = float(T[0, 0]) * xd + float(T[0, 1]) * yd + float(T[0, 2])
-            Y = float(T[1, 0]) * xd + float(T[1, 1]) * yd + float(T[1, 2])
-            tile = torch.as_tensor(np.asarray(cfg.pattern.flat_tile(), np.uint8), device=self.device)
-            ch = tile[(ys % 2) * 2 + xs % 2]
-            cols.append((torch.stack([X, Y], 1), ch, v.reshape(-1)[idx], s.reshape(-1)[idx],
-                         torch.full((len(idx),), int(cfg.sensor_id), dtype=torch.int32,
-                                    device=self.device)))  # radiometry.py:335
-        return tuple(torch.cat([c[i] for c in cols]) for i in range(5))
+        lib = N.lib()
+        st = torch.cuda.current_stream(self.device)
+        planes = self.sample_planes()
+        counts, wss = [], []
+        with torch.cuda.device(self.device):
+            for k, (v, s) in enumerate(planes):
+                h = int(self.raws[k].shape[0])
+                b = ctypes.c_size_t()
+                N.check(lib.hdr_sample_count_workspace_bytes(h, ctypes.byref(b)),
+                        "hdr_sample_count_workspace_bytes")
+                ws = torch.empty(int(b.value), dtype=torch.uint8, device=self.device)
+                n = ctypes.c_longlong()
+                N.check(lib.hdr_sample_count(ctypes.byref(self._sensors[k]), s.data_ptr(),
+                                             ctypes.byref(n), ws.data_ptr(), st.cuda_stream),
+                        "hdr_sample_count")
+                counts.append(int(n.value))
+                wss.append(ws)
+            total = sum(counts)
+            dev = self.device
+            pos = torch.empty((total, 2), dtype=torch.float64, device=dev)
+            ch = torch.empty(total, dtype=torch.uint8, device=dev)
+            val = torch.empty(total, dtype=torch.float64, device=dev)
+            sig = torch.empty(total, dtype=torch.float64, device=dev)
+            ids = torch.empty(total, dtype=torch.int32, device=dev)
+            off = 0
+            for k, (v, s) in enumerate(planes):
+                if counts[k]:
+                    N.check(lib.hdr_compact_samples(
+                        ctypes.byref(self._sensors[k]), int(self.configs[k].sensor_id),  # :335
+                        v.data_ptr(), s.data_ptr(), off, pos.data_ptr(), ch.data_ptr(),
+                        val.data_ptr(), sig.data_ptr(), ids.data_ptr(), wss[k].data_ptr(),
+                        st.cuda_stream), "hdr_compact_samples")
+                off += counts[k]
+        return pos, ch, val, sig, ids
 
 
 class CapturedReconstruction:

@@ -6,6 +6,7 @@ _evaluate_index).  The unit-cell CSR index is built on the GPU (stable sort
 by cell, torch as the device-memory/sort provider) and queries run in
 ``hdr_lpa_evaluate_samples`` -- a CUDA restatement of the reference's own
 kernel boundary ``_kernels.lpa_evaluate`` in its exact operation order.
+The index is a stable counting sort in the library (hdr_sample_index_*).
 """
 
 from __future__ import annotations
@@ -139,32 +140,43 @@ class RadianceSamples:
 class SampleIndex:
     """Unit-cell CSR grid over one channel's samples, on the GPU (reference
     radiometry.py:208-242): cells over floor(x), floor(y) from the bbox origin,
-    samples stable-sorted by cell, packed rows [x, y, value, sigma^2]."""
+    samples stable-sorted by cell, packed rows [x, y, value, sigma^2].  Built
+    by the library's stable counting sort (hdr_sample_index_bbox / _build):
+    per-cell counts, a device scan, an atomic scatter and a per-cell restore
+    of the original order -- no library sort."""
 
     def __init__(self, samples: RadianceSamples, channel: ColorChannel, device=None):
         dev = torch.device(device) if device is not None else _device()
-        ch = samples.device_column("channels", dev)
-        sel = torch.nonzero(ch == int(channel)).squeeze(1)  # ascending: the reference's order
-        self.n = int(sel.numel())
         pos = samples.device_column("positions", dev)
-        x = pos[sel, 0].contiguous()
-        y = pos[sel, 1].contiguous()
-        if self.n:
-            self.x0 = int(math.floor(float(x.min())))
-            self.y0 = int(math.floor(float(y.min())))
-            self.nx = int(math.floor(float(x.max()))) - self.x0 + 1
-            self.ny = int(math.floor(float(y.max()))) - self.y0 + 1
-        else:
-            self.x0 = self.y0 = 0
-            self.nx = self.ny = 1
-        cell = (torch.floor(y).long() - self.y0) * self.nx + (torch.floor(x).long() - self.x0)
-        order = torch.sort(cell, stable=True).indices
-        counts = torch.bincount(cell, minlength=self.nx * self.ny)
-        self.cell_start = torch.zeros(self.nx * self.ny + 1, dtype=torch.int64, device=dev)
-        self.cell_start[1:] = torch.cumsum(counts, 0)
-        v = samples.device_column("values", dev)[sel]
-        s = samples.device_column("sigmas", dev)[sel]
-        self.packed = torch.stack([x[order], y[order], v[order], (s * s)[order]], 1).contiguous()
+        ch = samples.device_column("channels", dev)
+        val = samples.device_column("values", dev)
+        sig = samples.device_column("sigmas", dev)
+        n = len(samples)
+        lib = N.lib()
+        st = torch.cuda.current_stream(dev)
+        hdr = torch.empty(64, dtype=torch.uint8, device=dev)
+        cnt, x0, y0, nx, ny = (ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int(),
+                               ctypes.c_int())
+        with torch.cuda.device(dev):
+            N.check(lib.hdr_sample_index_bbox(pos.data_ptr(), ch.data_ptr(), n, int(channel),
+                                              ctypes.byref(cnt), ctypes.byref(x0),
+                                              ctypes.byref(y0), ctypes.byref(nx), ctypes.byref(ny),
+                                              hdr.data_ptr(), st.cuda_stream),
+                    "hdr_sample_index_bbox")
+            self.n = int(cnt.value)
+            self.x0, self.y0, self.nx, self.ny = int(x0.value), int(y0.value), int(nx.value), int(ny.value)
+            ncells = self.nx * self.ny
+            wsb = ctypes.c_size_t()
+            N.check(lib.hdr_sample_index_workspace_bytes(n, ncells, ctypes.byref(wsb)),
+                    "hdr_sample_index_workspace_bytes")
+            ws = torch.empty(int(wsb.value), dtype=torch.uint8, device=dev)
+            self.cell_start = torch.empty(ncells + 1, dtype=torch.int64, device=dev)
+            self.packed = torch.empty((self.n, 4), dtype=torch.float64, device=dev)
+            N.check(lib.hdr_sample_index_build(
+                pos.data_ptr(), ch.data_ptr(), val.data_ptr(), sig.data_ptr(), n, int(channel),
+                self.x0, self.y0, self.nx, self.ny, self.cell_start.data_ptr(),
+                self.packed.data_ptr() if self.n else None, ws.data_ptr(), ws.numel(),
+                st.cuda_stream), "hdr_sample_index_build")
         self.device = dev
 
     def __len__(self) -> int:

@@ -160,3 +160,61 @@ def test_device_materialized_samples_reproduce_reference_pin9_sha(cuda):
     assert s.on_device
     img = hl.reconstruct_frame(s, out_size, params)
     assert hashlib.sha256(img.data.tobytes()).hexdigest() == manifest()["pin9_sha256_reference_test"]
+
+
+def _reference_index(pos, ch, vals, sig, channel):
+    """The reference's SampleIndex (radiometry.py:208-242) restated in numpy:
+    bbox cells, np.argsort(kind="stable"), CSR, packed [x, y, v, s^2]."""
+    sel = np.nonzero(ch == channel)[0]
+    x, y = pos[sel, 0], pos[sel, 1]
+    x0, y0 = int(np.floor(x.min())), int(np.floor(y.min()))
+    nx = int(np.floor(x.max())) - x0 + 1
+    ny = int(np.floor(y.max())) - y0 + 1
+    cell = (np.floor(y).astype(np.int64) - y0) * nx + (np.floor(x).astype(np.int64) - x0)
+    order = np.argsort(cell, kind="stable")
+    cs = np.zeros(nx * ny + 1, np.int64)
+    np.cumsum(np.bincount(cell, minlength=nx * ny), out=cs[1:])
+    packed = np.column_stack([x[order], y[order], vals[sel][order], (sig[sel] ** 2)[order]])
+    return (x0, y0, nx, ny), cs, packed
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_native_index_equals_stable_argsort(cuda, seed):
+    """hdr_sample_index_build (counting sort + per-cell order restore) equals
+    np.argsort(kind='stable') on samples with many ties per cell, negative
+    coordinates and channels interleaved at random."""
+    rng = np.random.default_rng(seed)
+    n = 20000
+    pos = np.column_stack([rng.uniform(-7.3, 25.9, n), rng.uniform(-3.1, 11.2, n)])
+    pos[::7] = np.floor(pos[::7]) + 0.25            # exact cell-interior duplicates
+    pos[::11] = np.floor(pos[::11])                 # exactly on cell corners
+    ch = rng.integers(0, 3, n).astype(np.uint8)
+    vals, sig = rng.normal(100, 30, n), rng.uniform(0.5, 3.0, n)
+    s = hl.RadianceSamples(pos, ch, vals, sig, np.zeros(n))
+    for c in range(3):
+        ix = s.index(c)
+        (x0, y0, nx, ny), cs, packed = _reference_index(pos, ch, vals, sig, c)
+        assert (ix.x0, ix.y0, ix.nx, ix.ny) == (x0, y0, nx, ny)
+        assert np.array_equal(ix.cell_start.cpu().numpy(), cs)
+        assert np.array_equal(ix.packed.cpu().numpy(), packed)
+
+
+def test_native_materialize_keeps_sensor_ids_and_order(cuda):
+    """materialize() through hdr_sample_count / hdr_compact_samples: the
+    oracle's sample columns (raster order, sensor-major) and the configs'
+    own (non-contiguous) sensor ids (radiometry.py:335)."""
+    import dataclasses
+
+    from paper_1308_4908_b200 import simulate as sim
+
+    W, H = 70, 46
+    rig = sim.baseline_rig("misaligned", W, H, seed=9)
+    sensors = [dataclasses.replace(c, sensor_id=i) for c, i in zip(rig.sensors, (7, 2, 40))]
+    frames = sim.simulate_rig(sim.hdr_chart(W, H), rig)
+    cals = rig.calibrations()
+    s = hl.frames_to_samples(frames, sensors, cals).materialize()
+    pos, chan, val, sig, sid = oracle.frames_to_samples(frames, sensors, cals)
+    assert np.array_equal(s.positions, pos) and np.array_equal(s.channels, chan)
+    assert np.array_equal(s.values, val) and np.array_equal(s.sigmas, sig)
+    assert np.array_equal(s.sensor_ids, sid)
+    assert set(np.unique(s.sensor_ids)) == {7, 2, 40}
