@@ -275,7 +275,7 @@ def run_next(args, wl, world, rank, local):
     out_size = wl["out"]
     rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0)
     cals = rigspec.calibrations()
-    frame_sets = [sim.simulate_rig_torch(sim.hdr_chart(W, H), rigspec, dev, seed=1000 * rank + i)
+    frame_sets = [sim.simulate_rig_device(sim.hdr_chart(W, H), rigspec, dev, seed=1000 * rank + i)
                   for i in range(N_DISTINCT)]
     rigs = [DeviceRig.from_device(fs, rigspec.sensors, cals) for fs in frame_sets]
     params = _params(wl)
@@ -548,7 +548,7 @@ def run_ours(args, wl, world, rank, local):
     gt = sim.hdr_chart(W, H)
     rigspec = sim.baseline_rig(wl["rig"], W, H, seed=0, n_sensors=wl.get("sensors", 3))
     cals = rigspec.calibrations()
-    frame_sets = [sim.simulate_rig_torch(gt, rigspec, dev, seed=1000 * rank + i)
+    frame_sets = [sim.simulate_rig_device(gt, rigspec, dev, seed=1000 * rank + i)
                   for i in range(N_DISTINCT)]
     torch.cuda.synchronize()
     rig = DeviceRig.from_device(frame_sets[0], rigspec.sensors, cals)

@@ -269,6 +269,18 @@ int hdr_compact_samples(const HdrSensor *sensor, int sensor_id, const double *va
  * (its first 64 bytes also serve hdr_sample_index_bbox).  (ABI v5)
  */
 int hdr_sample_index_workspace_bytes(long long n, long long ncells, size_t *bytes);
+
+/*
+ * Camera simulator on the device (input generator; reference simulate.py
+ * simulate_sensor / expose, :92-212): one raw frame into sensor->raw (uint16,
+ * pitch) from a float32 H x W x 3 ground truth; sensor->transform maps sensor
+ * pixels to ground-truth coordinates; the calibration scalars are the noise
+ * truth (bias DV, Var[r] DV^2, non-uniformity).  Counter-based Philox4x32-10
+ * keyed by (seed, sensor_id); noise_free = the draws' means (bit-identical to
+ * the reference's noise-free frames).  (ABI v5)
+ */
+int hdr_simulate_sensor(const float *gt, int gt_w, int gt_h, const HdrSensor *sensor,
+                        unsigned long long seed, int sensor_id, int noise_free, void *stream);
 int hdr_sample_index_bbox(const double *positions, const uint8_t *channels, long long n,
                           int channel, long long *count, int *x0, int *y0, int *nx, int *ny,
                           void *workspace, void *stream);

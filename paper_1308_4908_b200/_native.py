@@ -51,6 +51,7 @@ EXPORTED = (
     "hdr_sample_index_workspace_bytes",
     "hdr_sample_index_bbox",
     "hdr_sample_index_build",
+    "hdr_simulate_sensor",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
     "hdr_lpa_last_error",
@@ -229,6 +230,9 @@ def lib():
             L.hdr_sample_index_build.argtypes = [vp, vp, vp, vp, i64, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp,
                                                  vp, ctypes.c_size_t, vp]
+            L.hdr_simulate_sensor.argtypes = [vp, ctypes.c_int, ctypes.c_int,
+                                              ctypes.POINTER(HdrSensor), ctypes.c_ulonglong,
+                                              ctypes.c_int, ctypes.c_int, vp]
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
             L.hdr_lpa_status_string.restype = ctypes.c_char_p
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]

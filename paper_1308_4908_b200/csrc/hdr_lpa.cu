@@ -32,6 +32,7 @@
 #include "calpa.cuh"
 #include "samples.cuh"
 #include "sample_index.cuh"
+#include "simulate.cuh"
 
 namespace hdrlpa {
 
@@ -1084,6 +1085,20 @@ int hdr_sample_count_workspace_bytes(int height, size_t *bytes) {
     if (!bytes || height < 1) return HDR_ERR_ARG;
     *bytes = (size_t)(2 * ((long long)height + 1) + scan_scratch(height + 1)) * sizeof(long long);
     return HDR_OK;
+}
+
+int hdr_simulate_sensor(const float *gt, int gt_w, int gt_h, const HdrSensor *sensor,
+                        unsigned long long seed, int sensor_id, int noise_free, void *stream) {
+    if (!gt || gt_w < 1 || gt_h < 1 || !sensor || !sensor->raw) return HDR_ERR_ARG;
+    DevSensor d;
+    const int rc = fill_sensor(*sensor, d);
+    if (rc != HDR_OK) return rc;
+    if (d.planes || d.defective) return HDR_ERR_ARG;  // scalar noise truth only
+    dim3 grid((d.width + 127) / 128, d.height);
+    COUNT_LAUNCH();
+    simulate_sensor_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
+        gt, gt_w, gt_h, d, seed, sensor_id, noise_free, (uint16_t *)d.raw, d.pitch);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("simulate_sensor_kernel");
 }
 
 int hdr_fp64_peak_probe(double *flops_per_s, void *stream) {

@@ -5,8 +5,8 @@ Forward camera model of the reference (pkg/src/hdrfuse/simulate.py:1-12,
 y = floor(g e + r + 0.5) with readout r ~ Normal(bias, Var[r]), clipped to
 [0, saturation_level].  Ground-truth scenes are sampled bilinearly through
 each sensor's transform.  This module only produces inputs; it is not on the
-reconstruction path.  ``simulate_rig_torch`` generates the same model on the
-GPU (for the multi-megapixel bench frames).
+reconstruction path.  ``simulate_rig_device`` generates the same model on the
+GPU (hdr_simulate_sensor; the multi-megapixel bench and video frames).
 """
 
 from __future__ import annotations
@@ -163,38 +163,47 @@ def simulate_rig(gt: HDRImage, rig: RigSpec):
     return frames
 
 
-def simulate_rig_torch(gt: HDRImage, rig: RigSpec, device, seed: Optional[int] = None):
-    """GPU version of :func:`simulate_rig` (same model, torch RNG): returns a
-    list of (h, w) int16 device tensors holding the uint16 digital values."""
+def simulate_rig_device(gt: HDRImage, rig: RigSpec, device, seed: Optional[int] = None):
+    """The same camera model on the GPU (hdr_simulate_sensor; reference
+    simulate.py:92-212): one raw frame per sensor as an (h, w) int16 device
+    tensor holding the uint16 digital values (rows padded to 16 bytes for the
+    reconstruction's TMA staging).  Noise draws come from counter-based
+    Philox4x32-10 streams keyed by (seed, sensor_id) like the reference's
+    sensor_rng (:85-88); noise-free frames are bit-identical to
+    :func:`simulate_rig`'s."""
+    import ctypes
+
     import torch
 
-    gen = torch.Generator(device=device)
-    gen.manual_seed(rig.seed if seed is None else seed)
-    gtd = torch.as_tensor(gt.data, device=device, dtype=torch.float64)
+    from . import _native as N
+
+    device = torch.device(device)
+    gtd = torch.as_tensor(np.ascontiguousarray(gt.data, dtype=np.float32), device=device)
+    run_seed = rig.seed if seed is None else int(seed)
     out = []
-    for cfg, noise, (w, h) in zip(rig.sensors, rig.noise, rig.sensor_sizes):
-        ys, xs = torch.meshgrid(torch.arange(h, device=device, dtype=torch.float64),
-                                torch.arange(w, device=device, dtype=torch.float64), indexing="ij")
-        T = cfg.transform
-        X = (T[0, 0] * xs + T[0, 1] * ys + T[0, 2]).clamp(0, gt.width - 1)
-        Y = (T[1, 0] * xs + T[1, 1] * ys + T[1, 2]).clamp(0, gt.height - 1)
-        tile = torch.as_tensor(cfg.pattern.flat_tile(), device=device)
-        ch = tile[(ys.long() % 2) * 2 + xs.long() % 2]
-        x0, y0 = X.floor().long(), Y.floor().long()
-        x1, y1 = (x0 + 1).clamp(max=gt.width - 1), (y0 + 1).clamp(max=gt.height - 1)
-        fx, fy = X - x0, Y - y0
-        P = lambda yy, xx: gtd[yy, xx, ch]  # noqa: E731
-        f = (P(y0, x0) * (1 - fx) + P(y0, x1) * fx) * (1 - fy) + \
-            (P(y1, x0) * (1 - fx) + P(y1, x1) * fx) * fy
-        lam = cfg.exposure_time * noise.nonuniformity * cfg.exposure_scaling * f.clamp(min=0)
-        if rig.noise_free:
-            e, r = lam, noise.bias_dv
-        else:
-            e = torch.poisson(lam, generator=gen)
-            r = noise.bias_dv + math.sqrt(noise.readout_var_dv2) * torch.randn(
-                lam.shape, generator=gen, device=device, dtype=torch.float64)
-        y = torch.floor(cfg.gain * e + r + 0.5).clamp(0, cfg.saturation_level)
-        out.append(y.to(torch.int32).to(torch.int16))
+    with torch.cuda.device(device):
+        st = torch.cuda.current_stream(device)
+        for cfg, noise, (w, h) in zip(rig.sensors, rig.noise, rig.sensor_sizes):
+            pw = (w + 7) // 8 * 8
+            buf = torch.empty((h, pw), dtype=torch.int16, device=device)
+            s = N.HdrSensor()
+            s.raw, s.width, s.height, s.pitch = buf.data_ptr(), w, h, pw
+            s.saturation_level = int(cfg.saturation_level)
+            tile = cfg.pattern.flat_tile()
+            for i in range(4):
+                s.tile[i] = int(tile[i])
+            s.exposure_time, s.gain = float(cfg.exposure_time), float(cfg.gain)
+            s.exposure_scaling = float(cfg.exposure_scaling)
+            T = np.asarray(cfg.transform, dtype=np.float64).reshape(6)
+            for i in range(6):
+                s.transform[i] = float(T[i])
+            s.bias, s.readout_variance = float(noise.bias_dv), float(noise.readout_var_dv2)
+            s.nonuniformity = float(noise.nonuniformity)
+            N.check(N.lib().hdr_simulate_sensor(
+                gtd.data_ptr(), int(gt.width), int(gt.height), ctypes.byref(s),
+                ctypes.c_ulonglong(run_seed & (2 ** 64 - 1)), int(cfg.sensor_id),
+                1 if rig.noise_free else 0, st.cuda_stream), "hdr_simulate_sensor")
+            out.append(buf[:, :w])
     return out
 
 

@@ -15,7 +15,7 @@ from paper_1308_4908_b200.steering import (auto_gradient_scale, compute_steering
 W, H = 2400, 1700
 dev = torch.device("cuda", 0)
 rs = sim.baseline_rig("aligned", W, H, seed=0)
-frames = sim.simulate_rig_torch(sim.hdr_chart(W, H), rs, dev, seed=1)
+frames = sim.simulate_rig_device(sim.hdr_chart(W, H), rs, dev, seed=1)
 rig = DeviceRig.from_device(frames, rs.sensors, rs.calibrations())
 ap = hl.AdaptiveParams(base=hl.ReconstructionParams(order=1, scale=0.7))
 

@@ -13,7 +13,7 @@ W, H = 2400, 1700
 dev = torch.device("cuda", 0)
 rig = sim.baseline_rig("aligned", W, H, seed=0)
 gt = sim.hdr_chart(W, H)
-sets = [sim.simulate_rig_torch(gt, rig, dev, seed=i) for i in range(4)]
+sets = [sim.simulate_rig_device(gt, rig, dev, seed=i) for i in range(4)]
 host = [[t.cpu().pin_memory() for t in fs] for fs in sets]
 outs = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
 p = hl.ReconstructionParams(order=1, scale=0.7)

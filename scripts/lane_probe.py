@@ -17,7 +17,7 @@ out_size = wl["out"]
 dev = torch.device("cuda", 0)
 rs = sim.baseline_rig(wl["rig"], W, H, seed=0)
 cals = rs.calibrations()
-sets = [sim.simulate_rig_torch(sim.hdr_chart(W, H), rs, dev, seed=i) for i in range(6)]
+sets = [sim.simulate_rig_device(sim.hdr_chart(W, H), rs, dev, seed=i) for i in range(6)]
 p = bench._params(wl)
 rigs = [DeviceRig.from_device(fs, rs.sensors, cals) for fs in sets]
 n = 6

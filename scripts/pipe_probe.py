@@ -14,7 +14,7 @@ W, H = wl["size"]
 out_w, out_h = wl["out"]
 dev = torch.device("cuda", 0)
 rs = sim.baseline_rig(wl["rig"], W, H, seed=0)
-sets = [sim.simulate_rig_torch(sim.hdr_chart(W, H), rs, dev, seed=i) for i in range(3)]
+sets = [sim.simulate_rig_device(sim.hdr_chart(W, H), rs, dev, seed=i) for i in range(3)]
 host = [[t.cpu().pin_memory() for t in fs] for fs in sets]
 p = bench._params(wl)
 for slots in (1, 2, 3):

@@ -16,7 +16,7 @@ dev = torch.device("cuda", 0)
 W, H = wl["size"]
 gt = sim.hdr_chart(W, H)
 rs = sim.baseline_rig(wl["rig"], W, H, seed=0, n_sensors=wl.get("sensors", 3))
-frames = sim.simulate_rig_torch(gt, rs, dev, seed=1)
+frames = sim.simulate_rig_device(gt, rs, dev, seed=1)
 rig = DeviceRig.from_device(frames, rs.sensors, rs.calibrations())
 out = rig.allocate_outputs(wl["out"])
 p = bench._params(wl)

@@ -15,7 +15,7 @@ from paper_1308_4908_b200.samples import RadianceSamples, SampleIndex, evaluate_
 W, H = 2400, 1700
 dev = torch.device("cuda", 0)
 rs = sim.baseline_rig("misaligned", W, H, seed=0)
-frames = sim.simulate_rig_torch(sim.hdr_chart(W, H), rs, dev, seed=1)
+frames = sim.simulate_rig_device(sim.hdr_chart(W, H), rs, dev, seed=1)
 rig = DeviceRig.from_device(frames, rs.sensors, rs.calibrations())
 samples = RadianceSamples(*rig.materialize_samples())
 print("samples", len(samples), flush=True)
