@@ -10,6 +10,7 @@
 #include <type_traits>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "hdr_lpa.h"
@@ -77,6 +78,9 @@ inline int launch_ici(const DevParams &P, const TapParam &T, int tiles, int smem
                       cudaStream_t st) {
     const int occ_sm = fast_occupancy<ORDER, true, MAXC, 0, RT, false, false, true>(smem_bytes);
     const int occ_rg = fast_occupancy<ORDER, true, MAXC, 0, RT, false, false, false>(smem_bytes);
+    if (getenv("HDR_DEBUG_RT"))
+        fprintf(stderr, "ici kernel: dynamic smem %d B, CTAs/SM smem-state %d, register-state %d\n",
+                smem_bytes, occ_sm, occ_rg);
     if (occ_sm > 0 && occ_sm >= occ_rg)
         return launch_fast<ORDER, true, MAXC, 0, RT, false, false, true>(P, T, tiles, smem_bytes, st);
     return launch_fast<ORDER, true, MAXC, 0, RT, false, false, false>(P, T, tiles, smem_bytes, st);

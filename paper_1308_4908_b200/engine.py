@@ -112,7 +112,7 @@ class DeviceRig:
                 if plane.shape != (h, w):
                     raise ShapeMismatchError(
                         f"dimension mismatch: {name} {plane.shape} vs frame {(h, w)}")
-                u = _uniform_value(plane)
+                u = cal.scalar(name) if hasattr(cal, "scalar") else _uniform_value(plane)
                 entry[name] = u if u is not None else torch.from_numpy(
                     np.ascontiguousarray(plane)).to(device)
             cal_entries.append(entry)
@@ -136,7 +136,8 @@ class DeviceRig:
             for name in ("bias", "readout_variance", "nonuniformity"):
                 plane = np.asarray(getattr(getattr(cal, name), "data", getattr(cal, name)),
                                    dtype=np.float64)
-                u = float(plane) if plane.ndim == 0 else _uniform_value(plane)
+                u = float(plane) if plane.ndim == 0 else (
+                    cal.scalar(name) if hasattr(cal, "scalar") else _uniform_value(plane))
                 entry[name] = u if u is not None else torch.from_numpy(
                     np.ascontiguousarray(plane)).to(device)
             entries.append(entry)

@@ -111,12 +111,29 @@ class NoiseCalibration:
     def shape(self):
         return self.bias.data.shape
 
+    def scalar(self, name: str):
+        """The plane's value if the plane ``name`` is uniform, else None --
+        memoised (the planes are immutable), so a per-frame call does not scan
+        4-Mpx planes again (the GPU path passes uniform planes as scalars)."""
+        cache = self.__dict__.get("_scalars")
+        if cache is None:
+            cache = {}
+            object.__setattr__(self, "_scalars", cache)
+        if name not in cache:
+            flat = np.asarray(getattr(self, name).data).ravel()
+            cache[name] = float(flat[0]) if flat.size and (flat == flat[0]).all() else None
+        return cache[name]
+
     @classmethod
     def uniform(cls, width, height, bias=0.0, readout_variance=0.0, nonuniformity=1.0,
                 gain_estimate=0.0) -> "NoiseCalibration":
-        return cls(FloatFrame.full(width, height, bias),
-                   FloatFrame.full(width, height, readout_variance),
-                   FloatFrame.full(width, height, nonuniformity), gain_estimate)
+        cal = cls(FloatFrame.full(width, height, bias),
+                  FloatFrame.full(width, height, readout_variance),
+                  FloatFrame.full(width, height, nonuniformity), gain_estimate)
+        object.__setattr__(cal, "_scalars", {"bias": float(cal.bias.data.flat[0]),
+                                             "readout_variance": float(cal.readout_variance.data.flat[0]),
+                                             "nonuniformity": float(cal.nonuniformity.data.flat[0])})
+        return cal
 
 
 def _denominator(cfg: SensorConfig, a):
@@ -175,7 +192,8 @@ class RawFrameSet:
             if cal.shape != f.data.shape:
                 raise ShapeMismatchError(
                     f"dimension mismatch: calibration {cal.shape} vs frame {f.data.shape}")
-            _denominator(cfg, cal.nonuniformity.data)
+            a = cal.scalar("nonuniformity") if hasattr(cal, "scalar") else None
+            _denominator(cfg, cal.nonuniformity.data if a is None else a)
         self._device_cache = {}
 
     def __len__(self) -> int:
