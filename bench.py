@@ -334,7 +334,7 @@ def run_next(args, wl, world, rank, local):
     flop64 = n_inside * FLOP64_PER_SAMPLE[1]
     peak64 = ctypes_probe(N, stream)
     traffic = None
-    tpath = ROOT / "profiles" / "r01_traffic.json"
+    tpath = ROOT / "profiles" / "r02_traffic.json"
     if tpath.exists():
         traffic = (json.loads(tpath.read_text()).get(args.workload) or {}).get("traffic_bytes")
     achieved = flop64 / (ms_kernel * 1e-3)
@@ -696,7 +696,7 @@ def run_ours(args, wl, world, rank, local):
     if _cosited(rigspec.sensors, wl):
         planes_bytes = frame_sets[0][0].numel() * 16
     traffic, traffic_src = None, None
-    tpath = ROOT / "profiles" / "r01_traffic.json"
+    tpath = ROOT / "profiles" / "r02_traffic.json"
     if tpath.exists():
         tj = json.loads(tpath.read_text()).get(args.workload)
         if tj:
