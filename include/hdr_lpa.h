@@ -271,6 +271,22 @@ int hdr_compact_samples(const HdrSensor *sensor, int sensor_id, const double *va
 int hdr_sample_index_workspace_bytes(long long n, long long ncells, size_t *bytes);
 
 /*
+ * CALPA without a host round trip (ABI v5): hdr_gradient_scale writes to device
+ * memory the steering field's gradient scale, np.percentile(|finite values|,
+ * 100 q) with numpy's linear interpolation, 1.0 when none is finite or it is 0
+ * (steering.py:206-211; an exact radix select on the float32 bit patterns);
+ * hdr_steering_field_devscale is hdr_steering_field reading that scale from
+ * device memory.  Both are stream-ordered and CUDA-graph capturable.
+ */
+int hdr_gradient_scale_workspace_bytes(size_t *bytes);
+int hdr_gradient_scale(const float *values, long long n, double q, double *scale,
+                       void *workspace, size_t workspace_bytes, void *stream);
+int hdr_steering_field_devscale(const float *gx, const float *gy, int width, int height,
+                                int gradient_window, double lambda1, double lambda2,
+                                double alpha, double sigma_max, const double *gradient_scale,
+                                double *theta, double *sigma, double *gamma, void *stream);
+
+/*
  * Camera simulator on the device (input generator; reference simulate.py
  * simulate_sensor / expose, :92-212): one raw frame into sensor->raw (uint16,
  * pitch) from a float32 H x W x 3 ground truth; sensor->transform maps sensor

@@ -52,6 +52,9 @@ EXPORTED = (
     "hdr_sample_index_bbox",
     "hdr_sample_index_build",
     "hdr_simulate_sensor",
+    "hdr_gradient_scale_workspace_bytes",
+    "hdr_gradient_scale",
+    "hdr_steering_field_devscale",
     "hdr_fp64_peak_probe",
     "hdr_lpa_status_string",
     "hdr_lpa_last_error",
@@ -233,6 +236,11 @@ def lib():
             L.hdr_simulate_sensor.argtypes = [vp, ctypes.c_int, ctypes.c_int,
                                               ctypes.POINTER(HdrSensor), ctypes.c_ulonglong,
                                               ctypes.c_int, ctypes.c_int, vp]
+            L.hdr_gradient_scale_workspace_bytes.argtypes = [ctypes.POINTER(ctypes.c_size_t)]
+            L.hdr_gradient_scale.argtypes = [vp, i64, ctypes.c_double, vp, vp, ctypes.c_size_t, vp]
+            L.hdr_steering_field_devscale.argtypes = [
+                vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, vp, vp, vp, vp]
             L.hdr_fp64_peak_probe.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
             L.hdr_lpa_status_string.restype = ctypes.c_char_p
             L.hdr_lpa_status_string.argtypes = [ctypes.c_int]

@@ -12,6 +12,7 @@ namespace hdrlpa {
 struct SteerConsts {
     int half;
     double wstd, lam1, lam2, alpha, sigma_max, inv_scale;
+    const double *scale_dev;  // non-null: inv_scale = 1 / *scale_dev (device-computed scale)
 };
 
 // steering_field_kernel (_kernels.py:310-392), float64, one thread per pixel.
@@ -20,6 +21,7 @@ __global__ void steering_field_kernel(const float *gx, const float *gy, int w, i
                                       double *gamma) {
     const int xx = blockIdx.x * blockDim.x + threadIdx.x, yy = blockIdx.y;
     if (xx >= w) return;
+    if (K.scale_dev) K.inv_scale = 1.0 / *K.scale_dev;
     double s11 = 0.0, s12 = 0.0, s22 = 0.0;
     int n = 0;
     const double den = 2.0 * K.wstd * K.wstd;
@@ -190,6 +192,147 @@ __global__ void __launch_bounds__(128) lpa_steered_slow_kernel(const __grid_cons
             R.count = 0;
         }
         if ((threadIdx.x & (G - 1)) == 0) write_result(P, pix, c, R);
+    }
+}
+
+}  // namespace hdrlpa
+
+namespace hdrlpa {
+
+// ---------------------------------------------------------------------------
+// The steering field's gradient scale on the device (steering.py:206-211):
+// np.percentile(|finite values|, 99.5) with numpy's linear interpolation
+// (virtual index q (n-1), _lerp with its t >= 0.5 branch), 1.0 when there is
+// no finite value or the percentile is 0.  An exact two-pass radix select on
+// the float32 bit patterns of |v| (monotone for non-negative floats): the
+// high 16 bits pick the bins of ranks k and k+1, the low 16 bits the values.
+// Lets a CALPA frame run without a host round trip (CUDA-graph capturable).
+// Workspace: 4 x 65536 uint32 + 64 B.
+// ---------------------------------------------------------------------------
+constexpr int QBINS = 65536;
+struct QuantileState {
+    unsigned long long n;       // finite values
+    long long rank[2];          // k, k + 1 (clipped)
+    int bin[2];                 // their high-16 bins
+    long long before[2];        // values in lower bins
+    double t;                   // interpolation weight
+};
+
+__global__ void absq_hist_hi_kernel(const float *v, long long n, unsigned *hist,
+                                    unsigned long long *count) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float x = v[i];
+        if (!isfinite(x)) continue;
+        atomicAdd(&hist[__float_as_uint(fabsf(x)) >> 16], 1u);
+        ++c;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// one block of 1024 threads: bins of ranks k and k+1
+__global__ void __launch_bounds__(1024) absq_select_kernel(const unsigned *hist, double q,
+                                                            QuantileState *st) {
+    __shared__ unsigned long long part[1024];
+    const unsigned long long n = st->n;
+    if (n == 0) return;
+    const double vidx = q * (double)(n - 1);  // numpy: quantiles * (n - alpha - beta + 1) + alpha - 1
+    const long long k = (long long)floor(vidx);
+    const long long k1 = k + 1 < (long long)n ? k + 1 : (long long)n - 1;
+    unsigned long long sum = 0;
+    const int per = QBINS / 1024;
+    for (int j = 0; j < per; ++j) sum += hist[threadIdx.x * per + j];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
+        const unsigned long long add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    const unsigned long long lo = threadIdx.x ? part[threadIdx.x - 1] : 0, hi = part[threadIdx.x];
+    for (int r = 0; r < 2; ++r) {
+        const unsigned long long want = (unsigned long long)(r ? k1 : k);
+        if (want >= lo && want < hi) {  // this thread's bins hold the rank
+            unsigned long long acc = lo;
+            for (int j = 0; j < per; ++j) {
+                const unsigned h = hist[threadIdx.x * per + j];
+                if (want < acc + h) {
+                    st->bin[r] = threadIdx.x * per + j;
+                    st->before[r] = (long long)acc;
+                    break;
+                }
+                acc += h;
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        st->rank[0] = k;
+        st->rank[1] = k1;
+        st->t = vidx - (double)k;
+    }
+}
+
+__global__ void absq_hist_lo_kernel(const float *v, long long n, const QuantileState *st,
+                                    unsigned *hist0, unsigned *hist1) {
+    if (st->n == 0) return;
+    const int b0 = st->bin[0], b1 = st->bin[1];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float x = v[i];
+        if (!isfinite(x)) continue;
+        const unsigned u = __float_as_uint(fabsf(x));
+        if ((int)(u >> 16) == b0) atomicAdd(&hist0[u & 0xffffu], 1u);
+        if (b1 != b0 && (int)(u >> 16) == b1) atomicAdd(&hist1[u & 0xffffu], 1u);
+    }
+}
+
+__global__ void __launch_bounds__(1024) absq_finish_kernel(const unsigned *hist0,
+                                                            const unsigned *hist1,
+                                                            const QuantileState *st,
+                                                            double *scale) {
+    __shared__ unsigned long long part[1024];
+    __shared__ float val[2];
+    if (st->n == 0) {
+        if (threadIdx.x == 0) *scale = 1.0;
+        return;
+    }
+    const int per = QBINS / 1024;
+    for (int r = 0; r < 2; ++r) {
+        const unsigned *h = (r == 1 && st->bin[1] != st->bin[0]) ? hist1 : hist0;
+        const unsigned long long want = (unsigned long long)(st->rank[r] - st->before[r]);
+        unsigned long long sum = 0;
+        for (int j = 0; j < per; ++j) sum += h[threadIdx.x * per + j];
+        part[threadIdx.x] = sum;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            const unsigned long long add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+            __syncthreads();
+            part[threadIdx.x] += add;
+            __syncthreads();
+        }
+        const unsigned long long lo = threadIdx.x ? part[threadIdx.x - 1] : 0, hi = part[threadIdx.x];
+        if (want >= lo && want < hi) {
+            unsigned long long acc = lo;
+            for (int j = 0; j < per; ++j) {
+                const unsigned c = h[threadIdx.x * per + j];
+                if (want < acc + c) {
+                    val[r] = __uint_as_float(((unsigned)st->bin[r] << 16) | (unsigned)(threadIdx.x * per + j));
+                    break;
+                }
+                acc += c;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double a = (double)val[0], b = (double)val[1], t = st->t;
+        const double d = b - a;
+        const double p = t >= 0.5 ? b - d * (1.0 - t) : a + d * t;  // numpy _lerp
+        *scale = p > 0.0 ? p : 1.0;
     }
 }
 

@@ -868,13 +868,13 @@ int hdr_lpa_evaluate_samples(const HdrSampleIndex *index, const double *qx, cons
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("lpa_samples_kernel launch");
 }
 
-int hdr_steering_field(const float *gx, const float *gy, int width, int height,
-                       int gradient_window, double lambda1, double lambda2, double alpha,
-                       double sigma_max, double gradient_scale, double *theta, double *sigma,
-                       double *gamma, void *stream) {
+static int steering_field(const float *gx, const float *gy, int width, int height,
+                          int gradient_window, double lambda1, double lambda2, double alpha,
+                          double sigma_max, double gradient_scale, const double *scale_dev,
+                          double *theta, double *sigma, double *gamma, void *stream) {
     if (!gx || !gy || !theta || !sigma || !gamma || width <= 0 || height <= 0) return HDR_ERR_ARG;
     if (gradient_window < 3 || gradient_window % 2 == 0) return HDR_ERR_ARG;
-    if (!(gradient_scale > 0) || !isfinite(gradient_scale)) return HDR_ERR_ARG;
+    if (!scale_dev && (!(gradient_scale > 0) || !isfinite(gradient_scale))) return HDR_ERR_ARG;
     if (alpha < 0 || lambda1 < 0 || !(lambda2 > 0)) return HDR_ERR_ARG;
     SteerConsts K;
     K.half = gradient_window / 2;
@@ -883,12 +883,58 @@ int hdr_steering_field(const float *gx, const float *gy, int width, int height,
     K.lam2 = lambda2;
     K.alpha = alpha;
     K.sigma_max = sigma_max;
-    K.inv_scale = 1.0 / gradient_scale;
+    K.inv_scale = scale_dev ? 0.0 : 1.0 / gradient_scale;
+    K.scale_dev = scale_dev;
     dim3 grid((width + 127) / 128, height);
     COUNT_LAUNCH();
     steering_field_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(gx, gy, width, height, K, theta,
                                                                   sigma, gamma);
     return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("steering_field_kernel launch");
+}
+
+int hdr_steering_field(const float *gx, const float *gy, int width, int height,
+                       int gradient_window, double lambda1, double lambda2, double alpha,
+                       double sigma_max, double gradient_scale, double *theta, double *sigma,
+                       double *gamma, void *stream) {
+    return steering_field(gx, gy, width, height, gradient_window, lambda1, lambda2, alpha,
+                          sigma_max, gradient_scale, nullptr, theta, sigma, gamma, stream);
+}
+
+int hdr_steering_field_devscale(const float *gx, const float *gy, int width, int height,
+                                int gradient_window, double lambda1, double lambda2,
+                                double alpha, double sigma_max, const double *gradient_scale,
+                                double *theta, double *sigma, double *gamma, void *stream) {
+    if (!gradient_scale) return HDR_ERR_ARG;
+    return steering_field(gx, gy, width, height, gradient_window, lambda1, lambda2, alpha,
+                          sigma_max, 0.0, gradient_scale, theta, sigma, gamma, stream);
+}
+
+int hdr_gradient_scale_workspace_bytes(size_t *bytes) {
+    if (!bytes) return HDR_ERR_ARG;
+    *bytes = 3 * (size_t)QBINS * sizeof(unsigned) + 128;
+    return HDR_OK;
+}
+
+int hdr_gradient_scale(const float *values, long long n, double q, double *scale,
+                       void *workspace, size_t workspace_bytes, void *stream) {
+    size_t need = 0;
+    hdr_gradient_scale_workspace_bytes(&need);
+    if (!values || n < 0 || !scale || !workspace || !(q >= 0.0 && q <= 1.0)) return HDR_ERR_ARG;
+    if (workspace_bytes < need) return HDR_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned *hist = (unsigned *)workspace, *hist0 = hist + QBINS, *hist1 = hist0 + QBINS;
+    QuantileState *qs = (QuantileState *)(hist1 + QBINS);
+    if (cudaMemsetAsync(workspace, 0, need, st) != cudaSuccess) return cuda_fail("quantile memset");
+    const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+    COUNT_LAUNCH();
+    absq_hist_hi_kernel<<<blocks, 256, 0, st>>>(values, n, hist, &qs->n);
+    COUNT_LAUNCH();
+    absq_select_kernel<<<1, 1024, 0, st>>>(hist, q, qs);
+    COUNT_LAUNCH();
+    absq_hist_lo_kernel<<<blocks, 256, 0, st>>>(values, n, qs, hist0, hist1);
+    COUNT_LAUNCH();
+    absq_finish_kernel<<<1, 1024, 0, st>>>(hist0, hist1, qs, scale);
+    return cudaPeekAtLastError() == cudaSuccess ? HDR_OK : cuda_fail("gradient scale kernels");
 }
 
 int hdr_saturation_mask(const HdrSensor *sensor, uint32_t *out_bits, int words_per_row,

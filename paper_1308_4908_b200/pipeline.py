@@ -18,10 +18,34 @@ from .engine import DeviceRig
 from .lpa import ReconstructionParams
 
 
+def _capture(rig, fn, out):
+    """Record fn() (stream-ordered library launches, no allocation, no host
+    sync) as a CUDA graph over the rig's frame buffers."""
+    from . import _native as N
+    from .engine import CapturedReconstruction
+
+    side = torch.cuda.Stream(rig.device)
+    side.wait_stream(torch.cuda.current_stream(rig.device))
+    with torch.cuda.stream(side):
+        fn()  # eager first: workspace allocation, kernel attributes
+    side.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    n0 = N.lib().hdr_lpa_launch_count()
+    with torch.cuda.graph(graph, stream=side):
+        fn()
+    return CapturedReconstruction(graph, out, int(N.lib().hdr_lpa_launch_count() - n0),
+                                  list(rig.raws))
+
+
 class FramePipeline:
     def __init__(self, configs, cals, sensor_shapes, out_size, params: ReconstructionParams,
                  ref_size=None, device=None, slots: int = 2, d2h_streams: int = 1,
-                 graphs: bool = True, output: str = "float32", half_scale: float = 1.0 / 16):
+                 graphs: bool = True, output: str = "float32", half_scale: float = 1.0 / 16,
+                 calpa=None):
+        """``calpa``: an AdaptiveParams -- each frame runs calpa_reconstruct
+        (shared steering) entirely on the device (steering.calpa_device: first
+        pass, device gradient scale, steering field, steered pass), recorded
+        per slot as one CUDA graph; ``params`` is then ignored (calpa.base)."""
         self.device = torch.device(device if device is not None else
                                    torch.device("cuda", torch.cuda.current_device()))
         self.out_size = (int(out_size[0]), int(out_size[1]))
@@ -42,11 +66,25 @@ class FramePipeline:
                                                    want_rgb=output == "float32")
                      for _ in range(slots)]
         self.half_scale = half_scale
-        # per slot, the reconstruction recorded once as a CUDA graph (its frame
-        # buffers are the slot's fixed upload targets): one launch per frame
-        self.captured = [rig.capture(self.out_size, params, ref_size=ref_size, out=o,
-                                     half_scale=half_scale)
-                         for rig, o in zip(self.rigs, self.outs)] if graphs else None
+        self.calpa = calpa
+        if calpa is not None:
+            from .steering import CalpaScratch, calpa_device
+
+            if output != "float32":
+                raise ValueError("the CALPA pipeline streams float32")
+            self.scratch = [CalpaScratch(rig, self.out_size) for rig in self.rigs]
+            self._calpa_fn = [
+                (lambda rig=rig, o=o, sc=sc: calpa_device(rig, self.out_size, calpa,
+                                                         ref_size=ref_size, out=o, scratch=sc))
+                for rig, o, sc in zip(self.rigs, self.outs, self.scratch)]
+            self.captured = [_capture(rig, fn, o) for rig, fn, o in
+                             zip(self.rigs, self._calpa_fn, self.outs)] if graphs else None
+        else:
+            # per slot, the reconstruction recorded once as a CUDA graph (its frame
+            # buffers are the slot's fixed upload targets): one launch per frame
+            self.captured = [rig.capture(self.out_size, params, ref_size=ref_size, out=o,
+                                         half_scale=half_scale)
+                             for rig, o in zip(self.rigs, self.outs)] if graphs else None
         self.s_in = torch.cuda.Stream(self.device)
         self.s_comp = [torch.cuda.Stream(self.device) for _ in range(slots)]
         self.s_out = torch.cuda.Stream(self.device)
@@ -86,6 +124,8 @@ class FramePipeline:
                 s_comp.wait_event(self.ev_out[k])  # output slot downloaded
             if self.captured:
                 self.captured[k].replay()
+            elif self.calpa is not None:
+                self._calpa_fn[k]()
             else:
                 self.rigs[k].reconstruct(self.out_size, self.params, ref_size=self.ref_size,
                                          out=self.outs[k], stream=s_comp,

@@ -99,22 +99,93 @@ def auto_gradient_scale(values: torch.Tensor) -> float:
     return s if s > 0 else 1.0
 
 
-def compute_steering_field(grads, params: AdaptiveParams, gradient_scale: float = 1.0) -> SteeringField:
-    """Steering field for every output pixel (hdr_steering_field)."""
+def gradient_scale_device(values: torch.Tensor, out: Optional[torch.Tensor] = None,
+                          workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The gradient scale (steering.py:206-211) as a one-element float64 device
+    tensor, computed without a host round trip (hdr_gradient_scale: numpy's
+    linear 99.5th percentile of |finite values|, 1.0 if none or 0)."""
+    v = values.contiguous().float().reshape(-1)
+    dev = v.device
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dev)
+    if workspace is None:
+        nb = ctypes.c_size_t()
+        N.check(N.lib().hdr_gradient_scale_workspace_bytes(ctypes.byref(nb)),
+                "hdr_gradient_scale_workspace_bytes")
+        workspace = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev)
+    N.check(N.lib().hdr_gradient_scale(v.data_ptr(), v.numel(), 0.995, out.data_ptr(),
+                                       workspace.data_ptr(), workspace.numel(), st.cuda_stream),
+            "hdr_gradient_scale")
+    return out
+
+
+def compute_steering_field(grads, params: AdaptiveParams, gradient_scale=1.0,
+                           out: Optional[SteeringField] = None) -> SteeringField:
+    """Steering field for every output pixel (hdr_steering_field); the scale
+    may be a float or a one-element device tensor (no host round trip)."""
     gx, gy = (g.contiguous().float() for g in grads)
+    h, w = gx.shape
+    if out is None:
+        out = SteeringField(*(torch.empty((h, w), dtype=torch.float64, device=gx.device)
+                              for _ in range(3)))
+    theta, sigma, gamma = out.theta, out.sigma, out.gamma
+    st = torch.cuda.current_stream(gx.device)
+    if isinstance(gradient_scale, torch.Tensor):
+        N.check(N.lib().hdr_steering_field_devscale(
+            gx.data_ptr(), gy.data_ptr(), w, h, params.gradient_window, float(params.lambda1),
+            float(params.lambda2), float(params.alpha), float(params.sigma_max),
+            gradient_scale.data_ptr(), theta.data_ptr(), sigma.data_ptr(), gamma.data_ptr(),
+            st.cuda_stream), "hdr_steering_field_devscale")
+        return out
     scale = float(gradient_scale)
     if scale <= 0 or not math.isfinite(scale):
         raise ValueError(f"gradient_scale must be positive, got {gradient_scale}")
-    h, w = gx.shape
-    theta, sigma, gamma = (torch.empty((h, w), dtype=torch.float64, device=gx.device)
-                           for _ in range(3))
-    st = torch.cuda.current_stream(gx.device)
     N.check(N.lib().hdr_steering_field(
         gx.data_ptr(), gy.data_ptr(), w, h, params.gradient_window, float(params.lambda1),
         float(params.lambda2), float(params.alpha), float(params.sigma_max), scale,
         theta.data_ptr(), sigma.data_ptr(), gamma.data_ptr(), st.cuda_stream),
         "hdr_steering_field")
-    return SteeringField(theta, sigma, gamma)
+    return out
+
+
+class CalpaScratch:
+    """Preallocated device buffers of one all-device CALPA frame (first-pass
+    outputs, steering field, scale, quantile workspace): calpa_device needs
+    no allocation, so it can be captured in a CUDA graph."""
+
+    def __init__(self, rig, out_size):
+        out_w, out_h = int(out_size[0]), int(out_size[1])
+        dev = rig.device
+        self.first = rig.allocate_outputs((out_w, out_h), want_grad=True, raw_value=True)
+        self.field = SteeringField(*(torch.empty((out_h, out_w), dtype=torch.float64, device=dev)
+                                     for _ in range(3)))
+        self.scale = torch.empty(1, dtype=torch.float64, device=dev)
+        nb = ctypes.c_size_t()
+        N.check(N.lib().hdr_gradient_scale_workspace_bytes(ctypes.byref(nb)),
+                "hdr_gradient_scale_workspace_bytes")
+        self.qws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+
+
+def calpa_device(rig, out_size, params: AdaptiveParams, ref_size=None, out=None,
+                 scratch: Optional[CalpaScratch] = None):
+    """calpa_reconstruct (steering.py:214-248, shared steering) entirely on the
+    device and stream-ordered: isotropic G pass, device gradient scale,
+    steering field, steered pass.  Returns the output dict (``rgb``)."""
+    if not params.share_steering:
+        raise ValueError("calpa_device implements the shared-steering mode")
+    base = params.base
+    sc = scratch if scratch is not None else CalpaScratch(rig, out_size)
+    rig.reconstruct(out_size, base, ref_size=ref_size, out=sc.first)
+    g = int(ColorChannel.G)
+    grads = (sc.first["grad"][g, 0], sc.first["grad"][g, 1])
+    if params.gradient_scale:
+        scale = params.gradient_scale
+    else:
+        scale = gradient_scale_device(sc.first["value"][g], out=sc.scale, workspace=sc.qws)
+    fld = compute_steering_field(grads, params, scale, out=sc.field)
+    return rig.reconstruct_steered(out_size, base, (fld.theta, fld.sigma, fld.gamma),
+                                   ref_size=ref_size, out=out)
 
 
 def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
@@ -130,10 +201,10 @@ def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
         return compute_steering_field((gx, gy), params, scale)
 
     if params.share_steering:
-        fld = field_for(ColorChannel.G)
-        out = rig.reconstruct_steered(out_size, base, (fld.theta, fld.sigma, fld.gamma),
-                                      ref_size=ref_size)
+        sc = CalpaScratch(rig, out_size)
+        out = calpa_device(rig, out_size, params, ref_size=ref_size, scratch=sc)
         img = HDRImage(to_host(out["rgb"]))
+        fld = sc.field
     else:
         out_w, out_h = out_size
         planes = np.empty((out_h, out_w, 3), np.float32)

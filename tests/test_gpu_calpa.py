@@ -7,6 +7,7 @@ import torch
 
 import paper_1308_4908_b200 as hl
 from golden_cases import calpa_names, load
+from paper_1308_4908_b200 import simulate as sim
 from oracle import compare, oracle
 
 pytestmark = pytest.mark.gpu
@@ -72,3 +73,53 @@ def test_calpa_without_adaptation_equals_lpa(cuda):
     iso = hl.reconstruct_frame(raw, out_size, ap.base)
     s = compare.summary(eq.data, iso.data)
     assert s["nan_map_equal"] and s["max"] < 1e-5
+
+
+@pytest.mark.parametrize("case", ["random", "ties", "nan_inf", "all_nan", "zeros", "single"])
+def test_device_gradient_scale_equals_numpy_percentile(cuda, case):
+    """hdr_gradient_scale: np.percentile(|finite|, 99.5) (numpy's linear
+    interpolation, steering.py:206-211) exactly, 1.0 for none / zero."""
+    import torch
+
+    from paper_1308_4908_b200.steering import gradient_scale_device
+
+    rng = np.random.default_rng(7)
+    v = {"random": rng.normal(0, 1e4, 1_000_003),
+         "ties": rng.integers(-50, 50, 300_001).astype(float),
+         "nan_inf": np.where(rng.random(200_000) < 0.1, np.nan, rng.normal(0, 3e5, 200_000)),
+         "all_nan": np.full(1000, np.nan), "zeros": np.zeros(5000), "single": np.array([-3.5])}[case]
+    v = v.astype(np.float32)
+    if case == "nan_inf":
+        v[::977] = np.inf
+    got = float(gradient_scale_device(torch.from_numpy(v).to(cuda)).item())
+    f = np.abs(v[np.isfinite(v)].astype(np.float64))
+    want = float(np.percentile(f, 99.5)) if f.size else 1.0
+    want = want if want > 0 else 1.0
+    assert got == want, (got, want)
+
+
+def test_calpa_pipeline_equals_host_api(cuda):
+    """FramePipeline(calpa=...): the all-device CALPA graph per slot streams the
+    same float32 frames as calpa_reconstruct."""
+    import torch
+
+    from paper_1308_4908_b200.engine import DeviceRig
+    from paper_1308_4908_b200.pipeline import FramePipeline
+
+    W, H = 96, 64
+    gt = sim.hdr_chart(W, H)
+    rig = sim.baseline_rig("aligned", W, H, seed=9)
+    ap = hl.AdaptiveParams(base=hl.ReconstructionParams(order=1))
+    sets = [[torch.from_numpy(f.data.view(np.int16)).pin_memory() for f in
+             sim.simulate_rig(gt, sim.RigSpec(rig.sensors, rig.noise, rig.sensor_sizes, seed=s))]
+            for s in (1, 2, 3)]
+    pipe = FramePipeline(rig.sensors, rig.calibrations(), [(H, W)] * 3, (W, H), ap.base,
+                         device=cuda, calpa=ap)
+    outs = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in sets]
+    for hs, o in zip(sets, outs):
+        pipe.submit(hs, o)
+    pipe.synchronize()
+    for hs, o in zip(sets, outs):
+        dev = DeviceRig.from_device([t.to(cuda) for t in hs], rig.sensors, rig.calibrations())
+        want = hl.calpa_reconstruct(dev, (W, H), ap).data
+        assert np.array_equal(o.numpy(), want, equal_nan=True)
