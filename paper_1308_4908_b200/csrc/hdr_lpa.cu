@@ -631,10 +631,10 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
         const double ex = (TW - 1) * P.sx, ey = (TH - 1) * P.sy;
         const double wx = fabs(d.N[0]) * ex + fabs(d.N[1]) * ey + 2.0 * fastR * d.nrow0;
         const double wy = fabs(d.N[2]) * ex + fabs(d.N[3]) * ey + 2.0 * fastR * d.nrow1;
-        // + 2 for floor/ceil of the bbox ends, + 7 / + 1 for aligning the origin
-        // down to a multiple of 8 columns / 2 rows
-        int rw = (int)ceil(wx) + 2 + 7, rh = (int)ceil(wy) + 2 + 1;
-        rw = (rw + 7) & ~7;  // TMA box inner extent: multiple of 16 bytes
+        // + 2 for floor/ceil of the bbox ends, + 3 / + 1 for aligning the origin
+        // down to a multiple of 4 columns / 2 rows
+        int rw = (int)ceil(wx) + 2 + 3, rh = (int)ceil(wy) + 2 + 1;
+        rw = (rw + 3) & ~3;  // TMA box inner extent (rw floats): multiple of 16 bytes
         rh += rh & 1;
         d.rw = rw;
         d.rh = rh;

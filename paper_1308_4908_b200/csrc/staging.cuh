@@ -91,11 +91,13 @@ __device__ __forceinline__ bool region_origin(const DevSensor &S, const DevParam
         xmax = max(xmax, xhi);
         ymax = max(ymax, yhi);
     }
-    // x: multiple of 8 elements -- a TMA tile copy must start on a 16-byte
-    // boundary of the row (measured: unaligned starts raise an illegal-
-    // instruction fault; scripts/probes/tma_probe.cu).  Both even, so the
-    // Bayer phase of a staged pixel equals the parity of its coordinates.
-    ox = xmin & ~7;
+    // x: a TMA tile copy must start on a 16-byte boundary of the row
+    // (measured: unaligned starts raise an illegal-instruction fault;
+    // scripts/probes/tma_probe.cu).  The phase planes' x coordinate is in
+    // floats (float2 elements: the sensor column; float4 merged planes: twice
+    // it), so 4 columns are 16 bytes.  Both even, so the Bayer phase of a
+    // staged pixel equals the parity of its coordinates.
+    ox = xmin & ~3;
     oy = ymin & ~1;
     // true: every window of every pixel of the tile lies inside the region
     return xmax < ox + S.rw && ymax < oy + S.rh;
