@@ -789,8 +789,6 @@ def run_ours(args, wl, world, rank, local):
     # synchronous, one frame at a time
     e2e_api = None
     if not args.no_api_e2e:
-        from paper_1308_4908_b200 import simulate as sim
-
         rig_h, frames_h = _host_frames(wl, seed=1000 * rank)
         for _ in range(2):
             hl.reconstruct_frame(hl.frames_to_samples(frames_h, rig_h.sensors, cals),

@@ -21,7 +21,7 @@ import click
 import numpy as np
 
 from . import __version__
-from .lpa import ReconstructionParams, reconstruct_frame
+from .lpa import reconstruct_frame
 from .pnm import PnmParseError, read_pgm16, write_pfm, write_pgm16
 from .radiometry import ConfigurationError, frames_to_samples
 from .rig import ConfigError, load_rig

@@ -12,13 +12,13 @@ GPU (hdr_simulate_sensor; the multi-megapixel bench and video frames).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import numpy as np
 
 from .bayer import BayerPattern, ColorChannel, channel_map
-from .images import CFAImage, FloatFrame, HDRImage
+from .images import CFAImage, HDRImage
 from .radiometry import NoiseCalibration, SensorConfig
 
 # Kodak KAI-04050 profile used throughout the reference's tests and configs
