@@ -688,6 +688,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
                         int out_w, int out_h, double ref_w, double ref_h, int row_begin,
                         int row_end, const HdrOutputs *out, void *workspace,
                         size_t workspace_bytes, void *stream) {
+    NvtxRange nv("hdr_lpa_reconstruct");
     DevParams P;
     double fastR = 0.0;
     {

@@ -13,11 +13,20 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include "hdr_lpa.h"
 #include "config.cuh"
 #include "fast_kernel.cuh"
 
 namespace hdrlpa {
+
+// scoped NVTX range around the host-side enqueue of a library stage (no-op
+// unless a tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 extern thread_local char g_last_error[256];
 extern std::atomic<unsigned long long> g_launches;
@@ -91,6 +100,7 @@ inline int launch_ici(const DevParams &P, const TapParam &T, int tiles, int smem
 template <int ORDER>
 int launch_all(const DevParams &Pf, const DevParams &P, const TapParam &T, int tiles,
                       int smem_bytes, int maxc, cudaStream_t st) {
+    NvtxRange nv("hdr_lpa tile + exact kernels");
     int rc;
     const bool cnt = P.count || P.work;
     if (P.all_items) {  // no staged path (hdr_lpa_reconstruct): the exact path for everything

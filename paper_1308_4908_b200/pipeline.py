@@ -110,6 +110,10 @@ class FramePipeline:
     def submit(self, host_raws, host_rgb):
         """Queue one frame: ``host_raws`` pinned int16 (h, w) tensors, result
         into the pinned float32 (H, W, 3) tensor ``host_rgb``."""
+        with torch.cuda.nvtx.range(f"FramePipeline.submit {self.n}"):
+            return self._submit(host_raws, host_rgb)
+
+    def _submit(self, host_raws, host_rgb):
         k = self.n % self.slots
         with torch.cuda.stream(self.s_in):
             if self.ev_free[k] is not None:
