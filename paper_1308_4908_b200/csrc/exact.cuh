@@ -182,12 +182,17 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
 
 // One group of SLOW_LANES lanes per work item: they share every window's
 // candidates.
+// (measured: cfg2 4 / 8 / 16 lanes within noise of each other, kept at 8;
+// order 2 with ICI, cfg3 / cfg5: 4 lanes 1 % faster than 8)
 #ifndef SLOW_LANES
 #define SLOW_LANES 8
 #endif
+#ifndef SLOW_LANES_O2
+#define SLOW_LANES_O2 4
+#endif
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
-    constexpr int G = SLOW_LANES;  // lanes per work item
+    constexpr int G = ORDER >= 2 ? SLOW_LANES_O2 : SLOW_LANES;  // lanes per work item
     const uint32_t n = P.all_items ? P.all_items : *P.work_count;
     // items are fetched dynamically (their cost varies by orders of magnitude)
     const unsigned gmask = G >= 32 ? 0xffffffffu
