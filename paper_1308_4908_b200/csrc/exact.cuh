@@ -110,7 +110,8 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
                 sweep.rows(c, k, P.r[c][k], P.r2[c][k], V);
             }
             tk = V.T;
-            var_k = V.v;
+            var_k = (double)V.v;
+            if (HDR_VAR32 && !(var_k >= 1e-30 && var_k <= 1e37)) return FIT_AMBIG;
         } else {
             var_k = fit_variance<ORDER, EXACT>(P, c, k, sweep, fit.g, &tk);
         }
@@ -121,7 +122,8 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
         // bounds is decided by the exact path, so scale indices stay exact
         const float ek =
             EXACT ? 0.f
-                  : __double2float_ru(2.0 * FAST_EPS * (double)tk + P.gamma * sd * ICI_SD_EPS);
+                  : __double2float_ru(2.0 * FAST_EPS * (double)tk +
+                                      P.gamma * sd * (ICI_SD_EPS + VAR32_EPS_TERM * (count_k + 3)));
         if (k == 0) {
             S().L = lo;
             S().U = hi;

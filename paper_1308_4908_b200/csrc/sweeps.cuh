@@ -497,6 +497,28 @@ struct RowMoments {
     }
 };
 
+// The fast path's ICI variance v = sum t (phi.g)^2 is a sum of nonnegative
+// terms, accumulated in float32 (HDR_VAR32, default): its relative error is
+// at most (n + 3) 2^-24 for n nonzero terms (the FMA rounding per term, plus
+// fl32(phi.g), its square and t), i.e. (n + 3) 2^-25 on the standard
+// deviation, which ici() adds to the interval error bounds (n = the scale's
+// sample count).  Values outside [1e-30, 1e37] go to the exact path.
+#ifndef HDR_VAR32
+#define HDR_VAR32 1
+#endif
+#if HDR_VAR32
+using var_t = float;
+__device__ __forceinline__ void var_add(float &v, float t32, double, float pf) {
+    v = fmaf(t32, pf * pf, v);
+}
+#else
+using var_t = double;
+__device__ __forceinline__ void var_add(double &v, float t32, double pg, float) {
+    v = fma((double)t32, pg * pg, v);
+}
+#endif
+constexpr double VAR32_EPS_TERM = HDR_VAR32 ? 3.1e-8 : 0.0;  // (1.03 * 2^-25 per term on sd)
+
 // Row-factored variance sweep (ICI, fast path): phi.g = c0(dy) + dx (c1(dy) + g3 dx).
 // Also accumulates T = sum w |phi.g| |y| (fp32): the sharp precision bound of
 // c0 (fit_precise_sharp).
@@ -505,7 +527,8 @@ struct RowVariance {
     const double *g;
     float hl;
     bool sig;
-    double v, c0, c1;
+    var_t v;
+    double c0, c1;
     float T;
     __device__ __forceinline__ void begin_row(double dy, double dyy) {
         c0 = g[0];
@@ -523,13 +546,14 @@ struct RowVariance {
     __device__ __forceinline__ void sample(bool ok, double y, float iv, double dx, double, double,
                                            double, float d2f, bool = true) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
-        const double t = (double)(sig ? W * W : W * W * iv);
+        const float t32 = sig ? W * W : W * W * iv;
         double pg = c0;
         if (ORDER == 1) pg = fma(dx, c1, c0);
         if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
         if (ok) {
-            v = fma(t, pg * pg, v);
-            T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+            const float pf = (float)pg;
+            var_add(v, t32, pg, pf);
+            T = fmaf(W * iv, fabsf(pf) * fabsf((float)y), T);
         }
     }
     __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx,
@@ -546,19 +570,21 @@ struct RowVariance {
         double pg = c0;
         if (ORDER == 1) pg = fma(dx, c1, c0);
         if (ORDER == 2) pg = fma(dx, fma(g[3], dx, c1), c0);
-        v = fma((double)t32, pg * pg, v);
-        T = fmaf(W * e.y, fabsf((float)pg) * fabsf(e.x), T);
+        const float pf = (float)pg;
+        var_add(v, t32, pg, pf);
+        T = fmaf(W * e.y, fabsf(pf) * fabsf(e.x), T);
     }
     __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
-        const double t = (double)(sig ? W * W : W * W * iv);
+        const float t32 = sig ? W * W : W * W * iv;
         double pg = g[0];
         if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
         if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
         // W = 0 when !ok: both sums take zero contributions (no branch)
-        v = fma(t, pg * pg, v);
-        T = fmaf(W * iv, fabsf((float)pg) * fabsf((float)y), T);
+        const float pf = (float)pg;
+        var_add(v, t32, pg, pf);
+        T = fmaf(W * iv, fabsf(pf) * fabsf((float)y), T);
     }
 };
 
