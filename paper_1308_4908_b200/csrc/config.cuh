@@ -64,4 +64,15 @@ struct NC {
     static constexpr int P = (ORDER + 1) * (ORDER + 2) / 2;
 };
 
+// shared-memory helpers (32-bit shared-window addresses)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+// 8-byte shared-memory load at a 32-bit shared address (row-tap samples)
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
 }  // namespace hdrlpa

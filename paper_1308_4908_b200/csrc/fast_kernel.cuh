@@ -21,11 +21,6 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t a) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
-__device__ __forceinline__ float2 lds_f2(uint32_t a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-    return v;
-}
 
 // the pixel's own position in each sensor's staged phase planes (origins are
 // even), computed once per pixel for all channels
@@ -205,7 +200,7 @@ __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, cons
     }
 }
 
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER, bool MRGS, bool ICISM>
+template <int ORDER, bool ICI, int MAXC, int PAT, int RT, bool STEER, bool MRGS, bool ICISM>
 __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned char *sm,
                                              const unsigned char *taps, int tcol, int trow,
                                              const int (*org)[2], bool tile_covered,
@@ -366,7 +361,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
 // (no count/work output planes requested), 3 / 4 the same over co-sited
 // merged samples (radiance_merge_kernel)
 // MRGS: CALPA's steered pass over co-sited merged planes (ORDER >= 1)
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT = false, bool STEER = false,
+template <int ORDER, bool ICI, int MAXC, int PAT, int RT = 0, bool STEER = false,
           bool MRGS = false, bool ICISM = false>
 // Per-sensor tap kernels are held to 80 registers: 3 CTAs per SM beat 2 by
 // ~8% on cfg2 and 4 (64 registers) measured ~2% slower than 3.

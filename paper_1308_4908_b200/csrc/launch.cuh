@@ -38,7 +38,7 @@ extern thread_local cudaEvent_t g_timer_ev[2];
 extern thread_local bool g_timer_recorded;
 bool timer_active(cudaStream_t st);
 
-template <int ORDER, bool ICI, int MAXC, int PAT = 0, bool RT = false, bool STEER = false,
+template <int ORDER, bool ICI, int MAXC, int PAT = 0, int RT = 0, bool STEER = false,
           bool MRGS = false, bool ICISM = false>
 inline int launch_fast(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                        cudaStream_t st) {
@@ -69,7 +69,7 @@ inline int launch_fast(const DevParams &P, const TapParam &T, int tiles, int sme
 
 
 // CTAs per SM a fast kernel reaches with `smem_bytes` of dynamic shared memory
-template <int ORDER, bool ICI, int MAXC, int PAT, bool RT, bool STEER, bool MRGS, bool ICISM>
+template <int ORDER, bool ICI, int MAXC, int PAT, int RT, bool STEER, bool MRGS, bool ICISM>
 inline int fast_occupancy(int smem_bytes) {
     const void *fn = (const void *)lpa_fast_kernel<ORDER, ICI, MAXC, PAT, RT, STEER, MRGS, ICISM>;
     if (set_smem_attr(fn, smem_bytes) != HDR_OK) return 0;
@@ -82,7 +82,7 @@ inline int fast_occupancy(int smem_bytes) {
 // ICI kernels: the variant with the ICI state in shared memory (no spills)
 // whenever its extra static shared memory costs no CTA per SM, else the
 // register variant (e.g. 4-sensor rigs, whose staged planes fill the SM).
-template <int ORDER, int MAXC, bool RT>
+template <int ORDER, int MAXC, int RT>
 inline int launch_ici(const DevParams &P, const TapParam &T, int tiles, int smem_bytes,
                       cudaStream_t st) {
     const int occ_sm = fast_occupancy<ORDER, true, MAXC, 0, RT, false, false, true>(smem_bytes);
@@ -117,15 +117,18 @@ int launch_all(const DevParams &Pf, const DevParams &P, const TapParam &T, int t
     else if (P.pat)
         rc = cnt ? launch_fast<ORDER, false, 4, 1>(P, T, tiles, smem_bytes, st)
                  : launch_fast<ORDER, false, 4, 2>(P, T, tiles, smem_bytes, st);
+    // row taps (every separable sensor tapped; MAXC only sizes the column
+    // sweep of separable sensors, so it is irrelevant here): RT 1 counts the
+    // valid samples per tap for the count / work planes, RT 2 counts taps
     else if (P.rt && P.n_scales > 1)
-        rc = maxc <= 6 ? launch_ici<ORDER, 6, true>(P, T, tiles, smem_bytes, st)
-                       : launch_ici<ORDER, 8, true>(P, T, tiles, smem_bytes, st);
+        rc = cnt ? launch_ici<ORDER, 6, 1>(P, T, tiles, smem_bytes, st)
+                 : launch_ici<ORDER, 6, 2>(P, T, tiles, smem_bytes, st);
     else if (P.rt)
-        rc = maxc <= 4 ? launch_fast<ORDER, false, 4, 0, true>(P, T, tiles, smem_bytes, st)
-                       : launch_fast<ORDER, false, 8, 0, true>(P, T, tiles, smem_bytes, st);
+        rc = cnt ? launch_fast<ORDER, false, 4, 0, 1>(P, T, tiles, smem_bytes, st)
+                 : launch_fast<ORDER, false, 4, 0, 2>(P, T, tiles, smem_bytes, st);
     else if (P.n_scales > 1)
-        rc = maxc <= 6 ? launch_ici<ORDER, 6, false>(P, T, tiles, smem_bytes, st)
-                       : launch_ici<ORDER, 8, false>(P, T, tiles, smem_bytes, st);
+        rc = maxc <= 6 ? launch_ici<ORDER, 6, 0>(P, T, tiles, smem_bytes, st)
+                       : launch_ici<ORDER, 8, 0>(P, T, tiles, smem_bytes, st);
     else
         rc = maxc <= 4 ? launch_fast<ORDER, false, 4>(P, T, tiles, smem_bytes, st)
                        : launch_fast<ORDER, false, 8>(P, T, tiles, smem_bytes, st);

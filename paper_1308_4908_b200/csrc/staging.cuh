@@ -9,9 +9,6 @@ namespace hdrlpa {
 // ---------------------------------------------------------------------------
 // Fast path: persistent CTAs, double-buffered TMA staging of the raw tiles.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }

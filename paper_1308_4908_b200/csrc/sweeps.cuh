@@ -109,6 +109,7 @@ struct PerSample {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
     double dy_, dyy_;  // the row's offset (row taps pass it to begin_row)
+    __device__ __forceinline__ void row_count(int) {}  // the body counts (ok flag)
     __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx, double dxx,
                                              float d2f, bool inner = true) {
         begin_row(dy, dyy);
@@ -123,7 +124,11 @@ struct PerSample {
 // MRG4: the staged planes are the co-sited merged float4 planes
 // (sum 1/den, sum f_hat/den, sum |f_hat|/den, count; one "sensor"), and the
 // policy takes them through sample4() (CALPA's steered pass on co-sited rigs).
-template <int MAXC, bool BRANCHY, bool RT = false, bool MRG4 = false>
+// RT: 0 no row taps; 1 row taps counting the valid samples per tap; 2 row taps
+// counting every tap of a row (no count / work planes requested: an upper
+// bound is enough, the solve's positive-definiteness and condition tests
+// imply count >= p)
+template <int MAXC, bool BRANCHY, int RT = 0, bool MRG4 = false>
 struct TileSweep {
     const DevParams &P;
     const unsigned char *sm;
@@ -170,19 +175,27 @@ struct TileSweep {
         const int pw = S.rw >> 1;
         // the pixel's anchor: its own sensor pixel (sx = 1) or cell (sx = 1/2)
         const int ax = px >> P.rt_shift, ay = py >> P.rt_shift;
-        const unsigned char *vb = sm + S.off_vi +
-                                  8 * (((ay - org[s][1]) >> 1) * pw + ((ax - org[s][0]) >> 1));
+        // 32-bit shared address of the anchor's sample; a tap's packed word
+        // holds its byte offset as 24-bit two's complement under kmin << 24,
+        // so (vb + word) mod 2^24 is the sample's address (shared addresses
+        // are < 2^24) and kmin <= kin is word < (kin + 1) << 24
+        const uint32_t vb = smem_addr(sm) + S.off_vi +
+                            8 * (((ay - org[s][1]) >> 1) * pw + ((ax - org[s][0]) >> 1));
+        const uint32_t klim = (uint32_t)(kin + 1) << 24;
         for (int ri = rr.x; ri < rr.x + rr.y; ++ri) {
             const double dy = rdy[ri], dyy = dy * dy;
             const uint32_t fn = rfn[ri];
             const RowTap *t = taps + (fn & ((1u << RT_ROW_N_SHIFT) - 1));
             const RowTap *te = t + (fn >> RT_ROW_N_SHIFT);
+            int n;  // the row's sample count (RT 1) or tap count (RT 2)
             {  // every row run holds >= 1 tap: the first one opens the row's sums
                 const RowTap T = *t;
-                HDR_BOUNDS(P, vb + rt_off(T.off) >= sm + S.off_vi &&
-                                  vb + rt_off(T.off) + 8 <= sm + S.off_vi + S.rw * S.rh * 8);
-                const float2 e = *(const float2 *)(vb + rt_off(T.off));
-                pol.first_rt(dy, dyy, e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
+                const uint32_t a = (vb + (uint32_t)T.off) & 0xFFFFFFu;
+                HDR_BOUNDS(P, a >= smem_addr(sm) + S.off_vi &&
+                                  a + 8 <= smem_addr(sm) + S.off_vi + S.rw * S.rh * 8);
+                const float2 e = lds_f2(a);
+                pol.first_rt(dy, dyy, e, T.dx, T.dx * T.dx, T.d2f, (uint32_t)T.off < klim);
+                if constexpr (RT == 1) n = e.y > 0.f ? 1 : 0;
             }
 #ifndef HDR_RT_UNROLL
 #define HDR_RT_UNROLL 1
@@ -191,11 +204,15 @@ struct TileSweep {
 #pragma unroll kRtUnroll
             for (++t; t < te; ++t) {
                 const RowTap T = *t;
-                HDR_BOUNDS(P, vb + rt_off(T.off) >= sm + S.off_vi &&
-                                  vb + rt_off(T.off) + 8 <= sm + S.off_vi + S.rw * S.rh * 8);
-                const float2 e = *(const float2 *)(vb + rt_off(T.off));
-                pol.sample_rt(e, T.dx, T.dx * T.dx, T.d2f, rt_kmin(T.off) <= kin);
+                const uint32_t a = (vb + (uint32_t)T.off) & 0xFFFFFFu;
+                HDR_BOUNDS(P, a >= smem_addr(sm) + S.off_vi &&
+                                  a + 8 <= smem_addr(sm) + S.off_vi + S.rw * S.rh * 8);
+                const float2 e = lds_f2(a);
+                pol.sample_rt(e, T.dx, T.dx * T.dx, T.d2f, (uint32_t)T.off < klim);
+                if constexpr (RT == 1) n += e.y > 0.f ? 1 : 0;
             }
+            if constexpr (RT != 1) n = (int)(fn >> RT_ROW_N_SHIFT);
+            pol.row_count(n);
             pol.end_row(dy, dyy);
         }
     }
@@ -408,8 +425,9 @@ struct RowMoments {
         T[0] += wy;
 #pragma unroll
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
-        cnt += e.y > 0.f ? 1 : 0;
     }
+    // row taps: the sweep counts the row (row_count, before end_row)
+    __device__ __forceinline__ void row_count(int n) { cnt = n; }
     // the first tap of a row run: opens the row sums (no zeroing)
     __device__ __forceinline__ void first_rt(double, double, float2 e, double dx, double dxx,
                                              float d2f, bool = true) {
@@ -430,7 +448,6 @@ struct RowMoments {
         T[0] = wy;
 #pragma unroll
         for (int n = 1; n <= ORDER; ++n) T[n] = wy * px[n];
-        cnt = e.y > 0.f ? 1 : 0;
     }
     // co-sited merged sample: w = W sum 1/den, wy = W sum f_hat/den (fp32),
     // the bound's sum w |y| from W sum |f_hat|/den, count = the sensors' samples
@@ -490,7 +507,7 @@ struct RowMoments {
     }
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
-        const float w = ok ? ex2_approx(-hl * d2f) * iv : 0.f;
+        const float w = ex2_approx(-hl * d2f) * (ok ? iv : 0.f);
         const double y = ok ? v : 0.0;
         acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
         acc.add_fast((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
@@ -542,6 +559,7 @@ struct RowVariance {
             c1 += g[4] * dy;
         }
     }
+    __device__ __forceinline__ void row_count(int) {}
     __device__ __forceinline__ void end_row(double, double) {}
     __device__ __forceinline__ void sample(bool ok, double y, float iv, double dx, double, double,
                                            double, float d2f, bool = true) {
@@ -576,11 +594,11 @@ struct RowVariance {
     }
     __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
-        const float W = ok ? ex2_approx(-hl * d2f) : 0.f;
+        const float W = ex2_approx(-hl * d2f) * (ok ? 1.f : 0.f);
         const float t32 = sig ? W * W : W * W * iv;
         double pg = g[0];
         if (ORDER >= 1) pg += dx * g[1] + dy * g[2];
-        if (ORDER >= 2) pg += dxx * g[3] + __dmul_rn(dx, dy) * g[4] + dyy * g[5];
+        if (ORDER >= 2) pg += dxx * g[3] + (dx * dy) * g[4] + dyy * g[5];  // dx*dy: shared with the moments
         // W = 0 when !ok: both sums take zero contributions (no branch)
         const float pf = (float)pg;
         var_add(v, t32, pg, pf);
@@ -603,6 +621,7 @@ struct FusedVarMom {
         M.end_row(dy, dyy);
         V.end_row(dy, dyy);
     }
+    __device__ __forceinline__ void row_count(int n) { M.row_count(n); }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
                                            double dxx, double dyy, float d2f, bool inner) {
         M.sample(ok, v, iv, dx, dy, dxx, dyy, d2f);
@@ -633,7 +652,7 @@ template <class Sweep>
 struct HasRows {
     static constexpr bool value = false;
 };
-template <int MAXC, bool BRANCHY, bool RT, bool MRG4>
+template <int MAXC, bool BRANCHY, int RT, bool MRG4>
 struct HasRows<TileSweep<MAXC, BRANCHY, RT, MRG4>> {
     static constexpr bool value = true;
 };

@@ -11,5 +11,5 @@ sys.path.insert(0, ".")
 from paper_1308_4908_b200 import _native as N
 N.compile_library(Path("exp") / f"lib_{sys.argv[1]}.so", sys.argv[2].split(), verbose_ptxas=True)
 PY
-  echo "$n: $(grep -A2 'lpa_fast_kernelILi2ELb1ELi6ELi0ELb1E' exp/ptxas_$n.log | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
+  echo "$n: $(grep -A2 'lpa_fast_kernelILi2ELb1ELi6ELi0ELi2E' exp/ptxas_$n.log | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
 done
