@@ -172,11 +172,13 @@ struct RowAniso {
         const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
         m.sample4(ok, e, dx, dxx, ex2_approx(-q2));
     }
+    template <bool CNT = true>
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float, bool = true) {
         const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
-        m.general(ok, v, iv, dx, dy, dxx, dyy, q2);
+        m.template general<CNT>(ok, v, iv, dx, dy, dxx, dyy, q2);
     }
+    __device__ __forceinline__ void count_add(int n) { m.count_add(n); }
 };
 
 template <int ORDER, class Sweep>

@@ -667,10 +667,12 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
     for (int s = 0; s < n_sensors; ++s) {
         DevSensor &d = P.s[s];
         d.off_vi = take(d.rw * d.rh * (P.merged ? 16 : 8));  // [4][rh/2][rw/2] float2 / float4
-        d.off_tx0 = take(d.rw * 8);
-        d.off_tx3 = take(d.rw * 8);
-        d.off_ty1 = take(d.rh * 8);
-        d.off_ty4 = take(d.rh * 8);
+        // coordinate tables (staging.cuh): separable X(x), Y(y); otherwise the
+        // interleaved partial products {T00 x, T10 x}, {T01 y, T11 y}
+        d.off_tx0 = take(d.rw * (d.separable ? 8 : 16));
+        d.off_tx3 = d.off_tx0;
+        d.off_ty1 = d.separable ? 0 : take(d.rh * 16);
+        d.off_ty4 = d.separable ? take(d.rh * 8) : 0;
     }
     P.buf_stride = smem;
     smem_bytes = P.plane_base + nbuf_for(P.pat) * P.buf_stride;

@@ -52,8 +52,9 @@ struct DevSensor {
     double2 *lut;             // exact (f_hat, 1/den) per raw value (scalar calibration)
     float2 *phase;            // global phase planes [4][phg][pwg] of (f_hat, 1/den) (workspace)
     int pwg, phg;             // their padded width (float2 elements) and height
-    int off_tx0, off_tx3;     // f64 tables fl(T00*x), fl(T10*x) over the region's columns
-    int off_ty1, off_ty4;     // f64 tables fl(T01*y), fl(T11*y) over the region's rows
+    int off_tx0, off_tx3;     // f64 column tables: X(x) (separable) or {fl(T00*x), fl(T10*x)}
+    int off_ty1, off_ty4;     // f64 row tables: Y(y) at off_ty4 (separable) or
+                              // {fl(T01*y), fl(T11*y)} at off_ty1 (off_tx3: unused, = off_tx0)
     float Tf[4];              // fp32 linear part (pre-test of rotated sensors)
 };
 

@@ -140,20 +140,24 @@ __device__ __forceinline__ void stage_tile(const DevParams &P, unsigned char *pb
             const int ox = org[s][0], oy = org[s][1];
             // separable sensors: tx0 = X(x) = fl(fl(T00*x) + T02), ty4 = Y(y)
             // (exact, since fl(T01*y) = fl(T10*x) = 0); otherwise the four
-            // partial products.
-            double *tx0t = (double *)(pb + S.off_tx0), *tx3t = (double *)(pb + S.off_tx3);
-            double *ty1t = (double *)(pb + S.off_ty1), *ty4t = (double *)(pb + S.off_ty4);
-            for (int i = lane; i < S.rw; i += 32) {
-                const double xd = (double)(ox + i);
-                const double a = __dmul_rn(S.T[0], xd);
-                tx0t[i] = S.separable ? __dadd_rn(a, S.T[2]) : a;
-                tx3t[i] = __dmul_rn(S.T[3], xd);
-            }
-            for (int i = lane; i < S.rh; i += 32) {
-                const double yd = (double)(oy + i);
-                const double bb = __dmul_rn(S.T[4], yd);
-                ty1t[i] = __dmul_rn(S.T[1], yd);
-                ty4t[i] = S.separable ? __dadd_rn(bb, S.T[5]) : bb;
+            // partial products, interleaved: {fl(T00 x), fl(T10 x)} per column
+            // at off_tx0, {fl(T01 y), fl(T11 y)} per row at off_ty1.
+            if (S.separable) {
+                double *tx0t = (double *)(pb + S.off_tx0), *ty4t = (double *)(pb + S.off_ty4);
+                for (int i = lane; i < S.rw; i += 32)
+                    tx0t[i] = __dadd_rn(__dmul_rn(S.T[0], (double)(ox + i)), S.T[2]);
+                for (int i = lane; i < S.rh; i += 32)
+                    ty4t[i] = __dadd_rn(__dmul_rn(S.T[4], (double)(oy + i)), S.T[5]);
+            } else {
+                double2 *txi = (double2 *)(pb + S.off_tx0), *tyi = (double2 *)(pb + S.off_ty1);
+                for (int i = lane; i < S.rw; i += 32) {
+                    const double xd = (double)(ox + i);
+                    txi[i] = make_double2(__dmul_rn(S.T[0], xd), __dmul_rn(S.T[3], xd));
+                }
+                for (int i = lane; i < S.rh; i += 32) {
+                    const double yd = (double)(oy + i);
+                    tyi[i] = make_double2(__dmul_rn(S.T[1], yd), __dmul_rn(S.T[4], yd));
+                }
             }
         }
         __syncwarp();

@@ -104,10 +104,12 @@ struct PerSample {
                                            double dxx, double dyy, float d2f, bool = true) {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
+    template <bool CNT = true>  // the body counts (ok flag) either way
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         body(ok, v, iv, dx, dy, dxx, dyy, d2f);
     }
+    __device__ __forceinline__ void count_add(int) {}
     double dy_, dyy_;  // the row's offset (row taps pass it to begin_row)
     __device__ __forceinline__ void row_count(int) {}  // the body counts (ok flag)
     __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx, double dxx,
@@ -305,8 +307,10 @@ struct TileSweep {
                     }
                 }
             } else {
-                const double *tx3 = (const double *)(sm + S.off_tx3);
-                const double *ty1 = (const double *)(sm + S.off_ty1);
+                // interleaved coordinate tables {fl(T00 x), fl(T10 x)} per column and
+                // {fl(T01 y), fl(T11 y)} per row (staging.cuh)
+                const double2 *txi = (const double2 *)(sm + S.off_tx0);
+                const double2 *tyi = (const double2 *)(sm + S.off_ty1);
                 const double T2 = S.T[2], T5 = S.T[5];
                 // sensor-space position of q relative to the bbox corner (fp32 pre-test)
                 const double u = qx() - T2, v = qy() - T5;
@@ -335,25 +339,30 @@ struct TileSweep {
                         x0 = max(x0, xs);
                         x0 += (x0 - xs) & 1;
                         const int ly = y - oy;
-                        const double t1y = ty1[ly], t4y = ty4[ly];
+                        const double2 ty = tyi[ly];  // (fl(T01 y), fl(T11 y))
                         const int rb = ph * plane + (ly >> 1) * pw - (ox >> 1);
                         // straight-line body (the chord pre-test leaves few candidates
                         // outside the disk): masked and outside samples take weight 0
-                        for (int x = x0; x <= x1; x += 2) {
-                            const int k = rb + (x >> 1);
-                            const int lx = x - ox;
-                            HDR_BOUNDS(P, k >= 0 && k < 4 * plane && lx >= 0 && lx < S.rw &&
+                        const int ncand = ((x1 - x0) >> 1) + 1;  // <= 0: empty chord
+                        const float2 *pe = vi + rb + (x0 >> 1);
+                        const double2 *pt = txi + (x0 - ox);
+                        for (int j = 0; j < ncand; ++j, ++pe, pt += 2) {
+                            HDR_BOUNDS(P, rb + (x0 >> 1) + j >= 0 && rb + (x0 >> 1) + j < 4 * plane &&
+                                              x0 - ox + 2 * j >= 0 && x0 - ox + 2 * j < S.rw &&
                                               ly >= 0 && ly < S.rh);
-                            const float2 e = vi[k];
-                            const double X = __dadd_rn(__dadd_rn(tx0[lx], t1y), T2);
-                            const double Y = __dadd_rn(__dadd_rn(tx3[lx], t4y), T5);
+                            const float2 e = *pe;
+                            const double2 tx = *pt;
+                            const double X = __dadd_rn(__dadd_rn(tx.x, ty.x), T2);
+                            const double Y = __dadd_rn(__dadd_rn(tx.y, ty.y), T5);
                             const double dx = __dsub_rn(X, qx()), dy = __dsub_rn(Y, qy());
                             const double dxx = __dmul_rn(dx, dx), dyy = __dmul_rn(dy, dy);
                             const double d2 = __dadd_rn(dxx, dyy);  // _kernels.py:160-162
                             const bool ok = (e.y > 0.f) && !(d2 > r2);
-                            pol.general(ok, (double)e.x, e.y, dx, dy, dxx, dyy, (float)d2,
-                                        d2 <= r2in);
+                            pol.template general<RT != 2>(ok, (double)e.x, e.y, dx, dy, dxx,
+                                                          dyy, (float)d2, d2 <= r2in);
                         }
+                        // RT 2: the row's candidates as its count (an upper bound)
+                        if constexpr (RT == 2) pol.count_add(ncand > 0 ? ncand : 0);
                     }
                 }
             }
@@ -505,13 +514,16 @@ struct RowMoments {
         }
         acc.count += cnt;
     }
+    // CNT = false: the sweep counts the row's candidates (count_add)
+    template <bool CNT = true>
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         const float w = ex2_approx(-hl * d2f) * (ok ? iv : 0.f);
         const double y = ok ? v : 0.0;
         acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);
-        acc.add_fast((double)w, y, dx, dy, dxx, dyy, ok ? 1 : 0);
+        acc.add_fast((double)w, y, dx, dy, dxx, dyy, CNT ? (ok ? 1 : 0) : 0);
     }
+    __device__ __forceinline__ void count_add(int n) { acc.count += n; }
 };
 
 // The fast path's ICI variance v = sum t (phi.g)^2 is a sum of nonnegative
@@ -592,6 +604,8 @@ struct RowVariance {
         var_add(v, t32, pg, pf);
         T = fmaf(W * e.y, fabsf(pf) * fabsf(e.x), T);
     }
+    __device__ __forceinline__ void count_add(int) {}
+    template <bool CNT = true>
     __device__ __forceinline__ void general(bool ok, double y, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool = true) {
         const float W = ex2_approx(-hl * d2f) * (ok ? 1.f : 0.f);
@@ -629,11 +643,13 @@ struct FusedVarMom {
     }
     // rotated sensors: inner differs between the lanes of a warp, so both
     // halves run unconditionally (the variance with weight 0 outside r_kin)
+    template <bool CNT = true>
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float d2f, bool inner) {
-        M.general(ok, v, iv, dx, dy, dxx, dyy, d2f);
+        M.template general<CNT>(ok, v, iv, dx, dy, dxx, dyy, d2f);
         V.general(ok && inner, v, iv, dx, dy, dxx, dyy, d2f);
     }
+    __device__ __forceinline__ void count_add(int n) { M.count_add(n); }
     __device__ __forceinline__ void first_rt(double dy, double dyy, float2 e, double dx,
                                              double dxx, float d2f, bool inner) {
         V.begin_row(dy, dyy);
