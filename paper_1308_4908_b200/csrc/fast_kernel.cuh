@@ -133,17 +133,34 @@ __device__ __forceinline__ void accumulate_taps(const DevParams &P, const unsign
 // ---------------------------------------------------------------------------
 // Per-pixel kernel inputs (SteeringField.kernel_inputs, steering.py:80-107),
 // float64 in the reference's operation order; an = (h11, h12, h22, r0).
-__device__ __forceinline__ void steer_inputs(const DevParams &P, int pix, int c, double *an) {
+// The channel-independent part (one cos/sin pair per pixel): the steering
+// matrix C = gamma R diag(sigma, 1/sigma) R^T and sigma/gamma.
+struct SteerPixel {
+    double c11, c12, c22, s, g;
+};
+__device__ __forceinline__ SteerPixel steer_pixel(const DevParams &P, int pix) {
     const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
     const double ct = cos(th), st = sin(th);
+    SteerPixel o;
+    o.c11 = g * (s * ct * ct + st * st / s);
+    o.c12 = g * (ct * st) * (1.0 / s - s);
+    o.c22 = g * (s * st * st + ct * ct / s);
+    o.s = s;
+    o.g = g;
+    return o;
+}
+// ... and per channel: H^-1 = C / h, r0 = 3 sqrt(h sigma / gamma) (same
+// operation order as the one-piece form)
+__device__ __forceinline__ void steer_channel(const DevParams &P, const SteerPixel &sp, int c,
+                                              double *an) {
     const double h = P.h[c][0];  // channel scale
-    const double c11 = g * (s * ct * ct + st * st / s);
-    const double c12 = g * (ct * st) * (1.0 / s - s);
-    const double c22 = g * (s * st * st + ct * ct / s);
-    an[0] = c11 / h;
-    an[1] = c12 / h;
-    an[2] = c22 / h;
-    an[3] = 3.0 * sqrt(h * s / g);
+    an[0] = sp.c11 / h;
+    an[1] = sp.c12 / h;
+    an[2] = sp.c22 / h;
+    an[3] = 3.0 * sqrt(h * sp.s / sp.g);
+}
+__device__ __forceinline__ void steer_inputs(const DevParams &P, int pix, int c, double *an) {
+    steer_channel(P, steer_pixel(P, pix), c, an);
 }
 
 // Row-factored moments with the anisotropic window
@@ -267,6 +284,10 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     uint32_t vbs[PAT_MAXS];
     if constexpr (PAT) tap_bases<PAT_MAXS, MRG ? 16 : 8>(P, sm, org, px, py, vbs);
 
+    // STEER: the steering field's channel-independent part once per pixel
+    SteerPixel sp{};
+    if constexpr (STEER)
+        if (covered) sp = steer_pixel(P, pix);
     for (int c = 0; c < 3; ++c) {
         PixelResult R;
         R.sidx = 0;
@@ -274,7 +295,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         if (covered) {
             if constexpr (STEER) {
                 double an[4];
-                steer_inputs(P, pix, c, an);
+                steer_channel(P, sp, c, an);
                 const double r = fmin(an[3], P.max_radius);
                 Acc<PN> acc;
                 accumulate_aniso<ORDER>(sweep, c, an, r, __dmul_rn(r, r), acc);
