@@ -793,15 +793,19 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
         Pf.tiles_x = P.tiles_x;
         Pf.tiles_y = P.tiles_y;
         int rc2;
+#ifndef HDR_STEER_MAXC
+#define HDR_STEER_MAXC 4  // columns per branch-free chunk of the steered sweep (2/3/4/6/8: 0.75/0.83/0.67/0.77/0.89 ms)
+#endif
+        constexpr int SM = HDR_STEER_MAXC;
         switch (P.order) {
-            case 0: rc2 = launch_fast<0, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st); break;
+            case 0: rc2 = launch_fast<0, false, SM, 0, false, true>(P, T, tiles, smem_bytes, st); break;
             case 1:
-                rc2 = merged ? launch_fast<1, false, 8, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
-                             : launch_fast<1, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st);
+                rc2 = merged ? launch_fast<1, false, SM, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
+                             : launch_fast<1, false, SM, 0, false, true>(P, T, tiles, smem_bytes, st);
                 break;
             default:
-                rc2 = merged ? launch_fast<2, false, 8, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
-                             : launch_fast<2, false, 8, 0, false, true>(P, T, tiles, smem_bytes, st);
+                rc2 = merged ? launch_fast<2, false, SM, 0, false, true, true>(Pf, T, tiles, smem_bytes, st)
+                             : launch_fast<2, false, SM, 0, false, true>(P, T, tiles, smem_bytes, st);
                 break;
         }
         if (rc2 != HDR_OK) return rc2;

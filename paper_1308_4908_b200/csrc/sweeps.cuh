@@ -383,12 +383,15 @@ struct RowMoments {
     float hl;
     double S[2 * ORDER + 1], T[ORDER + 1];
     int cnt;
+    float fcnt;  // sample4: the merged positions' sample counts (exact in fp32; no
+                 // per-sample float-to-int conversion on the XU pipe)
     __device__ __forceinline__ void begin_row(double, double) {
 #pragma unroll
         for (int n = 0; n <= 2 * ORDER; ++n) S[n] = 0.0;
 #pragma unroll
         for (int n = 0; n <= ORDER; ++n) T[n] = 0.0;
         cnt = 0;
+        fcnt = 0.f;
     }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double,
                                            double dxx, double, float d2f, bool = true) {
@@ -436,7 +439,10 @@ struct RowMoments {
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
     }
     // row taps: the sweep counts the row (row_count, before end_row)
-    __device__ __forceinline__ void row_count(int n) { cnt = n; }
+    __device__ __forceinline__ void row_count(int n) {
+        cnt = n;
+        fcnt = 0.f;
+    }
     // the first tap of a row run: opens the row sums (no zeroing)
     __device__ __forceinline__ void first_rt(double, double, float2 e, double dx, double dxx,
                                              float d2f, bool = true) {
@@ -477,7 +483,7 @@ struct RowMoments {
         T[0] += wy;
 #pragma unroll
         for (int n = 1; n <= ORDER; ++n) T[n] = fma(wy, px[n], T[n]);
-        cnt += ok ? (int)e.w : 0;
+        fcnt += ok ? e.w : 0.f;
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) {
         double dp[5];
@@ -512,7 +518,7 @@ struct RowMoments {
                 }
             }
         }
-        acc.count += cnt;
+        acc.count += cnt + (int)fcnt;
     }
     // CNT = false: the sweep counts the row's candidates (count_add)
     template <bool CNT = true>
