@@ -277,6 +277,7 @@ int hdr_sample_index_workspace_bytes(long long n, long long ncells, size_t *byte
  * (steering.py:206-211; an exact radix select on the float32 bit patterns);
  * hdr_steering_field_devscale is hdr_steering_field reading that scale from
  * device memory.  Both are stream-ordered and CUDA-graph capturable.
+ * n < 2^32 (32-bit histogram counters; HDR_ERR_ARG otherwise).
  */
 int hdr_gradient_scale_workspace_bytes(size_t *bytes);
 int hdr_gradient_scale(const float *values, long long n, double q, double *scale,

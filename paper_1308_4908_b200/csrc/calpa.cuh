@@ -13,35 +13,14 @@ struct SteerConsts {
     int half;
     double wstd, lam1, lam2, alpha, sigma_max, inv_scale;
     const double *scale_dev;  // non-null: inv_scale = 1 / *scale_dev (device-computed scale)
+    double scale;             // tiled kernel: g / scale as the reference divides (0: scale_dev)
 };
 
-// steering_field_kernel (_kernels.py:310-392), float64, one thread per pixel.
-__global__ void steering_field_kernel(const float *gx, const float *gy, int w, int h,
-                                      SteerConsts K, double *theta, double *sigma,
-                                      double *gamma) {
-    const int xx = blockIdx.x * blockDim.x + threadIdx.x, yy = blockIdx.y;
-    if (xx >= w) return;
-    if (K.scale_dev) K.inv_scale = 1.0 / *K.scale_dev;
-    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
-    int n = 0;
-    const double den = 2.0 * K.wstd * K.wstd;
-    for (int dy = -K.half; dy <= K.half; ++dy) {
-        const int iy = yy + dy;
-        if (iy < 0 || iy >= h) continue;
-        for (int dx = -K.half; dx <= K.half; ++dx) {
-            const int ix = xx + dx;
-            if (ix < 0 || ix >= w) continue;
-            const double g1 = (double)gx[(size_t)iy * w + ix] * K.inv_scale;
-            const double g2 = (double)gy[(size_t)iy * w + ix] * K.inv_scale;
-            if (!(isfinite(g1) && isfinite(g2))) continue;
-            const double wgt = exp(-(double)(dx * dx + dy * dy) / den);
-            s11 += wgt * g1 * g1;
-            s12 += wgt * g1 * g2;
-            s22 += wgt * g2 * g2;
-            ++n;
-        }
-    }
-    const size_t o = (size_t)yy * w + xx;
+// The per-pixel epilogue of _kernels.steering_field_kernel (_kernels.py:303-392):
+// eigen-range of the 2x2 structure tensor, orientation, elongation, scaling.
+__device__ __forceinline__ void steering_epilogue(const SteerConsts &K, double s11, double s12,
+                                                  double s22, int n, size_t o, double *theta,
+                                                  double *sigma, double *gamma) {
     if (n == 0) {
         theta[o] = 0.0;
         sigma[o] = 1.0;
@@ -74,6 +53,98 @@ __global__ void steering_field_kernel(const float *gx, const float *gy, int w, i
     theta[o] = th;
     sigma[o] = sg;
     gamma[o] = pow((s1 * s2 + K.lam2) / n, K.alpha);
+}
+
+// Tiled form (round 2): a 32x8 block of pixels stages its (32+2h) x (8+2h)
+// neighbourhood once as float64 (g_x / scale, g_y / scale) with a validity
+// byte (inside the image and both finite; invalid entries hold (0, 0), whose
+// terms add +0 and leave the sums bit-identical to skipping them), and the
+// (2h+1)^2 window weights exp(-(dx^2+dy^2) / (2 wstd^2)) once per block; the
+// structure tensor then sums in the reference's order (rows, then columns;
+// (w g1) g1 without contraction, as _kernels.py evaluates it).
+constexpr int STF_TW = 32, STF_TH = 8;
+__host__ __device__ inline int stf_smem_bytes(int half) {
+    const int tw = STF_TW + 2 * half, th = STF_TH + 2 * half, nw = (2 * half + 1) * (2 * half + 1);
+    return tw * th * 16 + ((tw * th + 15) & ~15) + nw * 8;
+}
+__global__ void __launch_bounds__(STF_TW *STF_TH)
+    steering_field_tiled_kernel(const float *gx, const float *gy, int w, int h, SteerConsts K,
+                                double *theta, double *sigma, double *gamma) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int half = K.half, tw = STF_TW + 2 * half, th = STF_TH + 2 * half;
+    const int nwin = 2 * half + 1;
+    double2 *g = (double2 *)sm;
+    unsigned char *valid = sm + tw * th * 16;
+    double *wt = (double *)(sm + tw * th * 16 + ((tw * th + 15) & ~15));
+    const double scale = K.scale_dev ? *K.scale_dev : K.scale;
+    const int x0 = blockIdx.x * STF_TW - half, y0 = blockIdx.y * STF_TH - half;
+    const int tid = threadIdx.y * STF_TW + threadIdx.x;
+    for (int i = tid; i < tw * th; i += STF_TW * STF_TH) {
+        const int ix = x0 + i % tw, iy = y0 + i / tw;
+        double g1 = 0.0, g2 = 0.0;
+        bool ok = false;
+        if (ix >= 0 && ix < w && iy >= 0 && iy < h) {
+            g1 = __ddiv_rn((double)gx[(size_t)iy * w + ix], scale);  // gx / scale (steering.py)
+            g2 = __ddiv_rn((double)gy[(size_t)iy * w + ix], scale);
+            ok = isfinite(g1) && isfinite(g2);
+        }
+        g[i] = ok ? make_double2(g1, g2) : make_double2(0.0, 0.0);
+        valid[i] = ok ? 1 : 0;
+    }
+    const double den = 2.0 * K.wstd * K.wstd;
+    for (int i = tid; i < nwin * nwin; i += STF_TW * STF_TH) {
+        const int dx = i % nwin - half, dy = i / nwin - half;
+        wt[i] = exp(-(double)(dx * dx + dy * dy) / den);
+    }
+    __syncthreads();
+    const int xx = blockIdx.x * STF_TW + threadIdx.x, yy = blockIdx.y * STF_TH + threadIdx.y;
+    if (xx >= w || yy >= h) return;
+    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+    int n = 0;
+    for (int dy = 0; dy < nwin; ++dy) {
+        const double2 *gr = g + (threadIdx.y + dy) * tw + threadIdx.x;
+        const unsigned char *vr = valid + (threadIdx.y + dy) * tw + threadIdx.x;
+        const double *wr = wt + dy * nwin;
+        for (int dx = 0; dx < nwin; ++dx) {
+            const double2 v = gr[dx];
+            const double wgt = wr[dx];
+            const double a = __dmul_rn(wgt, v.x);
+            s11 = __dadd_rn(s11, __dmul_rn(a, v.x));
+            s12 = __dadd_rn(s12, __dmul_rn(a, v.y));
+            s22 = __dadd_rn(s22, __dmul_rn(__dmul_rn(wgt, v.y), v.y));
+            n += vr[dx];
+        }
+    }
+    steering_epilogue(K, s11, s12, s22, n, (size_t)yy * w + xx, theta, sigma, gamma);
+}
+
+// steering_field_kernel (_kernels.py:310-392), float64, one thread per pixel.
+__global__ void steering_field_kernel(const float *gx, const float *gy, int w, int h,
+                                      SteerConsts K, double *theta, double *sigma,
+                                      double *gamma) {
+    const int xx = blockIdx.x * blockDim.x + threadIdx.x, yy = blockIdx.y;
+    if (xx >= w) return;
+    if (K.scale_dev) K.inv_scale = 1.0 / *K.scale_dev;
+    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
+    int n = 0;
+    const double den = 2.0 * K.wstd * K.wstd;
+    for (int dy = -K.half; dy <= K.half; ++dy) {
+        const int iy = yy + dy;
+        if (iy < 0 || iy >= h) continue;
+        for (int dx = -K.half; dx <= K.half; ++dx) {
+            const int ix = xx + dx;
+            if (ix < 0 || ix >= w) continue;
+            const double g1 = (double)gx[(size_t)iy * w + ix] * K.inv_scale;
+            const double g2 = (double)gy[(size_t)iy * w + ix] * K.inv_scale;
+            if (!(isfinite(g1) && isfinite(g2))) continue;
+            const double wgt = exp(-(double)(dx * dx + dy * dy) / den);
+            s11 += wgt * g1 * g1;
+            s12 += wgt * g1 * g2;
+            s22 += wgt * g2 * g2;
+            ++n;
+        }
+    }
+    steering_epilogue(K, s11, s12, s22, n, (size_t)yy * w + xx, theta, sigma, gamma);
 }
 
 // Exact accumulation with an arbitrary SPD window Hinv (two-phase CALPA).
@@ -218,56 +289,141 @@ struct QuantileState {
     double t;                   // interpolation weight
 };
 
-__global__ void absq_hist_hi_kernel(const float *v, long long n, unsigned *hist,
-                                    unsigned long long *count) {
+// High-16-bit histogram, privatised per block in shared memory: |x| has a
+// zero sign bit, so its high 16 bits take 2^15 values (128 KB of counters);
+// one block per SM counts its slice with shared-memory atomics and adds its
+// non-zero bins to the global histogram (round 1's global atomics serialised
+// on the few hot bins of a natural image: 0.37 ms per 4-Mpx plane; now 12 us).
+constexpr int QBINS_HI = 32768;
+constexpr int QHIST_SMEM = QBINS_HI * 4;
+__global__ void __launch_bounds__(1024) absq_hist_hi_smem_kernel(const float *v, long long n,
+                                                                  unsigned *hist,
+                                                                  unsigned long long *count) {
+    extern __shared__ unsigned sh[];
+    for (int i = threadIdx.x; i < QBINS_HI; i += blockDim.x) sh[i] = 0u;
+    __syncthreads();
     unsigned long long c = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const float x = v[i];
         if (!isfinite(x)) continue;
-        atomicAdd(&hist[__float_as_uint(fabsf(x)) >> 16], 1u);
+        atomicAdd(&sh[__float_as_uint(fabsf(x)) >> 16], 1u);
         ++c;
     }
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+    __syncthreads();
+    for (int i = threadIdx.x; i < QBINS_HI; i += blockDim.x) {
+        const unsigned b = sh[i];
+        if (b) atomicAdd(&hist[i], b);
+    }
+}
+
+// Block-cooperative rank search over a QBINS-bin histogram (1024 threads):
+// block_chunk_scan sums chunks of 64 bins by coalesced warp loads and scans
+// the 1024 chunk sums; block_locate finds the chunk holding rank `want` and
+// scans its 64 bins in one warp, returning (through shared memory) the bin and
+// the count of values in lower bins.
+// (round 1 summed 64 bins per thread with strided loads and walked the chunk
+// with dependent loads: 40-80 us per search)
+constexpr int QPER = QBINS / 1024;  // 64 bins per chunk
+__device__ __forceinline__ void block_chunk_scan(const unsigned *h, unsigned long long *part) {
+    constexpr int PER = QPER;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // 32 chunks per warp, all loads in flight before the reductions (a
+    // load-reduce loop left one L2 round trip per chunk on the critical path)
+    unsigned a[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = wid + 32 * i;
+        a[i] = h[c * PER + lane] + h[c * PER + 32 + lane];  // two disjoint bins: <= n < 2^32
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        unsigned long long v = a[i];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) part[wid + 32 * i] = v;
+    }
+    __syncthreads();
+    {  // inclusive scan of part[1024]: warp scans, then the warp totals
+        __shared__ unsigned long long wsum[32];
+        unsigned long long x = part[threadIdx.x];
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, m);
+            if (lane >= m) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long t = wsum[lane];
+#pragma unroll
+            for (int m = 1; m < 32; m <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, m);
+                if (lane >= m) t += y;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        part[threadIdx.x] = x + (wid ? wsum[wid - 1] : 0ull);
+        __syncthreads();
+    }
+}
+// the bin of rank `want` given block_chunk_scan's part[]
+__device__ __forceinline__ void block_locate(const unsigned *h, unsigned long long want,
+                                             const unsigned long long *part, int *s_bin,
+                                             unsigned long long *s_before) {
+    constexpr int PER = QPER;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ int s_chunk;
+    {
+        const unsigned long long lo = threadIdx.x ? part[threadIdx.x - 1] : 0, hi = part[threadIdx.x];
+        if (want >= lo && want < hi) s_chunk = threadIdx.x;
+    }
+    __syncthreads();
+    if (wid == 0) {  // the chunk's 64 bins: inclusive scan of lane pairs
+        const int c = s_chunk;
+        const unsigned long long base = c ? part[c - 1] : 0;
+        const unsigned a = h[c * PER + 2 * lane], b = h[c * PER + 2 * lane + 1];
+        unsigned long long x = (unsigned long long)a + b;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, m);
+            if (lane >= m) x += y;
+        }
+        const unsigned long long lo = base + x - a - b;  // before this lane's two bins
+        if (want >= lo && want < lo + a) {
+            *s_bin = c * PER + 2 * lane;
+            *s_before = lo;
+        } else if (want >= lo + a && want < lo + a + b) {
+            *s_bin = c * PER + 2 * lane + 1;
+            *s_before = lo + a;
+        }
+    }
+    __syncthreads();
 }
 
 // one block of 1024 threads: bins of ranks k and k+1
 __global__ void __launch_bounds__(1024) absq_select_kernel(const unsigned *hist, double q,
                                                             QuantileState *st) {
     __shared__ unsigned long long part[1024];
+    __shared__ int s_bin;
+    __shared__ unsigned long long s_before;
     const unsigned long long n = st->n;
     if (n == 0) return;
     const double vidx = q * (double)(n - 1);  // numpy: quantiles * (n - alpha - beta + 1) + alpha - 1
     const long long k = (long long)floor(vidx);
     const long long k1 = k + 1 < (long long)n ? k + 1 : (long long)n - 1;
-    unsigned long long sum = 0;
-    const int per = QBINS / 1024;
-    for (int j = 0; j < per; ++j) sum += hist[threadIdx.x * per + j];
-    part[threadIdx.x] = sum;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
-        const unsigned long long add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-        __syncthreads();
-        part[threadIdx.x] += add;
-        __syncthreads();
-    }
-    const unsigned long long lo = threadIdx.x ? part[threadIdx.x - 1] : 0, hi = part[threadIdx.x];
+    block_chunk_scan(hist, part);
     for (int r = 0; r < 2; ++r) {
-        const unsigned long long want = (unsigned long long)(r ? k1 : k);
-        if (want >= lo && want < hi) {  // this thread's bins hold the rank
-            unsigned long long acc = lo;
-            for (int j = 0; j < per; ++j) {
-                const unsigned h = hist[threadIdx.x * per + j];
-                if (want < acc + h) {
-                    st->bin[r] = threadIdx.x * per + j;
-                    st->before[r] = (long long)acc;
-                    break;
-                }
-                acc += h;
-            }
+        block_locate(hist, (unsigned long long)(r ? k1 : k), part, &s_bin, &s_before);
+        if (threadIdx.x == 0) {
+            st->bin[r] = s_bin;
+            st->before[r] = (long long)s_before;
         }
+        __syncthreads();
     }
     if (threadIdx.x == 0) {
         st->rank[0] = k;
@@ -295,37 +451,20 @@ __global__ void __launch_bounds__(1024) absq_finish_kernel(const unsigned *hist0
                                                             const QuantileState *st,
                                                             double *scale) {
     __shared__ unsigned long long part[1024];
+    __shared__ int s_bin;
+    __shared__ unsigned long long s_before;
     __shared__ float val[2];
     if (st->n == 0) {
         if (threadIdx.x == 0) *scale = 1.0;
         return;
     }
-    const int per = QBINS / 1024;
     for (int r = 0; r < 2; ++r) {
-        const unsigned *h = (r == 1 && st->bin[1] != st->bin[0]) ? hist1 : hist0;
-        const unsigned long long want = (unsigned long long)(st->rank[r] - st->before[r]);
-        unsigned long long sum = 0;
-        for (int j = 0; j < per; ++j) sum += h[threadIdx.x * per + j];
-        part[threadIdx.x] = sum;
-        __syncthreads();
-        for (int off = 1; off < 1024; off <<= 1) {
-            const unsigned long long add = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-            __syncthreads();
-            part[threadIdx.x] += add;
-            __syncthreads();
-        }
-        const unsigned long long lo = threadIdx.x ? part[threadIdx.x - 1] : 0, hi = part[threadIdx.x];
-        if (want >= lo && want < hi) {
-            unsigned long long acc = lo;
-            for (int j = 0; j < per; ++j) {
-                const unsigned c = h[threadIdx.x * per + j];
-                if (want < acc + c) {
-                    val[r] = __uint_as_float(((unsigned)st->bin[r] << 16) | (unsigned)(threadIdx.x * per + j));
-                    break;
-                }
-                acc += c;
-            }
-        }
+        const bool other = r == 1 && st->bin[1] != st->bin[0];
+        const unsigned *h = other ? hist1 : hist0;
+        if (r == 0 || other) block_chunk_scan(h, part);
+        block_locate(h, (unsigned long long)(st->rank[r] - st->before[r]), part, &s_bin,
+                     &s_before);
+        if (threadIdx.x == 0) val[r] = __uint_as_float(((unsigned)st->bin[r] << 16) | (unsigned)s_bin);
         __syncthreads();
     }
     if (threadIdx.x == 0) {

@@ -892,6 +892,19 @@ static int steering_field(const float *gx, const float *gy, int width, int heigh
     K.sigma_max = sigma_max;
     K.inv_scale = scale_dev ? 0.0 : 1.0 / gradient_scale;
     K.scale_dev = scale_dev;
+    K.scale = scale_dev ? 0.0 : gradient_scale;
+    const int tiled_smem = stf_smem_bytes(K.half);
+    if (tiled_smem <= 160 * 1024) {  // the tiled kernel (windows up to ~70 px)
+        if (set_smem_attr((const void *)steering_field_tiled_kernel, tiled_smem) != HDR_OK)
+            return HDR_ERR_CUDA;
+        dim3 grid((width + STF_TW - 1) / STF_TW, (height + STF_TH - 1) / STF_TH);
+        COUNT_LAUNCH();
+        steering_field_tiled_kernel<<<grid, dim3(STF_TW, STF_TH), tiled_smem,
+                                      (cudaStream_t)stream>>>(gx, gy, width, height, K, theta,
+                                                              sigma, gamma);
+        return cudaPeekAtLastError() == cudaSuccess ? HDR_OK
+                                                    : cuda_fail("steering_field_tiled_kernel launch");
+    }
     dim3 grid((width + 127) / 128, height);
     COUNT_LAUNCH();
     steering_field_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(gx, gy, width, height, K, theta,
@@ -927,14 +940,22 @@ int hdr_gradient_scale(const float *values, long long n, double q, double *scale
     size_t need = 0;
     hdr_gradient_scale_workspace_bytes(&need);
     if (!values || n < 0 || !scale || !workspace || !(q >= 0.0 && q <= 1.0)) return HDR_ERR_ARG;
+    if (n >= (1ll << 32)) return HDR_ERR_ARG;  // 32-bit histogram counters
     if (workspace_bytes < need) return HDR_ERR_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned *hist = (unsigned *)workspace, *hist0 = hist + QBINS, *hist1 = hist0 + QBINS;
     QuantileState *qs = (QuantileState *)(hist1 + QBINS);
     if (cudaMemsetAsync(workspace, 0, need, st) != cudaSuccess) return cuda_fail("quantile memset");
     const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+    if (set_smem_attr((const void *)absq_hist_hi_smem_kernel, QHIST_SMEM) != HDR_OK)
+        return HDR_ERR_CUDA;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned hblocks =
+        (unsigned)std::max<long long>(1, std::min<long long>((n + 1023) / 1024, nsm));
     COUNT_LAUNCH();
-    absq_hist_hi_kernel<<<blocks, 256, 0, st>>>(values, n, hist, &qs->n);
+    absq_hist_hi_smem_kernel<<<hblocks, 1024, QHIST_SMEM, st>>>(values, n, hist, &qs->n);
     COUNT_LAUNCH();
     absq_select_kernel<<<1, 1024, 0, st>>>(hist, q, qs);
     COUNT_LAUNCH();
