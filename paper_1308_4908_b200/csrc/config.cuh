@@ -55,7 +55,15 @@ constexpr int NBUF = HDR_NBUF;
 #define HDR_NBUF_TAP 2
 #endif
 constexpr int NBUF_TAP = HDR_NBUF_TAP;
-__host__ __device__ constexpr int nbuf_for(int pat) { return pat ? NBUF_TAP : NBUF; }
+// CALPA's steered pass: windows up to max_radius make each tile's staged
+// region large and its compute short
+#ifndef HDR_NBUF_STEER
+#define HDR_NBUF_STEER 2
+#endif
+constexpr int NBUF_STEER = HDR_NBUF_STEER;
+__host__ __device__ constexpr int nbuf_for(int pat, bool steer = false) {
+    return steer ? NBUF_STEER : (pat ? NBUF_TAP : NBUF);
+}
 static const size_t LUT_BYTES = 65536 * sizeof(double2);
 static const size_t RT_TABLE_BYTES = 64 * 1024;  // row-tap table (workspace, then shared memory)
 

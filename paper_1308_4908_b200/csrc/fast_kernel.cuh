@@ -295,7 +295,13 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         if (covered) {
             if constexpr (STEER) {
                 double an[4];
-                steer_channel(P, sp, c, an);
+                // the fast path rounds H^-1 to fp32 for its weights: C * (1/h)
+                // instead of C / h there (the radius an[3] stays exact)
+                const double ih = P.hinv[c][0];
+                an[0] = sp.c11 * ih;
+                an[1] = sp.c12 * ih;
+                an[2] = sp.c22 * ih;
+                an[3] = 3.0 * sqrt(P.h[c][0] * sp.s / sp.g);
                 const double r = fmin(an[3], P.max_radius);
                 Acc<PN> acc;
                 accumulate_aniso<ORDER>(sweep, c, an, r, __dmul_rn(r, r), acc);
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(NT, (ORDER >= 2 ? HDR_O2_MINBLOCKS
     lpa_fast_kernel(const __grid_constant__ DevParams P,
                     const __grid_constant__
                     typename std::conditional<(PAT != 0), TapParam, NoTaps>::type T) {
-    constexpr int NBUF = nbuf_for(PAT);
+    constexpr int NBUF = nbuf_for(PAT, STEER);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int s_org[NBUF][MAXS][2];
     __shared__ int s_cov[NBUF];

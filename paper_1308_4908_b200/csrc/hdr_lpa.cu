@@ -675,7 +675,7 @@ static int setup_staging(DevParams &P, int n_sensors, double fastR, bool allow_t
         d.off_ty4 = d.separable ? take(d.rh * 8) : 0;
     }
     P.buf_stride = smem;
-    smem_bytes = P.plane_base + nbuf_for(P.pat) * P.buf_stride;
+    smem_bytes = P.plane_base + nbuf_for(P.pat, P.st_theta != nullptr) * P.buf_stride;
     if (smem_bytes > 200 * 1024) return STAGING_TOO_LARGE;  // windows too large to stage
     for (int s = 0; s < n_sensors; ++s)
         if (!encode_phase_map(P.s[s], &P.tmap[s], P.merged != 0)) {
