@@ -140,7 +140,8 @@ struct SteerPixel {
 };
 __device__ __forceinline__ SteerPixel steer_pixel(const DevParams &P, int pix) {
     const double th = P.st_theta[pix], s = P.st_sigma[pix], g = P.st_gamma[pix];
-    const double ct = cos(th), st = sin(th);
+    double st, ct;
+    sincos(th, &st, &ct);  // one argument reduction for both
     SteerPixel o;
     o.c11 = g * (s * ct * ct + st * st / s);
     o.c12 = g * (ct * st) * (1.0 / s - s);
