@@ -12,8 +12,9 @@ for line in src:
         print("reference", j["config"]["workload"], f"{j['value']:.4f} fps", j["cpu_baseline"]["cores"], "cores")
         continue
     r = j["roofline"]
-    print(f"{j['config']['workload']}: {j['value']:.1f} fps ({j['mpix_per_s']:.0f} Mpx/s) "
+    mpx = f" ({j['mpix_per_s']:.0f} Mpx/s)" if "mpix_per_s" in j else ""
+    hbm = f" | hbm frac {r['hbm']['frac']:.4f}" if "hbm" in r else ""
+    print(f"{j['config']['workload']}: {j['value']:.1f} fps{mpx} "
           f"e2e {j['e2e']['value']:.1f} fps | kernel {r['kernel_ms']:.3f} ms, {r['bound']} "
-          f"{r['achieved']:.2f}/{r['peak']:.2f} {r['unit']} frac {r['frac']:.3f} | hbm frac "
-          f"{r['hbm']['frac']:.4f} | slow {j['slow_path_items']} | clocks {j['clocks']} | "
-          f"cpu {j['cpu_baseline']}")
+          f"{r['achieved']:.2f}/{r['peak']:.2f} {r['unit']} frac {r['frac']:.3f}{hbm} | "
+          f"slow {j.get('slow_path_items')} | clocks {j['clocks']} | cpu {j.get('cpu_baseline')}")
