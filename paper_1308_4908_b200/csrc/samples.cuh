@@ -81,12 +81,15 @@ __device__ int csr_fit_at(const CsrIndex &ix, double qx, double qy, double h11, 
     cx_hi = min(cx_hi, ix.nx - 1);
     cy_hi = min(cy_hi, ix.ny - 1);
     const double h12x2 = __dmul_rn(2.0, h12);
-    for (int cy = cy_lo; cy <= cy_hi; ++cy) {
+    // the cells [cx_lo, cx_hi] of one cell row are consecutive in the CSR
+    // order, so their rows form ONE range: the same samples in the same order
+    // as the reference's cell-by-cell loop, without the per-cell loop (whose
+    // lane-dependent trip counts left ~40 % of each warp idle)
+    for (int cy = cy_lo; cx_lo <= cx_hi && cy <= cy_hi; ++cy) {
         const int64_t row = (int64_t)cy * ix.nx;
-        for (int cx = cx_lo; cx <= cx_hi; ++cx) {
-            const int64_t cell = row + cx;
-            const int64_t k1 = ix.cell_start[cell + 1];
-            for (int64_t k = ix.cell_start[cell]; k < k1; ++k) {
+        {
+            const int64_t k1 = ix.cell_start[row + cx_hi + 1];
+            for (int64_t k = ix.cell_start[row + cx_lo]; k < k1; ++k) {
                 const double4 R = *(const double4 *)(ix.packed + 4 * k);
                 const double dx = __dsub_rn(R.x, qx), dy = __dsub_rn(R.y, qy);
                 if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) > r2) continue;
