@@ -9,12 +9,15 @@ import sys
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1308_4908_b200/libhdrlpa.so"
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 HEAD = {
-    "lpa_fast_kernel<1,0,4,4,...> (cfg2 co-sited taps)": r"lpa_fast_kernelILi1ELb0ELi4ELi4ELb0ELb0ELb0ELb0E",
-    "lpa_fast_kernel<2,1,6,0,RT,ICISM> (cfg3/cfg5 ICI)": r"lpa_fast_kernelILi2ELb1ELi6ELi0ELb1ELb0ELb0ELb1E",
-    "lpa_fast_kernel<2,1,6,0,RT> (ICI, register state)": r"lpa_fast_kernelILi2ELb1ELi6ELi0ELb1ELb0ELb0ELb0E",
+    "lpa_fast_kernel<1,0,4,4,...> (cfg2 co-sited taps)": r"lpa_fast_kernelILi1ELb0ELi4ELi4ELi0ELb0ELb0ELb0E",
+    "lpa_fast_kernel<2,1,6,0,RT2,ICISM> (cfg3/cfg5 ICI)": r"lpa_fast_kernelILi2ELb1ELi6ELi0ELi2ELb0ELb0ELb1E",
+    "lpa_fast_kernel<2,1,6,0,RT2> (ICI, register state)": r"lpa_fast_kernelILi2ELb1ELi6ELi0ELi2ELb0ELb0ELb0E",
+    "lpa_fast_kernel<1,0,4,0,0,STEER,MRGS> (CALPA steered pass)": r"lpa_fast_kernelILi1ELb0ELi4ELi0ELi0ELb1ELb1ELb0E",
     "lpa_slow_kernel<2> (exact path)": r"lpa_slow_kernelILi2E",
     "radiance_merge_kernel (cfg2 pre-pass)": r"radiance_merge_kernel",
     "radiance_phase_kernel (pre-pass)": r"radiance_phase_kernel",
+    "steering_field_tiled_kernel (CALPA)": r"steering_field_tiled_kernel",
+    "lpa_samples_kernel<1> (scattered samples)": r"lpa_samples_kernelILi1E",
 }
 OPS = ["UTMALDG", "SYNCS", "DFMA", "DMUL", "DADD", "DSETP", "MUFU", "F2F", "FFMA", "LDS", "STS",
        "LDG", "STG", "STL", "LDL", "BRA", "SHFL"]
