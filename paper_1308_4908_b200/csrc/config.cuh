@@ -30,6 +30,9 @@ constexpr int TW = 32, TH = 8, NT = TW * TH;  // NT consumer threads, one per ti
 
 // workspace layout: [header: work counter][pre-computed taps][work items]
 static const size_t WS_HEADER = 256;
+// header words: 0 full-evaluation items, 1 tile counter, 2 exact-path item
+// counter, 3 fault bits, 4 recomputation items, 5 recomputation counter
+static const int WS_HEADER_WORDS = 6;
 // Order-2 tile sweeps: skip samples outside the disk with branches (1) or
 // accumulate them with zero weight (0; the row-factored moments make a
 // sample cheap enough that divergent branches cost more than they save)

@@ -192,10 +192,49 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
 #ifndef SLOW_LANES_O2
 #define SLOW_LANES_O2 4
 #endif
+constexpr uint32_t ITEM_DONE = 0xffffffffu;  // a recomputation that succeeded
+
+// The recomputations (kk > 0, from the end of the item list) in a kernel of
+// their own: a small, uniform code path (one float64 fit at the selected
+// scale) instead of sharing warps and the instruction cache with the full
+// ladder / ICI evaluations (round 2: the mixed kernel issued 12 % of cycles,
+// 10.6 of 32 lanes active, instruction-fetch stalls dominant).  A success
+// writes the result and marks the slot ITEM_DONE; a failure leaves the item
+// as a full evaluation (kk = 0) for lpa_slow_kernel.
+template <int ORDER>
+__global__ void __launch_bounds__(128) lpa_precise_kernel(const __grid_constant__ DevParams P) {
+    constexpr int G = ORDER >= 2 ? SLOW_LANES_O2 : SLOW_LANES;
+    const uint32_t n = *P.prec_count;
+    const unsigned gmask = G >= 32 ? 0xffffffffu
+                                   : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+    const int leader = (threadIdx.x & 31) & ~(G - 1);
+    for (;;) {
+        uint32_t i = 0;
+        if ((threadIdx.x & (G - 1)) == 0) i = atomicAdd(P.prec_counter, 1u);
+        i = __shfl_sync(gmask, i, leader);
+        if (i >= n) break;
+        const uint32_t slot = P.item_cap - 1u - i;
+        const uint32_t item = P.work_items[slot];
+        const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
+        const int kk = (int)((item >> 2) & 15);
+        const int ox = pix % P.out_w, oy = pix / P.out_w;
+        const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
+        PixelResult R;
+        const bool ok = precise_fit<ORDER>(P, c, kk - 1, sweep, R);
+        if ((threadIdx.x & (G - 1)) == 0) {
+            if (ok) write_result(P, pix, c, R);
+            P.work_items[slot] = ok ? ITEM_DONE : (item & ~(15u << 2));
+        }
+    }
+}
+
 template <int ORDER>
 __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ DevParams P) {
     constexpr int G = ORDER >= 2 ? SLOW_LANES_O2 : SLOW_LANES;  // lanes per work item
-    const uint32_t n = P.all_items ? P.all_items : *P.work_count;
+    // the full evaluations, then the recomputation slots (those that failed
+    // lpa_precise_kernel's float64 fit; ITEM_DONE ones are skipped)
+    const uint32_t n0 = P.all_items ? P.all_items : *P.work_count;
+    const uint32_t n = P.all_items ? P.all_items : n0 + *P.prec_count;
     // items are fetched dynamically (their cost varies by orders of magnitude)
     const unsigned gmask = G >= 32 ? 0xffffffffu
                                    : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
@@ -205,7 +244,9 @@ __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ D
         if ((threadIdx.x & (G - 1)) == 0) i = atomicAdd(P.slow_counter, 1u);
         i = __shfl_sync(gmask, i, leader);
         if (i >= n) break;
-        const uint32_t item = P.all_items ? (((i / 3u) << 6) | (i % 3u)) : P.work_items[i];
+        const uint32_t item = P.all_items ? (((i / 3u) << 6) | (i % 3u))
+                                          : P.work_items[i < n0 ? i : P.item_cap - 1u - (i - n0)];
+        if (item == ITEM_DONE) continue;
         const int pix = P.row_begin * P.out_w + (int)(item >> 6), c = (int)(item & 3);
         const int kk = (int)((item >> 2) & 15);
         const int ox = pix % P.out_w, oy = pix / P.out_w;

@@ -365,9 +365,12 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
             // work item: band-relative pixel | kk | channel, kk = 0: full exact
             // evaluation, kk = k + 1: float64 recomputation of the fit at scale k
             const uint32_t kk = st == FIT_PREC ? (uint32_t)R.sidx + 1u : 0u;
-            const uint32_t slot = atomicAdd(P.work_count, 1u);
-            P.work_items[slot] =
+            const uint32_t item =
                 ((uint32_t)(pix - P.row_begin * P.out_w) << 6) | (kk << 2) | (uint32_t)c;
+            if (kk)  // recomputations from the end of the list (lpa_precise_kernel)
+                P.work_items[P.item_cap - 1u - atomicAdd(P.prec_count, 1u)] = item;
+            else
+                P.work_items[atomicAdd(P.work_count, 1u)] = item;
         }
     }
 }

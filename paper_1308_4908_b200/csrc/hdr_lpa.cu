@@ -546,6 +546,9 @@ static int setup_params(const HdrSensor *sensors, int n_sensors, const HdrParams
     P.tile_counter = (uint32_t *)workspace + 1;
     P.slow_counter = (uint32_t *)workspace + 2;
     P.fault = (uint32_t *)workspace + 3;
+    P.prec_count = (uint32_t *)workspace + 4;
+    P.prec_counter = (uint32_t *)workspace + 5;
+    P.item_cap = (uint32_t)((size_t)out_w * out_h * 3);
     P.rt_global = (const unsigned char *)workspace + WS_HEADER;
     char *wsp = (char *)workspace + WS_HEADER + RT_TABLE_BYTES;
     for (int s = 0; s < n_sensors; ++s) {
@@ -733,7 +736,7 @@ int hdr_lpa_reconstruct(const HdrSensor *sensors, int n_sensors, const HdrParams
         Pf.tiles_y = P.tiles_y;
     }
     const DevParams &PF = merged ? Pf : P;
-    if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
+    if (cudaMemsetAsync(workspace, 0, WS_HEADER_WORDS * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (P.rt && upload_table(rt_table, (unsigned char *)P.rt_global, st) != HDR_OK)
         return HDR_ERR_CUDA;
@@ -780,7 +783,7 @@ int hdr_lpa_reconstruct_steered(const HdrSensor *sensors, int n_sensors,
     const bool staged =
         merged ||
         setup_staging(P, n_sensors, P.max_radius, false, T, rt_table, smem_bytes, maxc) == HDR_OK;
-    if (cudaMemsetAsync(workspace, 0, 4 * sizeof(uint32_t), st) != cudaSuccess)
+    if (cudaMemsetAsync(workspace, 0, WS_HEADER_WORDS * sizeof(uint32_t), st) != cudaSuccess)
         return cuda_fail("cudaMemsetAsync");
     if (launch_prepass(P, st, merged) != HDR_OK) return HDR_ERR_CUDA;
     int dev = 0, nsm = 148;
@@ -1212,11 +1215,11 @@ int hdr_lpa_workspace_status(const void *workspace, uint32_t *slow_items, uint32
                              void *stream) {
     if (!workspace) return HDR_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    uint32_t hdr[4];
+    uint32_t hdr[WS_HEADER_WORDS];
     if (cudaMemcpyAsync(hdr, workspace, sizeof(hdr), cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return cuda_fail("workspace status copy");
     if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("workspace status sync");
-    if (slow_items) *slow_items = hdr[0];
+    if (slow_items) *slow_items = hdr[0] + hdr[4];  // full evaluations + recomputations
     if (fault) *fault = hdr[3];
     if (hdr[3]) {
         snprintf(g_last_error, sizeof(g_last_error),
@@ -1230,10 +1233,12 @@ int hdr_lpa_workspace_status(const void *workspace, uint32_t *slow_items, uint32
 int hdr_lpa_slow_items(const void *workspace, uint32_t *count, void *stream) {
     if (!workspace || !count) return HDR_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemcpyAsync(count, workspace, sizeof(uint32_t), cudaMemcpyDeviceToHost, st) !=
-        cudaSuccess)
+    uint32_t hdr[WS_HEADER_WORDS];
+    if (cudaMemcpyAsync(hdr, workspace, sizeof(hdr), cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return HDR_ERR_CUDA;
-    return cudaStreamSynchronize(st) == cudaSuccess ? HDR_OK : HDR_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return HDR_ERR_CUDA;
+    *count = hdr[0] + hdr[4];  // full evaluations + recomputations
+    return HDR_OK;
 }
 
 }  // extern "C"

@@ -138,6 +138,9 @@ int launch_all(const DevParams &Pf, const DevParams &P, const TapParam &T, int t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     COUNT_LAUNCH();
+    lpa_precise_kernel<ORDER><<<nsm * 4, 128, 0, st>>>(P);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_precise_kernel launch");
+    COUNT_LAUNCH();
     lpa_slow_kernel<ORDER><<<nsm * 4, 128, 0, st>>>(P);
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("lpa_slow_kernel launch");
     return HDR_OK;

@@ -148,6 +148,12 @@ struct DevParams {
     uint32_t *tile_counter;          // fast kernel: next tile to hand out (workspace header)
     uint32_t *slow_counter;          // exact path: next work item to evaluate
     uint32_t *fault;                 // HDR_FAULT_* bits raised by a kernel (workspace header)
+    // float64 recomputations of a fit whose fast-path decisions stood (kk > 0):
+    // enqueued from the END of work_items (slot item_cap - 1 - i) and evaluated
+    // by lpa_precise_kernel before lpa_slow_kernel takes the full evaluations
+    uint32_t *prec_count;            // workspace header word 4
+    uint32_t *prec_counter;          // word 5: next recomputation to evaluate
+    uint32_t item_cap;               // work_items capacity
     uint32_t all_items;              // > 0: no fast kernel; the exact path evaluates every
                                      // (pixel, channel) of the band (item i: pixel i / 3, channel i % 3)
     uint32_t *work_items;

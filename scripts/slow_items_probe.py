@@ -23,7 +23,13 @@ ow, oh = wl["out"]
 out = rig.reconstruct(wl["out"], p, ref_size=(W, H), want_scale_idx=True, want_outcome=True)
 n = rig.slow_items(wl["out"])
 ws = rig.workspace(ow, oh)
-items = ws[ws.numel() - ow * oh * 3 * 4:].view(torch.int32)[:n].cpu().numpy().astype("uint32")
+hdr = ws[:24].view(torch.int32).cpu().numpy().astype("uint32")  # header words 0..5
+all_items = ws[ws.numel() - ow * oh * 3 * 4:].view(torch.int32).cpu().numpy().astype("uint32")
+cap = ow * oh * 3
+back = all_items[cap - hdr[4]:][::-1]  # recomputation slots (after lpa_precise_kernel)
+print("full evaluations", hdr[0], "recomputations", hdr[4],
+      "of which failed -> full", int(((back != 0xFFFFFFFF) & (((back >> 2) & 15) == 0)).sum()))
+items = all_items[:hdr[0]]
 kk = (items >> 2) & 15
 ch = items & 3
 pix = items >> 6
