@@ -10,11 +10,20 @@ namespace hdrlpa {
 // Exact evaluation (slow path): lpa_evaluate's ladder (_kernels.py:257-300)
 // and the ICI rule.
 // ---------------------------------------------------------------------------
+// skip0: the fast path decided (with certainty, solve_fast's FIT_FAIL) that
+// step 0 of this order is invalid -- start at step 1 with the same radius
+// sequence (r0, then min(1.5 r, max_radius))
 template <int ORDER, class Sweep>
-__device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+__device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, PixelResult &R,
+                             bool skip0 = false) {
     constexpr int PN = NC<ORDER>::P;
     double r = P.r[c][0];  // already min(r0, max_radius)
     int step = 0;
+    if (skip0) {
+        if (r >= P.max_radius * (1.0 - 1e-12)) return false;
+        r = fmin(r * 1.5, P.max_radius);
+        step = 1;
+    }
     Acc<PN> acc;
     for (;;) {
         accumulate<ORDER, true>(P, c, 0, r, __dmul_rn(r, r), sweep, acc);
@@ -35,9 +44,10 @@ __device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, Pixe
 }
 
 template <int ORDER, class Sweep>
-__device__ void ladder(const DevParams &P, int c, const Sweep &sweep, PixelResult &R) {
+__device__ void ladder(const DevParams &P, int c, const Sweep &sweep, PixelResult &R,
+                       bool skip0 = false) {
     R.sidx = 0;
-    if (ladder_order<ORDER>(P, c, sweep, R)) return;
+    if (ladder_order<ORDER>(P, c, sweep, R, skip0)) return;
     if constexpr (ORDER >= 1) {
         if (ladder_order<ORDER - 1>(P, c, sweep, R)) return;
     }
@@ -193,6 +203,9 @@ __device__ bool precise_fit(const DevParams &P, int c, int k, const Sweep &sweep
 #define SLOW_LANES_O2 4
 #endif
 constexpr uint32_t ITEM_DONE = 0xffffffffu;  // a recomputation that succeeded
+// work-item kk code: scale 0 / the fixed scale certainly invalid (solve_fast's
+// FIT_FAIL), the exact path runs the ladder from step 1
+constexpr uint32_t KK_LADDER = 15u;
 
 // The recomputations (kk > 0, from the end of the item list) in a kernel of
 // their own: a small, uniform code path (one float64 fit at the selected
@@ -252,7 +265,9 @@ __global__ void __launch_bounds__(128) lpa_slow_kernel(const __grid_constant__ D
         const int ox = pix % P.out_w, oy = pix / P.out_w;
         const GlobalSweep<G> sweep{P, qcoord(ox, P.sx), qcoord(oy, P.sy)};
         PixelResult R;
-        if (kk && precise_fit<ORDER>(P, c, kk - 1, sweep, R)) {
+        if (kk == (int)KK_LADDER) {
+            ladder<ORDER>(P, c, sweep, R, true);
+        } else if (kk && precise_fit<ORDER>(P, c, kk - 1, sweep, R)) {
             // the fast path's decisions stand; only the value was recomputed
         } else if (P.n_scales > 1) {
             if (ici<ORDER, true>(P, c, sweep, R) != FIT_OK) ladder<ORDER>(P, c, sweep, R);

@@ -364,10 +364,14 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
         } else {
             // work item: band-relative pixel | kk | channel, kk = 0: full exact
             // evaluation, kk = k + 1: float64 recomputation of the fit at scale k
-            const uint32_t kk = st == FIT_PREC ? (uint32_t)R.sidx + 1u : 0u;
+            // kk = KK_LADDER: scale 0 certainly invalid (the ladder from step 1;
+            // ICI kernels only -- the extra select cost the 64-register
+            // co-sited tap kernel 1.7 %)
+            const uint32_t kk = st == FIT_PREC ? (uint32_t)R.sidx + 1u
+                                               : (ICI && st == FIT_FAIL ? KK_LADDER : 0u);
             const uint32_t item =
                 ((uint32_t)(pix - P.row_begin * P.out_w) << 6) | (kk << 2) | (uint32_t)c;
-            if (kk)  // recomputations from the end of the list (lpa_precise_kernel)
+            if (kk && kk != KK_LADDER)  // recomputations from the end of the list (lpa_precise_kernel)
                 P.work_items[P.item_cap - 1u - atomicAdd(P.prec_count, 1u)] = item;
             else
                 P.work_items[atomicAdd(P.work_count, 1u)] = item;
