@@ -19,6 +19,33 @@ def _case():
     return frames, cfgs, cals, out_size, ap, arrays
 
 
+@pytest.mark.parametrize("window,nan_frac", [(5, 0.0), (9, 0.02), (71, 0.02)])
+def test_steering_field_windows_and_nans(cuda, window, nan_frac):
+    """The tiled steering-field kernel (windows whose neighbourhood fits shared
+    memory) and the per-pixel fallback (window 71) against the oracle, with
+    non-finite gradients skipped as the reference skips them
+    (_kernels.py:310-392); image edges inside every window."""
+    import dataclasses
+
+    rng = np.random.default_rng(window)
+    h, w = 61, 83
+    gx = (rng.standard_normal((h, w)) * 40).astype(np.float32)
+    gy = (rng.standard_normal((h, w)) * 40 + 10).astype(np.float32)
+    bad = rng.random((h, w)) < nan_frac
+    gx[bad] = np.nan
+    gy[rng.random((h, w)) < nan_frac / 2] = np.inf
+    frames, cfgs, cals, out_size, ap, arrays = _case()
+    ap = dataclasses.replace(ap, gradient_window=window)
+    scale = 7.5
+    th, sg, gm = oracle.steering_field(gx.astype(np.float64), gy.astype(np.float64), ap, scale)
+    f = hl.compute_steering_field((torch.from_numpy(gx).cuda(), torch.from_numpy(gy).cuda()),
+                                  ap, scale)
+    gth, gsg, ggm = f.numpy()
+    np.testing.assert_allclose(gsg, sg, rtol=1e-12)
+    np.testing.assert_allclose(ggm, gm, rtol=1e-12)
+    np.testing.assert_allclose(gth, th, rtol=1e-9, atol=1e-12)
+
+
 def test_steering_field_kernel_matches_oracle(cuda):
     frames, cfgs, cals, out_size, ap, arrays = _case()
     o = oracle.reconstruct(frames, cfgs, cals, out_size, ap.base, channels=(1,))
