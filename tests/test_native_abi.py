@@ -137,6 +137,20 @@ def test_singular_transform_is_a_configuration_error():
     assert rc == N.HDR_ERR_CONFIG
 
 
+def test_gradient_scale_argument_validation():
+    """hdr_gradient_scale rejects arguments before any device work (its
+    histogram counters are 32-bit: n < 2^32; q in [0, 1]; workspace size)."""
+    need = ctypes.c_size_t()
+    assert N.lib().hdr_gradient_scale_workspace_bytes(ctypes.byref(need)) == N.HDR_OK
+    L = N.lib()
+    assert L.hdr_gradient_scale(8192, 1 << 32, 0.995, 16384, 1 << 20, need.value, None) == \
+        N.HDR_ERR_ARG
+    assert L.hdr_gradient_scale(8192, 100, 1.5, 16384, 1 << 20, need.value, None) == N.HDR_ERR_ARG
+    assert L.hdr_gradient_scale(8192, -1, 0.5, 16384, 1 << 20, need.value, None) == N.HDR_ERR_ARG
+    assert L.hdr_gradient_scale(8192, 100, 0.5, 16384, 1 << 20, need.value - 1, None) == \
+        N.HDR_ERR_WORKSPACE
+
+
 def test_status_codes_map_to_reference_exceptions():
     import paper_1308_4908_b200 as hl
 
