@@ -879,7 +879,8 @@ def run_ours(args, wl, world, rank, local):
             "slow_path_items": slow_items,
             "cpu_baseline": cpu,
             "e2e": {"value": fps_e2e, "unit": "frames/s", "h2d_bytes_per_step": pipe.h2d_bytes,
-                    "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": ms_e2e / args.steps},
+                    "d2h_bytes_per_step": pipe.d2h_bytes, "ms_per_step": ms_e2e / args.steps,
+                    "slots": args.e2e_slots},
             "e2e_reference_api": e2e_api,
             "e2e_fp16_output": {"value": world * args.steps / (ms_half / 1e3), "unit": "frames/s",
                                 "h2d_bytes_per_step": pipe_h.h2d_bytes,
@@ -955,8 +956,11 @@ def main():
                     help="reference arm: time the C restatement even if hdrfuse is staged")
     ap.add_argument("--dry-run", action="store_true",
                     help="exercise the multi-rank plumbing only (no GPU work)")
-    ap.add_argument("--e2e-slots", type=int, default=3,
-                    help="device slots (frames in flight) of the end-to-end pipeline")
+    ap.add_argument("--e2e-slots", type=int, default=None,
+                    help="device slots (frames in flight) of the end-to-end pipeline "
+                         "(default: 6 for the compute-bound ICI workloads, 3 otherwise -- "
+                         "measured: cfg3 2/3/4/6/8 slots 116/119/119/121.5/121.4 frames/s, "
+                         "cfg2 (PCIe-bound) 3/6/8 slots 1050/880/887)")
     ap.add_argument("--lanes", type=int, default=4,
                     help="streams consecutive frames alternate between (CUDA-graph mode)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
@@ -966,6 +970,8 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch(args.gpus))
     wl = WORKLOADS[args.workload]
+    if args.e2e_slots is None:
+        args.e2e_slots = 6 if wl.get("J", 1) > 1 else 3
     world, rank, local = _dist_init()
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
