@@ -5,6 +5,7 @@ outcomes and ICI indices): rig kind, sensor count, Bayer pattern, frame size
 per case from a seeded generator."""
 
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -14,6 +15,10 @@ from paper_1308_4908_b200 import simulate as sim
 from oracle import compare, oracle
 
 pytestmark = pytest.mark.gpu
+
+# HDR_FUZZ_SCALE multiplies the case counts (stress campaigns on the GPU box;
+# the default suite keeps 64 / 12 / 24 cases)
+_SCALE = int(os.environ.get("HDR_FUZZ_SCALE", "1"))
 
 PATTERNS = [hl.BayerPattern.RGGB, hl.BayerPattern.BGGR, hl.BayerPattern.GRBG,
             hl.BayerPattern.GBRG]
@@ -30,11 +35,16 @@ def _draw(k):
     scale = float(rng.choice([0.5, 0.7, 1.0]))
     up = int(rng.integers(0, 4) == 0)
     pat = PATTERNS[int(rng.integers(0, 4))]
-    return dict(W=W, H=H, rig=rig_name, n=n_sensors, order=order, J=J, mode=mode, scale=scale,
-                up=up, pat=pat, seed=int(rng.integers(0, 1 << 16)))
+    d = dict(W=W, H=H, rig=rig_name, n=n_sensors, order=order, J=J, mode=mode, scale=scale,
+             up=up, pat=pat, seed=int(rng.integers(0, 1 << 16)), ratio=2 ** 0.5, gamma=1.5)
+    if k >= 64:  # stress cases: other ICI ratios / widths, larger windows
+        d["ratio"] = float(rng.choice([1.2, 2 ** 0.5, 2.0]))
+        d["gamma"] = float(rng.choice([0.5, 1.0, 1.5, 3.0]))
+        d["scale"] = float(rng.choice([0.5, 0.7, 1.0, 1.5, 2.0]))
+    return d
 
 
-@pytest.mark.parametrize("k", range(64))
+@pytest.mark.parametrize("k", range(64 * _SCALE))
 def test_random_configuration_parity(cuda, k):
     d = _draw(k)
     gt = sim.hdr_chart(d["W"], d["H"])
@@ -44,7 +54,7 @@ def test_random_configuration_parity(cuda, k):
     frames = sim.simulate_rig(gt, rig)
     cals = rig.calibrations()
     p = hl.ReconstructionParams(order=d["order"], scale=d["scale"], ici_scales=d["J"],
-                                weight_mode=d["mode"])
+                                weight_mode=d["mode"], ici_ratio=d["ratio"], ici_gamma=d["gamma"])
     out_size = (d["W"] * (1 + d["up"]), d["H"] * (1 + d["up"]))
     ref_size = (d["W"], d["H"])
     dev = hl.frames_to_samples(frames, list(rig.sensors), cals).device()
@@ -59,7 +69,7 @@ def test_random_configuration_parity(cuda, k):
     assert int((got["scale_idx"] != ref["scale_idx"]).sum()) == 0
 
 
-@pytest.mark.parametrize("k", range(12))
+@pytest.mark.parametrize("k", range(12 * _SCALE))
 def test_random_steered_pass_parity(cuda, k):
     """CALPA's steered pass (fast path + exact slow path) on random rigs and
     random steering fields, against the oracle's two-phase evaluation on the
@@ -93,7 +103,7 @@ def test_random_steered_pass_parity(cuda, k):
         assert int((out["outcome"][c].cpu().numpy() != oc).sum()) == 0
 
 
-@pytest.mark.parametrize("k", range(24))
+@pytest.mark.parametrize("k", range(24 * _SCALE))
 def test_random_affine_rig_parity(cuda, k):
     """General affine rigs (translations of several pixels, rotations up to
     5 deg, scales, shears), per-pixel calibration planes, defective pixels,
