@@ -146,11 +146,11 @@ def reconstruct_frame(samples, out_size, params: ReconstructionParams, ref_size=
             planes.append(torch.clamp_min(val, 0.0).to(torch.float32))  # keeps NaN (lpa.py:428)
             if return_gradients:
                 grads[ch] = (to_host(gx), to_host(gy))
-        img = HDRImage(to_host(torch.stack(planes, 2)))
+        img = HDRImage._from_device_output(to_host(torch.stack(planes, 2)))
         return (img, grads) if return_gradients else img
     rig = _device_rig(samples)
     out = rig.reconstruct(out_size, params, ref_size=ref_size, want_grad=return_gradients)
-    img = HDRImage(to_host(out["rgb"]))
+    img = HDRImage._from_device_output(to_host(out["rgb"]))
     rig.status(out_size)  # synchronous API: surface a kernel fault (after the sync above)
     if not return_gradients:
         return img

@@ -203,7 +203,7 @@ def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
     if params.share_steering:
         sc = CalpaScratch(rig, out_size)
         out = calpa_device(rig, out_size, params, ref_size=ref_size, scratch=sc)
-        img = HDRImage(to_host(out["rgb"]))
+        img = HDRImage._from_device_output(to_host(out["rgb"]))
         fld = sc.field
     else:
         out_w, out_h = out_size
@@ -214,7 +214,7 @@ def calpa_reconstruct(samples, out_size, params: AdaptiveParams, ref_size=None,
             o = rig.reconstruct_steered(out_size, base, (f.theta, f.sigma, f.gamma),
                                         ref_size=ref_size)
             planes[:, :, int(ch)] = to_host(o["rgb"][:, :, int(ch)])
-        img = HDRImage(planes)
+        img = HDRImage._from_device_output(planes)
     if return_field:
         return img, fld
     return img

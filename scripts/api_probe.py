@@ -27,10 +27,16 @@ for it in range(6):
     out = dev.reconstruct(wl["out"], params, ref_size=(W, H))
     torch.cuda.synchronize()
     t.append(time.perf_counter())
-    img = hl.HDRImage(to_host(out["rgb"]))
+    img = hl.HDRImage._from_device_output(to_host(out["rgb"]))
     t.append(time.perf_counter())
     dev.status(wl["out"])
     t.append(time.perf_counter())
     d = [f"{(b - a) * 1e3:.2f}" for a, b in zip(t, t[1:])]
     print("frames_to_samples / device() / reconstruct / to_host / status ms:", d,
           f"total {(t[-1] - t[0]) * 1e3:.1f}")
+
+for it in range(4):  # the whole public call
+    t0 = time.perf_counter()
+    img = hl.reconstruct_frame(hl.frames_to_samples(frames, rig.sensors, cals), wl["out"], params,
+                               ref_size=(W, H))
+    print(f"reconstruct_frame(frames_to_samples(...)) {(time.perf_counter() - t0) * 1e3:.1f} ms")
