@@ -70,6 +70,11 @@ extern "C" {
  * transform, frame size and Bayer phase) would be merged into one sample per
  * position (A/B comparisons of the two tap kernels). */
 #define HDR_FLAG_NO_MERGE 2
+/* SKIP_R / SKIP_G / SKIP_B leave a channel out (its output planes are not
+ * written): CALPA's first pass needs the G channel only (steering.py:214-248). */
+#define HDR_FLAG_SKIP_R 4
+#define HDR_FLAG_SKIP_G 8
+#define HDR_FLAG_SKIP_B 16
 
 /* Outcome plane codes (optional diagnostics): order*16 + radius-step of the
  * accepted fit (radius step 0 = base radius), or HDR_OUTCOME_NAN. */

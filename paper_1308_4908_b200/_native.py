@@ -33,6 +33,9 @@ HDR_WEIGHT_VARIANCE, HDR_WEIGHT_SIGMA = 0, 1
 HDR_OUTCOME_NAN = 0xFF
 HDR_FLAG_FAST_ONLY = 1
 HDR_FLAG_NO_MERGE = 2
+HDR_FLAG_SKIP_R = 4
+HDR_FLAG_SKIP_G = 8
+HDR_FLAG_SKIP_B = 16
 
 EXPORTED = (
     "hdr_lpa_workspace_bytes",

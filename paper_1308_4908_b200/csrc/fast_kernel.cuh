@@ -290,6 +290,7 @@ __device__ __forceinline__ void tile_compute(const DevParams &P, const unsigned 
     if constexpr (STEER)
         if (covered) sp = steer_pixel(P, pix);
     for (int c = 0; c < 3; ++c) {
+        if ((P.flags >> (2 + c)) & 1) continue;  // HDR_FLAG_SKIP_R/G/B
         PixelResult R;
         R.sidx = 0;
         int st = FIT_AMBIG;

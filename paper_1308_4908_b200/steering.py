@@ -176,7 +176,10 @@ def calpa_device(rig, out_size, params: AdaptiveParams, ref_size=None, out=None,
         raise ValueError("calpa_device implements the shared-steering mode")
     base = params.base
     sc = scratch if scratch is not None else CalpaScratch(rig, out_size)
-    rig.reconstruct(out_size, base, ref_size=ref_size, out=sc.first)
+    # the isotropic pass of the G channel only (steering.py:214-248 steers every
+    # channel with the G field): R and B left out of the tile kernel
+    rig.reconstruct(out_size, base, ref_size=ref_size, out=sc.first,
+                    flags=N.HDR_FLAG_SKIP_R | N.HDR_FLAG_SKIP_B)
     g = int(ColorChannel.G)
     grads = (sc.first["grad"][g, 0], sc.first["grad"][g, 1])
     if params.gradient_scale:
