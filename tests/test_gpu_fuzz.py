@@ -108,6 +108,22 @@ def test_random_affine_rig_parity(cuda, k):
     """General affine rigs (translations of several pixels, rotations up to
     5 deg, scales, shears), per-pixel calibration planes, defective pixels,
     mixed exposure scalings and sensor sizes, 16-bit sensors."""
+    frames, sensors, cals, p, W, H, n, bit16 = affine_case(k)
+    dev = hl.frames_to_samples(frames, sensors, cals).device()
+    out = dev.reconstruct((W, H), p, want_scale_idx=True, want_outcome=True)
+    got = {kk: v.cpu().numpy() for kk, v in out.items()}
+    ref = oracle.reconstruct(frames, sensors, cals, (W, H), p)
+    s = compare.summary(got["rgb"], ref["rgb"])
+    print(k, n, bit16, p, s)
+    assert s["nan_map_equal"], s
+    assert s["frac_over"] == 0 and s["max"] <= 1e-4, s
+    assert int((got["outcome"] != ref["outcome"]).sum()) == 0
+    assert int((got["scale_idx"] != ref["scale_idx"]).sum()) == 0
+
+
+def affine_case(k):
+    """The random affine rig of case k (frames, sensors, calibrations, params,
+    W, H, sensor count, 16-bit flag)."""
     rng = np.random.default_rng(9000 + k)
     W, H = int(rng.integers(48, 110)), int(rng.integers(40, 90))
     n = int(rng.integers(2, 5))
@@ -145,16 +161,7 @@ def test_random_affine_rig_parity(cuda, k):
             nonuniformity=hl.FloatFrame(rng.uniform(0.97, 1.03, c0.shape)))
     p = hl.ReconstructionParams(order=int(rng.integers(0, 3)), scale=float(rng.choice([0.5, 0.7, 1.2])),
                                 ici_scales=int(rng.choice([1, 3])))
-    dev = hl.frames_to_samples(frames, sensors, cals).device()
-    out = dev.reconstruct((W, H), p, want_scale_idx=True, want_outcome=True)
-    got = {kk: v.cpu().numpy() for kk, v in out.items()}
-    ref = oracle.reconstruct(frames, sensors, cals, (W, H), p)
-    s = compare.summary(got["rgb"], ref["rgb"])
-    print(k, n, bit16, p, s)
-    assert s["nan_map_equal"], s
-    assert s["frac_over"] == 0 and s["max"] <= 1e-4, s
-    assert int((got["outcome"] != ref["outcome"]).sum()) == 0
-    assert int((got["scale_idx"] != ref["scale_idx"]).sum()) == 0
+    return frames, sensors, cals, p, W, H, n, bit16
 
 
 @pytest.mark.parametrize("order", [1, 2])
