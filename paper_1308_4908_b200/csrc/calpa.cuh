@@ -191,7 +191,10 @@ __device__ bool steered_order(const DevParams &P, int c, const Sweep &sweep, con
             accumulate_hinv<ORDER>(sweep, c, h11, h12, h22, r, __dmul_rn(r, r), acc);
             R.work += acc.count;
             Fit fit;
-            if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
+            int st = solve_exact<PN>(acc, P.cond, fit);
+            if (st == FIT_CRITICAL)  // the reference's order (exact_ref.cuh)
+                st = settle_critical<ORDER>(P, c, sweep.qx, sweep.qy, h11, h12, h22, r, fit);
+            if (st == FIT_OK) {
                 R.count = acc.count;
                 R.val = fit.c0;
                 R.gx = ORDER >= 1 ? fit.c1 : qnan();

@@ -2,7 +2,7 @@
 // float64 recomputation, and lpa_slow_kernel over the fast path's work list.
 #pragma once
 
-#include "sweeps.cuh"
+#include "exact_ref.cuh"
 
 namespace hdrlpa {
 
@@ -29,7 +29,11 @@ __device__ bool ladder_order(const DevParams &P, int c, const Sweep &sweep, Pixe
         accumulate<ORDER, true>(P, c, 0, r, __dmul_rn(r, r), sweep, acc);
         R.work += acc.count;
         Fit fit;
-        if (solve_exact<PN>(acc, P.cond, fit) == FIT_OK) {
+        int st = solve_exact<PN>(acc, P.cond, fit);
+        if (st == FIT_CRITICAL)  // the reference's closed form decides on noise: its order
+            st = settle_critical<ORDER>(P, c, sweep.qx, sweep.qy, P.hinv[c][0], 0.0,
+                                        P.hinv[c][0], r, fit);
+        if (st == FIT_OK) {
             R.count = acc.count;
             R.val = fit.c0;
             R.gx = ORDER >= 1 ? fit.c1 : qnan();
@@ -97,7 +101,12 @@ __device__ int ici(const DevParams &P, int c, const Sweep &sweep, PixelResult &R
     for (; k < P.n_scales; ++k) {
         if constexpr (!FUSED) accumulate<ORDER, EXACT>(P, c, k, P.r[c][k], P.r2[c][k], sweep, acc);
         R.work += acc.count;
-        const int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
+        int st = EXACT ? solve_exact<PN>(acc, P.cond, fit) : solve_fast<PN>(acc, P.cond, fit);
+        if constexpr (EXACT) {
+            if (st == FIT_CRITICAL)
+                st = settle_critical<ORDER>(P, c, sweep.qx, sweep.qy, P.hinv[c][k], 0.0,
+                                            P.hinv[c][k], P.r[c][k], fit);
+        }
         if (st == FIT_AMBIG) return FIT_AMBIG;
         if (st != FIT_OK) {
             if (k == 0) return FIT_FAIL;

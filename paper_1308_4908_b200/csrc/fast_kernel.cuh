@@ -171,29 +171,33 @@ template <int ORDER>
 struct RowAniso {
     static constexpr int PN = NC<ORDER>::P;
     RowMoments<ORDER> m;
-    float h11, h12x2, h22;  // pre-scaled by log2(e)
-    float a, b;             // per row: h22 dy^2, 2 h12 dy
+    // pre-scaled by log2(e).  q is formed in float64: a strongly anisotropic
+    // window's terms h11 dx^2, 2 h12 dx dy, h22 dy^2 cancel, and an fp32 sum
+    // of them left weight errors far beyond FAST_EPS (1.4e-4 relative on a
+    // sigma = 20 field in the stress fuzz); only the sum is rounded to fp32
+    double h11, h12x2, h22;
+    double a, b;  // per row: h22 dy^2, 2 h12 dy
     __device__ __forceinline__ void begin_row(double dy, double dyy) {
         m.begin_row(dy, dyy);
-        a = h22 * (float)dyy;
-        b = h12x2 * (float)dy;
+        a = h22 * dyy;
+        b = h12x2 * dy;
     }
     __device__ __forceinline__ void end_row(double dy, double dyy) { m.end_row(dy, dyy); }
     __device__ __forceinline__ void sample(bool ok, double v, float iv, double dx, double dy,
                                            double dxx, double dyy, float, bool = true) {
-        const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
+        const float q2 = (float)fma(h11, dxx, fma(b, dx, a));
         // RowMoments' weight is ex2(-hl * d2f) * iv: feed it q2 with hl = 1
         m.sample(ok, v, iv, dx, dy, dxx, dyy, q2);
     }
     __device__ __forceinline__ void sample4(bool ok, float4 e, double dx, double dy, double dxx,
                                             double dyy, float) {
-        const float q2 = fmaf(h11, (float)dxx, fmaf(b, (float)dx, a));
+        const float q2 = (float)fma(h11, dxx, fma(b, dx, a));
         m.sample4(ok, e, dx, dxx, ex2_approx(-q2));
     }
     template <bool CNT = true>
     __device__ __forceinline__ void general(bool ok, double v, float iv, double dx, double dy,
                                             double dxx, double dyy, float, bool = true) {
-        const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+        const float q2 = (float)fma(h11, dxx, fma(h12x2, dx * dy, h22 * dyy));
         m.template general<CNT>(ok, v, iv, dx, dy, dxx, dyy, q2);
     }
     __device__ __forceinline__ void count_add(int n) { m.count_add(n); }
@@ -202,16 +206,16 @@ struct RowAniso {
 template <int ORDER, class Sweep>
 __device__ __forceinline__ void accumulate_aniso(const Sweep &sweep, int c, const double *an,
                                                  double r, double r2, Acc<NC<ORDER>::P> &acc) {
-    constexpr float L2E = 1.4426950408889634f;
+    constexpr double L2E = 1.4426950408889634;
     acc.zero();
-    const float h11 = (float)an[0] * L2E, h12x2 = 2.f * (float)an[1] * L2E, h22 = (float)an[2] * L2E;
+    const double h11 = an[0] * L2E, h12x2 = 2.0 * an[1] * L2E, h22 = an[2] * L2E;
     if constexpr (ORDER >= 1) {
-        RowAniso<ORDER> pol{RowMoments<ORDER>{acc, 1.0f}, h11, h12x2, h22, 0.f, 0.f};
+        RowAniso<ORDER> pol{RowMoments<ORDER>{acc, 1.0f}, h11, h12x2, h22, 0.0, 0.0};
         sweep.rows(c, -1, r, r2, pol);
     } else {
         sweep(c, -1, r, r2, [&](bool ok, double v, float iv, double dx, double dy, double dxx,
                                 double dyy, float) {
-            const float q2 = fmaf(h11, (float)dxx, fmaf(h12x2, (float)(dx * dy), h22 * (float)dyy));
+            const float q2 = (float)fma(h11, dxx, fma(h12x2, dx * dy, h22 * dyy));
             const float w = ok ? ex2_approx(-q2) * iv : 0.f;
             const double y = ok ? v : 0.0;
             acc.sabs = fmaf(w, fabsf((float)y), acc.sabs);

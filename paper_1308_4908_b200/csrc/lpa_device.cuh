@@ -28,6 +28,15 @@ constexpr int FIT_OK = 0;
 constexpr int FIT_FAIL = 1;   // TOO_FEW / ILL_CONDITIONED (decided)
 constexpr int FIT_AMBIG = 2;  // condition number too close to the threshold to decide from bounds
 constexpr int FIT_PREC = 3;   // decisions sound, value needs the float64 recomputation (fit_precise)
+// exact path, p = 3: the reference's closed-form eigenvalue range decides on
+// rounding noise (near-singular window, or cond within reach of the
+// threshold): settled by a reference-order re-evaluation (exact_ref.cuh)
+constexpr int FIT_CRITICAL = 4;
+// p = 3 windows whose condition number may exceed CLOSED_FORM_SAFE * threshold
+// are not decided from bounds: the closed form's lambda_min carries an
+// absolute error up to ~1e-8 lambda_max on near-degenerate windows, so only
+// cond < 0.1 threshold is certainly accepted by it as well
+constexpr double CLOSED_FORM_SAFE = 0.1;
 
 struct DevSensor {
     const uint16_t *raw;
@@ -581,7 +590,9 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         const double C00 = fma(d, f, -e * e), C01 = fma(cc, e, -b * f), C02 = fma(b, e, -cc * d);
         const double C11 = fma(a, f, -cc * cc), C12 = fma(b, cc, -a * e), C22 = fma(a, d, -b * b);
         const double det = fma(a, C00, fma(b, C01, cc * C02));
-        if (!(a > 0.0) || !(C22 > 0.0) || !(det > 0.0)) return FIT_FAIL;
+        // not positive definite in float64 (count >= 3): a near-singular window,
+        // on which the reference's closed form decides on rounding noise
+        if (!(a > 0.0) || !(C22 > 0.0) || !(det > 0.0)) return FIT_AMBIG;
         // The cofactors are differences of products: near-singular windows
         // (e.g. coincident samples of identical sensors at a frame corner) leave
         // them at rounding-noise level, where their ratios are meaningless.  A
@@ -606,11 +617,10 @@ __device__ __forceinline__ int solve_fast(const Acc<P> &acc, double cond, Fit &f
         fit.g[2] = C02 * rd;
         const double cu = (a + d + f) * ((C00 + C11 + C22) * rd);
         if (!(cu >= 9.0 * (1.0 - 1e-6))) return FIT_AMBIG;  // tr A tr A^-1 >= p^2 always
-        const double margin = 1e-5;  // >> relative eigenvalue perturbation of fp32 weights
-        if (cu <= cond * (1.0 - margin)) return FIT_OK;
-        // the lower bound only for windows the upper one does not clear
-        const double cl = fmax(a, fmax(d, f)) * (fmax(C00, fmax(C11, C22)) * rd);
-        if (cl >= cond * (1.0 + margin)) return FIT_FAIL;
+        // accepted only where the reference's closed form certainly accepts
+        // too (cond < CLOSED_FORM_SAFE threshold; the fp32 weights move cond
+        // by ~1e-6 relative); everything else is decided by the exact path
+        if (cu <= cond * CLOSED_FORM_SAFE) return FIT_OK;
         return FIT_AMBIG;
     } else {
         double A[P * (P + 1) / 2], L[P * (P + 1) / 2], inv[P];
@@ -657,6 +667,41 @@ __device__ __forceinline__ bool fit_precise_sharp(double c0, float T, double flo
 // ---------------------------------------------------------------------------
 // Exact eigenvalue range for the slow path (_kernels.py:26-73)
 // ---------------------------------------------------------------------------
+// _chol_solve (_kernels.py:76-101) in the reference's operation order
+template <int P>
+__device__ bool chol_solve_ref(const double (&A)[6][6], const double *b, double *coef) {
+    double L[6][6], work[6];
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double s = A[i][j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(L[i][k], L[j][k]));
+            if (i == j) {
+                if (s <= 0.0) return false;
+                L[i][i] = __dsqrt_rn(s);
+            } else {
+                L[i][j] = __ddiv_rn(s, L[j][j]);
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        double s = b[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = __dsub_rn(s, __dmul_rn(L[i][k], work[k]));
+        work[i] = __ddiv_rn(s, L[i][i]);
+    }
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+        double s = work[i];
+#pragma unroll
+        for (int k = i + 1; k < P; ++k) s = __dsub_rn(s, __dmul_rn(L[k][i], coef[k]));
+        coef[i] = __ddiv_rn(s, L[i][i]);
+    }
+    return true;
+}
+
 // p == 3: the reference's trigonometric closed form, same operation order
 __device__ __forceinline__ void eig_range3(const double *A, double &lmin, double &lmax) {
     const double a11 = A[uidx<3>(0, 0)], a22 = A[uidx<3>(1, 1)], a33 = A[uidx<3>(2, 2)];
@@ -684,6 +729,38 @@ __device__ __forceinline__ void eig_range3(const double *A, double &lmin, double
     const double tp = __dmul_rn(2.0, pp);
     lmax = __dadd_rn(q, __dmul_rn(tp, cos(phi)));
     lmin = __dadd_rn(q, __dmul_rn(tp, cos(__dadd_rn(phi, 2.0943951023931953))));  // 2.0 * math.pi / 3.0
+}
+
+// eig_range3 plus a bound `err` on how far the reference's closed form could
+// move lambda_min / lambda_max given last-bit differences of A (summation
+// order) and of libm: the argument r of acos carries an error dr <= 1e-14,
+// and d acos / dr = 1 / sqrt(1 - r^2) blows up on near-degenerate windows
+// (two eigenvalues close, r -> +-1), where the eigenvalues move by up to
+// 2 p dr / (3 sqrt(1 - r^2)) -- ~1e-8 lambda_max at r = 1.
+// lmin_cap: the largest lambda_min the closed form can return whatever the
+// rounding of its acos argument (phi >= 0, so cos(phi + 2 pi / 3) <= -1/2:
+// lambda_min <= q - p), which keeps rank-deficient windows certainly rejected.
+__device__ __forceinline__ void eig_range3_err(const double *A, double &lmin, double &lmax,
+                                               double &err, double &lmin_cap) {
+    eig_range3(A, lmin, lmax);
+    const double a11 = A[uidx<3>(0, 0)], a22 = A[uidx<3>(1, 1)], a33 = A[uidx<3>(2, 2)];
+    const double a12 = A[uidx<3>(0, 1)], a13 = A[uidx<3>(0, 2)], a23 = A[uidx<3>(1, 2)];
+    const double q = (a11 + a22 + a33) / 3.0;
+    const double e1 = a11 - q, e2 = a22 - q, e3 = a33 - q;
+    const double p2 = e1 * e1 + e2 * e2 + e3 * e3 + 2.0 * (a12 * a12 + a13 * a13 + a23 * a23);
+    const double pp = sqrt(p2 / 6.0);
+    constexpr double dr = 1e-14;
+    double r = 0.0;
+    if (pp > 0.0) {
+        const double b11 = e1 / pp, b22 = e2 / pp, b33 = e3 / pp;
+        const double b12 = a12 / pp, b13 = a13 / pp, b23 = a23 / pp;
+        r = 0.5 * (b11 * (b22 * b33 - b23 * b23) - b12 * (b12 * b33 - b23 * b13) +
+                   b13 * (b12 * b23 - b22 * b13));
+    }
+    const double s2 = fmax(1.0 - r * r, dr);
+    const double round_q = 1e-14 * (fabs(a11) + fabs(a22) + fabs(a33));
+    err = 2.0 * pp * dr / (3.0 * sqrt(s2)) + round_q;
+    lmin_cap = q - pp + round_q;
 }
 
 // p == 6: cyclic Jacobi (the reference calls LAPACK dsyevd, _kernels.py:72)
@@ -733,6 +810,39 @@ static __device__ __noinline__ void eig_range6(const double *A, double &lmin, do
     }
 }
 
+// _fit_at's decision and solve (_kernels.py:184-199) on upper-triangle sums
+// accumulated in the reference's order: count < p, A00 <= 0 (p == 1), the
+// eigenvalue-range test (closed form for p == 3, Jacobi for p == 6), then
+// _chol_solve.  Shared by the scattered-sample kernel and the exact path's
+// reference-order re-evaluation (exact_ref.cuh).
+template <int P>
+__device__ __forceinline__ int ref_decide(double (&A)[6][6], const double *rhs, int count,
+                                          double cond, double *coef) {
+    if (count < P) return FIT_FAIL;
+#pragma unroll
+    for (int a = 0; a < P; ++a)
+#pragma unroll
+        for (int b = a + 1; b < P; ++b) A[b][a] = A[a][b];
+    if constexpr (P == 1) {
+        if (A[0][0] <= 0.0) return FIT_FAIL;
+        coef[0] = __ddiv_rn(rhs[0], A[0][0]);
+        return FIT_OK;
+    } else {
+        double packedA[P * (P + 1) / 2], lmin, lmax;
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < P; ++a)
+#pragma unroll
+            for (int b = a; b < P; ++b) packedA[k++] = A[a][b];
+        if constexpr (P == 3)
+            eig_range3(packedA, lmin, lmax);
+        else
+            eig_range6(packedA, lmin, lmax);
+        if (lmin <= 0.0 || lmax > cond * lmin) return FIT_FAIL;
+        return chol_solve_ref<P>(A, rhs, coef) ? FIT_OK : FIT_FAIL;
+    }
+}
+
 // Exact decision (slow path), mirroring _fit_at's tail (_kernels.py:184-200).
 template <int P>
 __device__ __forceinline__ int solve_exact(const Acc<P> &acc, double cond, Fit &fit) {
@@ -751,6 +861,28 @@ __device__ __forceinline__ int solve_exact(const Acc<P> &acc, double cond, Fit &
         // reference's eigenvalues'); only the rest pays for the eigenvalues.
         double A[P * (P + 1) / 2], L[P * (P + 1) / 2], inv[P];
         acc.fill_A(A);
+        if constexpr (P == 3) {
+            // the reference's closed form (_kernels.py:38-71) decides; where its
+            // rounding could land on either side of the threshold, the
+            // reference-order re-evaluation does (FIT_CRITICAL, exact_ref.cuh).
+            // cond <= CLOSED_FORM_SAFE threshold (the bound tr A tr A^-1) is
+            // accepted by the closed form whatever its rounding.
+            if (cholesky<P>(A, L, inv)) {
+                double cu, cl;
+                chol_finish<P>(A, acc.b, L, inv, fit, cu, cl);
+                if (cu <= cond * CLOSED_FORM_SAFE) return FIT_OK;
+            }
+            double lmin, lmax, err, cap;
+            eig_range3_err(A, lmin, lmax, err, cap);
+            const double lo = lmin - err, hi = fmin(lmin + err, cap);
+            if (hi <= 0.0 || lmax - err > cond * hi) return FIT_FAIL;
+            if (!(lo > 0.0 && lmax + err <= cond * lo)) return FIT_CRITICAL;
+            // cond <= threshold: the reference's _chol_solve succeeds
+            if (!cholesky<P>(A, L, inv)) return FIT_CRITICAL;
+            double cu, cl;
+            chol_finish<P>(A, acc.b, L, inv, fit, cu, cl);
+            return FIT_OK;
+        }
         if (!cholesky<P>(A, L, inv)) return FIT_FAIL;
         double cu, cl;
         chol_finish<P>(A, acc.b, L, inv, fit, cu, cl);

@@ -26,40 +26,6 @@ struct CsrQuery {
     double *val, *gx, *gy;
 };
 
-template <int P>
-__device__ bool chol_solve_ref(const double (&A)[6][6], const double *b, double *coef) {
-    double L[6][6], work[6];
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int j = 0; j <= i; ++j) {
-            double s = A[i][j];
-#pragma unroll
-            for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(L[i][k], L[j][k]));
-            if (i == j) {
-                if (s <= 0.0) return false;
-                L[i][i] = __dsqrt_rn(s);
-            } else {
-                L[i][j] = __ddiv_rn(s, L[j][j]);
-            }
-        }
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-        double s = b[i];
-#pragma unroll
-        for (int k = 0; k < i; ++k) s = __dsub_rn(s, __dmul_rn(L[i][k], work[k]));
-        work[i] = __ddiv_rn(s, L[i][i]);
-    }
-#pragma unroll
-    for (int i = P - 1; i >= 0; --i) {
-        double s = work[i];
-#pragma unroll
-        for (int k = i + 1; k < P; ++k) s = __dsub_rn(s, __dmul_rn(L[k][i], coef[k]));
-        coef[i] = __ddiv_rn(s, L[i][i]);
-    }
-    return true;
-}
-
 // _fit_at (_kernels.py:104-200) over the CSR index
 template <int ORDER>
 __device__ int csr_fit_at(const CsrIndex &ix, double qx, double qy, double h11, double h12,
@@ -120,29 +86,7 @@ __device__ int csr_fit_at(const CsrIndex &ix, double qx, double qy, double h11, 
             }
         }
     }
-    if (count < P) return FIT_FAIL;
-#pragma unroll
-    for (int a = 0; a < P; ++a)
-#pragma unroll
-        for (int b = a + 1; b < P; ++b) A[b][a] = A[a][b];
-    if constexpr (P == 1) {
-        if (A[0][0] <= 0.0) return FIT_FAIL;
-        coef[0] = __ddiv_rn(rhs[0], A[0][0]);
-        return FIT_OK;
-    } else {
-        double packedA[P * (P + 1) / 2], lmin, lmax;
-        int k = 0;
-#pragma unroll
-        for (int a = 0; a < P; ++a)
-#pragma unroll
-            for (int b = a; b < P; ++b) packedA[k++] = A[a][b];
-        if constexpr (P == 3)
-            eig_range3(packedA, lmin, lmax);
-        else
-            eig_range6(packedA, lmin, lmax);
-        if (lmin <= 0.0 || lmax > cond * lmin) return FIT_FAIL;
-        return chol_solve_ref<P>(A, rhs, coef) ? FIT_OK : FIT_FAIL;
-    }
+    return ref_decide<P>(A, rhs, count, cond, coef);
 }
 
 template <int ORDER>
