@@ -136,9 +136,6 @@ __device__ __forceinline__ int settle_critical(const DevParams &P, int c, double
                                                double h11, double h12, double h22, double r,
                                                Fit &fit) {
     double coef[6], g[6];
-#ifdef HDR_EXP_NO_SETTLE
-    if (true) return FIT_FAIL;  // experiment: cost of the re-evaluation
-#endif
     if (ref_fit_at<ORDER>(P, c, qx, qy, h11, h12, h22, r, coef, g) != FIT_OK) return FIT_FAIL;
     fit.c0 = coef[0];
     fit.c1 = ORDER >= 1 ? coef[1] : 0.0;
