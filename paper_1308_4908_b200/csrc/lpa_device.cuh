@@ -733,13 +733,19 @@ __device__ __forceinline__ void eig_range3(const double *A, double &lmin, double
 
 // eig_range3 plus a bound `err` on how far the reference's closed form could
 // move lambda_min / lambda_max given last-bit differences of A (summation
-// order) and of libm: the argument r of acos carries an error dr <= 1e-14,
+// order) and of libm: the argument r of acos carries an error dr (HDR_CF_DR),
 // and d acos / dr = 1 / sqrt(1 - r^2) blows up on near-degenerate windows
 // (two eigenvalues close, r -> +-1), where the eigenvalues move by up to
 // 2 p dr / (3 sqrt(1 - r^2)) -- ~1e-8 lambda_max at r = 1.
 // lmin_cap: the largest lambda_min the closed form can return whatever the
 // rounding of its acos argument (phi >= 0, so cos(phi + 2 pi / 3) <= -1/2:
 // lambda_min <= q - p), which keeps rank-deficient windows certainly rejected.
+// dr: a bound on |r_reference - r_here| -- the sums differ by the summation
+// order (~count ulps worst case) and libm's last bits; r's sensitivity to
+// them is ~10x on these windows (lambda_max dominates, B = (A - qI)/p)
+#ifndef HDR_CF_DR
+#define HDR_CF_DR 1e-13
+#endif
 __device__ __forceinline__ void eig_range3_err(const double *A, double &lmin, double &lmax,
                                                double &err, double &lmin_cap) {
     eig_range3(A, lmin, lmax);
@@ -749,7 +755,7 @@ __device__ __forceinline__ void eig_range3_err(const double *A, double &lmin, do
     const double e1 = a11 - q, e2 = a22 - q, e3 = a33 - q;
     const double p2 = e1 * e1 + e2 * e2 + e3 * e3 + 2.0 * (a12 * a12 + a13 * a13 + a23 * a23);
     const double pp = sqrt(p2 / 6.0);
-    constexpr double dr = 1e-14;
+    constexpr double dr = HDR_CF_DR;
     double r = 0.0;
     if (pp > 0.0) {
         const double b11 = e1 / pp, b22 = e2 / pp, b33 = e3 / pp;
