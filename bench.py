@@ -708,11 +708,24 @@ def run_ours(args, wl, world, rank, local):
     # sweep it evaluated -- all ICI scales; the variance sweeps of ICI add
     # 2p+3 FP64 FLOP per inside sample per scale)
     cnt = rig.reconstruct((out_w, out_h), params, ref_size=(W, H), want_work=True,
-                          flags=N.HDR_FLAG_FAST_ONLY)
+                          want_scale_idx=True, flags=N.HDR_FLAG_FAST_ONLY)
     n_inside = float(cnt["work"].to(torch.int64).sum().item())
     p = wl["order"]
     per64 = FLOP64_PER_SAMPLE[p] + (2 * NC[p] + 3 if wl["J"] > 1 else 0)
-    flop64 = n_inside * per64
+    # plus the solves (SURVEY.md s8(d) "Other terms": Cholesky + substitution,
+    # ~2p^3/3 + 2p^2 FLOP each): one per scale the fast kernel evaluated --
+    # min(selected index + 2, J) under ICI (the scale that ended the search
+    # included), one otherwise; pixel-channels of the exact path (work 0 in a
+    # FAST_ONLY run) excluded
+    done = cnt["work"] > 0
+    if wl["J"] > 1:
+        ev = torch.clamp(cnt["scale_idx"].to(torch.int64) + 2, max=wl["J"])
+        n_solves = float(ev[done].sum().item())
+    else:
+        n_solves = float(done.sum().item())
+    pp = NC[p]
+    flop64_solve = n_solves * (2.0 * pp ** 3 / 3.0 + 2.0 * pp * pp) if p >= 1 else 0.0
+    flop64 = n_inside * per64 + flop64_solve
     flop32 = n_inside * FLOP32_PER_SAMPLE[p]
     peak64 = ctypes_probe(N, stream)
     fp32_peak = 148 * 128 * 2 * (clk["sm_max_mhz"] or 1965.0) * 1e6
@@ -866,6 +879,7 @@ def run_ours(args, wl, world, rank, local):
                          "fast_path_ms": ms_fastpath,
                          "cosited_merge": _cosited(rigspec.sensors, wl),
                          "inside_samples_per_launch": n_inside,
+                         "solves_per_launch": n_solves, "flop64_solves_per_launch": flop64_solve,
                          "flop64_per_launch": flop64, "flop32_per_launch": flop32,
                          "fp32": {"achieved_tflops": flop32 / (ms_fast * 1e-3) / 1e12,
                                   "peak_tflops": fp32_peak / 1e12,
