@@ -333,13 +333,16 @@ def run_next(args, wl, world, rank, local):
         calpa_device(rigs[0], out_size, ap, scratch=sc)  # the field of frame 0
         o = rigs[0].reconstruct_steered(out_size, ap.base, (sc.field.theta, sc.field.sigma,
                                                             sc.field.gamma), want_work=True)
-        n_inside = float(o["work"].to(torch.int64).sum().item())
+        work = o["work"]
         kname = "lpa_fast_kernel STEER (+ lpa_steered_slow_kernel)"
     else:  # same windows and samples as the raw-frame path: its work plane counts them
-        n_inside = float(rigs[0].reconstruct(out_size, params, want_work=True)["work"]
-                         .to(torch.int64).sum().item())
+        work = rigs[0].reconstruct(out_size, params, want_work=True)["work"]
         kname = "lpa_samples_kernel"
-    flop64 = n_inside * FLOP64_PER_SAMPLE[1]
+    n_inside = float(work.to(torch.int64).sum().item())
+    # plus one order-1 solve per evaluated pixel-channel (a lower bound: ladder
+    # steps solve again), 2p^3/3 + 2p^2 = 36 FLOP
+    n_solves = float((work > 0).sum().item())
+    flop64 = n_inside * FLOP64_PER_SAMPLE[1] + n_solves * 36.0
     peak64 = ctypes_probe(N, stream)
     traffic = None
     tpath = ROOT / "profiles" / "r02_traffic.json"
