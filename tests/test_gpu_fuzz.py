@@ -195,3 +195,15 @@ def test_cosited_steered_pass_merge_ab(cuda, order):
         s = compare.summary(rgb[:, :, c], np.maximum(val, 0.0).astype(np.float32))
         assert s["nan_map_equal"] and s["frac_over"] == 0 and s["max"] <= 1e-4, s
         assert int((a["outcome"][c].cpu().numpy() != oc).sum()) == 0
+
+
+@pytest.mark.parametrize("kind,k", [("steered", 80), ("affine", 219), ("affine", 379)])
+def test_razor_edge_order1_decisions(cuda, kind, k):
+    """Stress-campaign cases whose order-1 condition test sits where the
+    reference's closed-form eigenvalue range decides on rounding noise
+    (DESIGN.md s4): settled in the reference's own summation order
+    (exact_ref.cuh), outcomes and radiance equal to the oracle's."""
+    if kind == "steered":
+        test_random_steered_pass_parity(cuda, k)
+    else:
+        test_random_affine_rig_parity(cuda, k)
