@@ -197,12 +197,14 @@ def test_cosited_steered_pass_merge_ab(cuda, order):
         assert int((a["outcome"][c].cpu().numpy() != oc).sum()) == 0
 
 
-@pytest.mark.parametrize("kind,k", [("steered", 80), ("affine", 219), ("affine", 379)])
+@pytest.mark.parametrize("kind,k", [("steered", 80), ("affine", 219), ("affine", 379),
+                                    ("steered", 227)])
 def test_razor_edge_order1_decisions(cuda, kind, k):
-    """Stress-campaign cases whose order-1 condition test sits where the
+    """Stress-campaign cases: order-1 condition tests where the
     reference's closed-form eigenvalue range decides on rounding noise
-    (DESIGN.md s4): settled in the reference's own summation order
-    (exact_ref.cuh), outcomes and radiance equal to the oracle's."""
+    (80, 219, 379: settled in the reference's own summation order,
+    exact_ref.cuh), and a strongly anisotropic steered window whose fp32
+    quadratic form escaped the precision bound (227: float64 q)."""
     if kind == "steered":
         test_random_steered_pass_parity(cuda, k)
     else:
